@@ -1,0 +1,225 @@
+"""CPU oracle for the Chapter 5 agnostic SE path (arxiv/paper_1803_04880).
+
+TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  The product (``paper_1803_04880_b200``, ``libse.so``) never imports
+it, and it never imports the product.  See ``oracle/oracle.h`` for the
+readings and citations; this file only marshals numpy arrays through ctypes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboracle.so")
+SOURCES = ["dwt53.c", "aes128.c", "sha2.c", "protect.c"]
+
+MODE_BLOCK8 = 0
+MODE_FULL = 1
+FLAG_PUBLIC_PLAIN = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C11, -O2, no intrinsics)."""
+    srcs = [os.path.join(_HERE, s) for s in SOURCES]
+    hdr = os.path.join(_HERE, "oracle.h")
+    if not force and os.path.exists(LIB_PATH):
+        newest = max(os.path.getmtime(p) for p in srcs + [hdr])
+        if os.path.getmtime(LIB_PATH) >= newest:
+            return LIB_PATH
+    tmp = LIB_PATH + f".tmp{os.getpid()}"
+    cmd = ["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
+           "-o", tmp] + srcs
+    subprocess.check_call(cmd)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+_lib = None
+
+_u8p = C.POINTER(C.c_uint8)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_u64p = C.POINTER(C.c_uint64)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB_PATH)
+        u64, u32 = C.c_uint64, C.c_uint32
+        L.oracle_layout.argtypes = [u64, u32, u32, u32, _u64p]
+        L.oracle_lift_fwd_1d.argtypes = [_i32p, _i32p, C.c_int]
+        L.oracle_lift_inv_1d.argtypes = [_i32p, _i32p, C.c_int]
+        L.oracle_dwt_fwd.argtypes = [_u8p, u64, u32, u32, u32, _i32p]
+        L.oracle_dwt_inv.argtypes = [_i32p, u64, u32, u32, u32, _u8p]
+        L.oracle_dwt_inv.restype = C.c_int64
+        L.oracle_aes128_sbox.argtypes = [_u8p]
+        L.oracle_aes128_encrypt_block.argtypes = [_u8p, _u8p, _u8p]
+        L.oracle_aes128_ctr.argtypes = [_u8p, _u8p, u64, _u8p, _u8p, u64]
+        L.oracle_sha256.argtypes = [_u8p, u64, _u8p]
+        L.oracle_sha512.argtypes = [_u8p, u64, _u8p]
+        L.oracle_protect_range.argtypes = [u64, u32, u32, u32, u32, u64, _u8p, _u8p,
+                                           _u8p, _u8p, _u8p, _u8p, u64, u64]
+        L.oracle_recover_range.argtypes = [u64, u32, u32, u32, u32, u64, _u8p, _u8p,
+                                           _u8p, _u8p, _u8p, _u8p, _i64p, u64, u64]
+        L.oracle_dwt2_fwd_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
+        L.oracle_dwt2_inv_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
+        L.oracle_record_fields.argtypes = [u32, u32, C.c_int, _i32p, _i32p, _i32p, _i32p, _i32p]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def _u8(x) -> np.ndarray:
+    a = np.ascontiguousarray(np.frombuffer(bytes(x), dtype=np.uint8) if isinstance(x, (bytes, bytearray)) else x,
+                             dtype=np.uint8)
+    if a.size == 0:
+        a = np.zeros(1, dtype=np.uint8)[:0]
+    return a
+
+
+def layout(n_bytes: int, width: int, levels: int, mode: int = MODE_BLOCK8) -> dict:
+    out = np.zeros(8, dtype=np.uint64)
+    rc = lib().oracle_layout(n_bytes, width, levels, mode, _p(out, _u64p))
+    if rc:
+        raise ValueError(f"invalid geometry n={n_bytes} W={width} L={levels} mode={mode}")
+    keys = ["rows", "n_blocks", "a_bits", "b_bits", "c_bits", "a_bytes", "b_bytes", "c_bytes"]
+    return {k: int(v) for k, v in zip(keys, out)}
+
+
+def lift_fwd_1d(x) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.int32)
+    y = np.zeros_like(x)
+    lib().oracle_lift_fwd_1d(_p(x, _i32p), _p(y, _i32p), x.size)
+    return y
+
+
+def lift_inv_1d(y) -> np.ndarray:
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    x = np.zeros_like(y)
+    lib().oracle_lift_inv_1d(_p(y, _i32p), _p(x, _i32p), y.size)
+    return x
+
+
+def dwt2_fwd_region(a, levels: int) -> np.ndarray:
+    """In-place-style dyadic transform of a whole int32 2-D array (copy returned)."""
+    a = np.array(a, dtype=np.int32, order="C", copy=True)
+    lib().oracle_dwt2_fwd_region(_p(a, _i32p), a.shape[1], a.shape[0], a.shape[1], levels)
+    return a
+
+
+def dwt2_inv_region(a, levels: int) -> np.ndarray:
+    a = np.array(a, dtype=np.int32, order="C", copy=True)
+    lib().oracle_dwt2_inv_region(_p(a, _i32p), a.shape[1], a.shape[0], a.shape[1], levels)
+    return a
+
+
+def dwt_fwd(data, width: int, levels: int, mode: int = MODE_BLOCK8) -> np.ndarray:
+    d = _u8(data)
+    lay = layout(d.size, width, levels, mode)
+    coef = np.zeros((lay["rows"], width), dtype=np.int32)
+    buf = d if d.size else np.zeros(1, np.uint8)
+    rc = lib().oracle_dwt_fwd(_p(buf, _u8p), d.size, width, levels, mode, _p(coef, _i32p))
+    assert rc == 0
+    return coef
+
+
+def dwt_inv(coef, n_bytes: int, width: int, levels: int, mode: int = MODE_BLOCK8):
+    coef = np.ascontiguousarray(coef, dtype=np.int32)
+    out = np.zeros(max(n_bytes, 1), dtype=np.uint8)
+    bad = lib().oracle_dwt_inv(_p(coef, _i32p), n_bytes, width, levels, mode, _p(out, _u8p))
+    return out[:n_bytes], int(bad)
+
+
+def aes128_sbox() -> np.ndarray:
+    s = np.zeros(256, dtype=np.uint8)
+    lib().oracle_aes128_sbox(_p(s, _u8p))
+    return s
+
+
+def aes128_encrypt_block(key: bytes, block: bytes) -> bytes:
+    k, b = _u8(key), _u8(block)
+    out = np.zeros(16, dtype=np.uint8)
+    lib().oracle_aes128_encrypt_block(_p(k, _u8p), _p(b, _u8p), _p(out, _u8p))
+    return out.tobytes()
+
+
+def aes128_ctr(key: bytes, iv: bytes, data, ctr_offset: int = 0) -> np.ndarray:
+    k, v, d = _u8(key), _u8(iv), _u8(data)
+    out = np.zeros(max(d.size, 1), dtype=np.uint8)
+    buf = d if d.size else np.zeros(1, np.uint8)
+    lib().oracle_aes128_ctr(_p(k, _u8p), _p(v, _u8p), ctr_offset, _p(buf, _u8p), _p(out, _u8p), d.size)
+    return out[:d.size]
+
+
+def sha256(msg: bytes) -> bytes:
+    m = _u8(msg) if len(msg) else np.zeros(1, np.uint8)
+    out = np.zeros(32, dtype=np.uint8)
+    lib().oracle_sha256(_p(m, _u8p), len(msg), _p(out, _u8p))
+    return out.tobytes()
+
+
+def sha512(msg: bytes) -> bytes:
+    m = _u8(msg) if len(msg) else np.zeros(1, np.uint8)
+    out = np.zeros(64, dtype=np.uint8)
+    lib().oracle_sha512(_p(m, _u8p), len(msg), _p(out, _u8p))
+    return out.tobytes()
+
+
+def record_fields(levels: int, mode: int, stream: int):
+    arrs = [np.zeros(64, dtype=np.int32) for _ in range(5)]
+    n = lib().oracle_record_fields(levels, mode, stream, *[_p(a, _i32p) for a in arrs])
+    return [tuple(int(a[k]) for a in arrs) for k in range(n)]
+
+
+def _streams(lay):
+    return [np.zeros(max(lay[k], 1), dtype=np.uint8) for k in ("a_bytes", "b_bytes", "c_bytes")]
+
+
+def protect(data, width: int, levels: int, key: bytes, iv: bytes, mode: int = MODE_BLOCK8,
+            flags: int = 0, block_offset: int = 0, block_range=None, out=None):
+    """Returns (A', B', C') byte streams.  ``block_range=(b0, b1)`` processes
+    only those local blocks into ``out`` (or fresh zeroed streams)."""
+    d = _u8(data)
+    lay = layout(d.size, width, levels, mode)
+    a, b, c = out if out is not None else _streams(lay)
+    k, v = _u8(key), _u8(iv)
+    b0, b1 = block_range if block_range is not None else (0, lay["n_blocks"])
+    buf = d if d.size else np.zeros(1, np.uint8)
+    rc = lib().oracle_protect_range(d.size, width, levels, mode, flags, block_offset,
+                                    _p(k, _u8p), _p(v, _u8p), _p(buf, _u8p),
+                                    _p(a, _u8p), _p(b, _u8p), _p(c, _u8p), b0, b1)
+    if rc:
+        raise ValueError(f"oracle_protect failed rc={rc}")
+    return a[:lay["a_bytes"]], b[:lay["b_bytes"]], c[:lay["c_bytes"]]
+
+
+def recover(a, b, c, n_bytes: int, width: int, levels: int, key: bytes, iv: bytes,
+            mode: int = MODE_BLOCK8, flags: int = 0, block_offset: int = 0, block_range=None,
+            out=None):
+    """Returns (bytes, (first_bad_block, bad_blocks))."""
+    lay = layout(n_bytes, width, levels, mode)
+    streams = []
+    for s, key_ in zip((a, b, c), ("a_bytes", "b_bytes", "c_bytes")):
+        s = _u8(s)
+        assert s.size >= lay[key_], (key_, s.size, lay[key_])
+        streams.append(s if s.size else np.zeros(1, np.uint8))
+    o = out if out is not None else np.zeros(max(n_bytes, 1), dtype=np.uint8)
+    rep = np.zeros(2, dtype=np.int64)
+    k, v = _u8(key), _u8(iv)
+    b0, b1 = block_range if block_range is not None else (0, lay["n_blocks"])
+    rc = lib().oracle_recover_range(n_bytes, width, levels, mode, flags, block_offset,
+                                    _p(k, _u8p), _p(v, _u8p), *[_p(s, _u8p) for s in streams],
+                                    _p(o, _u8p), _p(rep, _i64p), b0, b1)
+    if rc:
+        raise ValueError(f"oracle_recover failed rc={rc}")
+    return o[:n_bytes], (int(rep[0]), int(rep[1]))
