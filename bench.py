@@ -1,0 +1,466 @@
+#!/usr/bin/env python3
+"""bench.py — protect+recover throughput of the agnostic SE hot path on B200.
+
+Contract (see task / DESIGN.md §6):
+  python bench.py [--gpus N --steps K --warmup W] [--config 2] [--impl se|reference]
+One step = one pass of the whole hot path (fused
+protect, then fused recover) over one synthetic input resident in HBM.  The
+metric is BASELINE.json's: input GB/s through protect+recover, whole job, and
+the dominant kernel's fraction of its roofline.  Under torchrun each rank
+processes its own independent file (weak scaling, no data-path collective);
+NCCL is used only for the barrier and the max-over-ranks of the timings.
+
+--impl reference times the CPU oracle (oracle/, plain C) on the host cores on
+a bounded sample of the same workload — the paper-defined computation, as it
+stands; it is a reported baseline, not a target.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+L2_BYTES = 126 * (1 << 20)
+
+# ---------------------------------------------------------------- roofline model
+# Algorithmic ALU-pipe operations per 8x8 block: the shift /
+# rotate / logic operations (SHF, LOP3, PRMT class) the method needs in a
+# minimal 32-bit mapping.  Adds are excluded (they may issue on the FMA pipe
+# as IMAD), so these ops alone set a lower bound on ALU-pipe cycles.
+#   SHA-256 rounds 8..63 (host midstate covers 0..7):  8*10 + 48*18 = 944
+#   SHA-512 rounds 4..79 (host midstate covers 0..3): 12*20 + 64*36 = 2544
+#   5/3 lifting shifts: L1 16 lifts*8 + L2 8 lifts*4 (+ L3 4 lifts*2) = 160 (168)
+#   byte unpack 64; field pack/unpack ~2 per field + word splits = 140
+#   mask XORs: B + C words = 19;  AES-CTR: 260 ops per AES block * a_bits/128
+ALU_OPS = {
+    1: {"sha256": 0, "sha512": 2544, "dwt": 128 + 64, "pack": 140, "xor": 15, "aes": 260 * 160 / 128},
+    2: {"sha256": 944, "sha512": 2544, "dwt": 160 + 64, "pack": 140, "xor": 19, "aes": 260 * 40 / 128},
+    3: {"sha256": 944, "sha512": 2544, "dwt": 168 + 64, "pack": 140, "xor": 20, "aes": 260 * 10 / 128},
+}
+ALU_LANES_PER_SM_CLK = 64      # B300_MICROARCH.md: IADD3/LOP3/SHF/PRMT on alu-pipe, rt_SMSP = 2
+NUM_SMS = 148
+
+
+def alu_ops_per_block(levels: int, masked: bool) -> float:
+    d = ALU_OPS[levels]
+    ops = d["dwt"] + d["pack"] + d["aes"]
+    if masked:
+        ops += d["sha256"] + d["sha512"] + d["xor"]
+    return float(ops)
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---------------------------------------------------------------- clocks sampler
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 10:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+
+        def num(s):
+            try:
+                return float(s)
+            except ValueError:
+                return None
+        loaded = [r for r in self.rows if (num(r[3]) or 0) > 0] or self.rows
+        sm = [num(r[1]) for r in loaded if num(r[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in loaded:
+            for name, v in zip(names, r[6:10]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(loaded[0][2]),
+                "reasons": sorted(reasons), "samples": len(loaded),
+                "power_w_max": max((num(r[4]) or 0) for r in loaded)}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(cfg: int):
+    c = synth.CONFIGS[cfg]
+    x = synth.config_input(cfg)
+    return c, x
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_se(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1803_04880_b200 as se
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    se.lib()
+    c, x_np = workload(args.config)
+    W, L, n = c["width"], c["levels"], x_np.size
+    key = synth.KEY
+    iv = synth.iv_for(args.config, rank)                # each rank: its own independent file
+    flags = se.FLAG_PUBLIC_PLAIN if args.plain else 0
+    masked = not args.plain
+    lay = se.fragment_layout(n, W, L)
+    stream = torch.cuda.Stream(device=dev)
+    x = torch.from_numpy(x_np).to(dev)
+    a = torch.empty(lay["a_bytes"], dtype=torch.uint8, device=dev)
+    b = torch.empty(max(lay["b_bytes"], 16), dtype=torch.uint8, device=dev)[: lay["b_bytes"]]
+    cc = torch.empty(lay["c_bytes"], dtype=torch.uint8, device=dev)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    rep = torch.empty(2, dtype=torch.int64, device=dev)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)   # 252 MB > L2
+    torch.cuda.synchronize()
+
+    def step():
+        se.fragment_protect(x, W, L, key, iv, flags=flags, out=(a, b, cc), stream=stream)
+        se.fragment_recover(a, b, cc, n, W, L, key, iv, flags=flags, out=out, report=rep, stream=stream)
+
+    # correctness of the timed configuration (cheap property at full size)
+    with torch.cuda.stream(stream):
+        step()
+    stream.synchronize()
+    assert torch.equal(out, x), "recover(protect(x)) != x in the timed configuration"
+    assert rep.cpu().tolist() == [-1, 0]
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    # warm-up: at least W steps and ~1 s of sustained load (clock sampling)
+    t_end = time.time() + args.soak
+    i = 0
+    while i < args.warmup or time.time() < t_end:
+        step()
+        i += 1
+    stream.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    se.launch_count(reset=True)
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k)                                  # evict L2 between timed steps
+            ev[k][0].record(stream)
+            se.fragment_protect(x, W, L, key, iv, flags=flags, out=(a, b, cc), stream=stream)
+            ev[k][1].record(stream)
+            se.fragment_recover(a, b, cc, n, W, L, key, iv, flags=flags, out=out, report=rep, stream=stream)
+            ev[k][2].record(stream)
+    stream.synchronize()
+    launches = se.launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks.stop()
+    t_prot = [e[0].elapsed_time(e[1]) for e in ev]          # ms
+    t_rec = [e[1].elapsed_time(e[2]) for e in ev]
+    total_ms = sum(t_prot) + sum(t_rec)
+    ms_step = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        ms_step = total_ms / args.steps
+
+    # ---- e2e: same metric with host buffers, H2D/D2H inside the timed region
+    e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, args.e2e_steps)
+
+    # ---- comparator: full-file AES-128-CTR on the same GPU (paper methodology)
+    aes_gbs = None
+    if not args.no_comparator:
+        y = torch.empty_like(x)
+        for _ in range(3):
+            se.cipher_encrypt(key, iv, x, out=y, stream=stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(reps):
+                se.cipher_encrypt(key, iv, x, out=y, stream=stream)
+            e1.record(stream)
+        stream.synchronize()
+        aes_gbs = n * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+        del y
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    peaks, peak_src = load_peaks()
+    clk = clocks.summary()
+    gbs = n * world / (ms_step / 1e3) / 1e9
+    # dominant kernel = the slower of the two fused kernels
+    mp, mr = sum(t_prot) / args.steps, sum(t_rec) / args.steps
+    dom_name, dom_ms = ("k_protect_block8", mp) if mp >= mr else ("k_recover_block8", mr)
+    ops = alu_ops_per_block(L, masked) * lay["n_blocks"]
+    achieved = ops / (dom_ms / 1e3) / 1e9                     # Gop/s
+    peak_alu = NUM_SMS * ALU_LANES_PER_SM_CLK * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+    hbm_bytes = n + lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"]
+    line = {
+        "metric": "protect+recover GB/s per GPU and at 1/2/4/8 B200; % of HBM roofline",
+        "value": round(gbs, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": c["name"] + (" (PUBLIC_PLAIN)" if args.plain else ""), "n_bytes": n,
+                   "width": W, "levels": L, "mode": "BLOCK8", "n_blocks": lay["n_blocks"],
+                   "per_rank_input": "independent file per rank (own IV)", "l2": "flushed between steps",
+                   "parallelism": f"dp{world} by file"},
+        "roofline": {"bound": "alu", "kernel": dom_name, "achieved": round(achieved, 1),
+                     "peak": round(peak_alu, 1), "unit": "Gop/s", "frac": round(achieved / peak_alu, 4),
+                     "traffic": None, "peak_source": f"guide: {NUM_SMS} SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x "
+                                                    f"{peaks.get('sm_max_mhz', 1965.0)} MHz ({peak_src} clock)",
+                     "alu_ops_per_block": alu_ops_per_block(L, masked)},
+        "hbm": {"bytes_per_step": 2 * hbm_bytes, "achieved_gbs": round(2 * hbm_bytes / (ms_step / 1e3) / 1e9, 1),
+                "peak_gbs": peaks.get("hbm_gbs"), "frac": round(2 * hbm_bytes / (ms_step / 1e3) / 1e9 /
+                                                                 peaks.get("hbm_gbs", 6551.7), 4)},
+        "kernels_ms": {"protect": round(mp, 5), "recover": round(mr, 5)},
+        "protect_gbs": round(n / (mp / 1e3) / 1e9, 3),
+        "recover_gbs": round(n / (mr / 1e3) / 1e9, 3),
+        "comparator_aes128_ctr_gbs": None if aes_gbs is None else round(aes_gbs, 2),
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(x_np, W, L, key, iv, flags, args.cpu_seconds)
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps):
+    """protect + recover with host-resident input and results: pinned H2D of the
+    input, D2H of the three fragments and of the recovered bytes, every step."""
+    n = x_np.size
+    lay = se.fragment_layout(n, W, L)
+    stream = torch.cuda.Stream(device=dev)
+    hx = torch.from_numpy(x_np).pin_memory()
+    ha = torch.empty(lay["a_bytes"], dtype=torch.uint8).pin_memory()
+    hb = torch.empty(max(lay["b_bytes"], 1), dtype=torch.uint8).pin_memory()[: lay["b_bytes"]]
+    hc = torch.empty(lay["c_bytes"], dtype=torch.uint8).pin_memory()
+    hout = torch.empty(n, dtype=torch.uint8).pin_memory()
+    dx = torch.empty(n, dtype=torch.uint8, device=dev)
+    a = torch.empty(lay["a_bytes"], dtype=torch.uint8, device=dev)
+    b = torch.empty(max(lay["b_bytes"], 16), dtype=torch.uint8, device=dev)[: lay["b_bytes"]]
+    c = torch.empty(lay["c_bytes"], dtype=torch.uint8, device=dev)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    rep = torch.empty(2, dtype=torch.int64, device=dev)
+
+    def one():
+        with torch.cuda.stream(stream):
+            dx.copy_(hx, non_blocking=True)
+            se.fragment_protect(dx, W, L, key, iv, flags=flags, out=(a, b, c), stream=stream)
+            ha.copy_(a, non_blocking=True)
+            if lay["b_bytes"]:
+                hb.copy_(b, non_blocking=True)
+            hc.copy_(c, non_blocking=True)
+            se.fragment_recover(a, b, c, n, W, L, key, iv, flags=flags, out=out, report=rep, stream=stream)
+            hout.copy_(out, non_blocking=True)
+
+    for _ in range(3):
+        one()
+    stream.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+    for _ in range(steps):
+        one()
+    with torch.cuda.stream(stream):
+        e1.record(stream)
+    stream.synchronize()
+    assert torch.equal(hout, hx)
+    ms = e0.elapsed_time(e1) / steps
+    return {"value": round(n / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n,
+            "d2h_bytes_per_step": lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"] + n,
+            "ms_per_step": round(ms, 4), "path": "torch pinned copies + fragment_protect/recover (C ABI)"}
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+
+def oracle_time(x_np, W, L, key, iv, flags, n_blocks_sample, threads):
+    """Oracle protect + recover over the first n_blocks_sample blocks, split
+    across `threads` host threads (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    lay = oracle.layout(x_np.size, W, L)
+    nb = min(n_blocks_sample, lay["n_blocks"])
+    bufs = [np.zeros(max(lay[k], 1), np.uint8) for k in ("a_bytes", "b_bytes", "c_bytes")]
+    out = np.zeros(max(x_np.size, 1), np.uint8)
+    groups = -(-nb // 128)
+    per = -(-groups // threads)
+    ranges = [(g0 * 128, min(nb, (g0 + per) * 128)) for g0 in range(0, groups, per)]
+
+    def prot(r):
+        oracle.protect(x_np, W, L, key, iv, flags=flags, block_range=r, out=bufs)
+
+    def rec(r):
+        oracle.recover(bufs[0], bufs[1], bufs[2], x_np.size, W, L, key, iv, flags=flags, block_range=r, out=out)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(prot, ranges))
+        list(ex.map(rec, ranges))
+    dt = time.perf_counter() - t0
+    return nb, dt
+
+
+def cpu_baseline(x_np, W, L, key, iv, flags, seconds):
+    threads = os.cpu_count() or 1
+    nb_probe, dt_probe = oracle_time(x_np, W, L, key, iv, flags, 256 * threads, threads)
+    rate = nb_probe / max(dt_probe, 1e-6)
+    total_nb = -(-x_np.size // (W * 8)) * (W // 8)
+    nb = int(min(total_nb, max(128, rate * seconds)))
+    nb, dt = oracle_time(x_np, W, L, key, iv, flags, nb, threads)
+    gbs = nb * 64 / dt / 1e9
+    return {"value": round(gbs, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {nb} of {total_nb} 8x8 blocks of the same input (protect+recover), "
+                      f"{threads} host threads, {dt:.1f} s",
+            "host_cpu": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    c, x_np = workload(args.config)
+    W, L = c["width"], c["levels"]
+    key, iv = synth.KEY, synth.iv_for(args.config, 0)
+    flags = 1 if args.plain else 0
+    threads = os.cpu_count() or 1
+    nb_probe, dt_probe = oracle_time(x_np, W, L, key, iv, flags, 128 * threads, threads)
+    rate = nb_probe / max(dt_probe, 1e-6)
+    total_nb = -(-x_np.size // (W * 8)) * (W // 8)
+    budget = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.2)
+    nb = int(min(total_nb, max(128, rate * budget)))
+    for _ in range(args.warmup):
+        oracle_time(x_np, W, L, key, iv, flags, nb, threads)
+    times = []
+    for _ in range(args.steps):
+        _, dt = oracle_time(x_np, W, L, key, iv, flags, nb, threads)
+        times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    gbs = nb * 64 / (ms / 1e3) / 1e9
+    sample = f"first {nb} of {total_nb} 8x8 blocks per step (protect+recover), {threads} host threads"
+    return {
+        "metric": "protect+recover GB/s per GPU and at 1/2/4/8 B200; % of HBM roofline",
+        "impl": "reference", "value": round(gbs, 6), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": c["name"], "n_bytes": x_np.size, "width": W, "levels": L, "mode": "BLOCK8"},
+        "cpu_baseline": {"value": round(gbs, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                         "sample": sample, "host_cpu": cpu_model()},
+        "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--impl", default="se", choices=["se", "reference"])
+    ap.add_argument("--plain", action="store_true", help="PUBLIC_PLAIN measurement mode (C26)")
+    ap.add_argument("--soak", type=float, default=1.5, help="seconds of sustained warm-up load")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-comparator", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    line = run_reference(args) if args.impl == "reference" else run_se(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/*
+ * se.h — C ABI of libse.so: B200-native (sm_100a) agnostic selective
+ * encryption, the Chapter 5 hot path of arxiv/paper_1803_04880.
+ *
+ * The operation (PAPER.md "Design of DWT based SE"): any byte
+ * stream is read as a 2-D matrix of 8-bit "pixels", tiled into 8x8
+ * blocks; each block is transformed by a lossless integer Le Gall 5/3 lifting
+ * DWT (Eq. 5.1-5.2), two levels; the coefficients are
+ * split into three fragments per block (D_iA, D_iB, D_iC):
+ *   A  private fragment  = 2nd-level LL, 4 x 10 bits = 40 bits
+ *   B  1st public frag.  = 2nd-level HL/LH/HH, 124 bits
+ *   C  2nd public frag.  = 1st-level HL/LH/HH, 480 bits
+ * A is encrypted with AES-128; B is XORed with SHA-256 of (key, A)
+ * (P:2130); C is XORed with SHA-512 of (B', key).  Recovery is the
+ * exact inverse.  Where the paper is silent the readings are
+ * those of DESIGN.md §3; the byte-exact definition is the
+ * oracle in oracle/ (which this library does not use).
+ *
+ * Conventions shared by every call:
+ *   Geometry   n_bytes bytes form a W x R matrix, W = width (a positive
+ *              multiple of 8), R = ceil(n_bytes / W) rounded up to a multiple
+ *              of 8; bytes past n_bytes read as 0 (C18).  Blocks are numbered
+ *              row-major: b = br * (W/8) + bc (C11).
+ *   Levels     1, 2 (the paper) or 3 (C21).  L = 1: A = LL1 (160 b), B empty;
+ *              L = 3: A = LL3 (10 b), B = level-3 + level-2 details (155 b).
+ *   Streams    A', B', C' are dense bit streams, records in block order,
+ *              MSB-first, fields offset-binary (C9-C11), the final byte zero-
+ *              padded; sizes from fragment_layout().
+ *   Key, IV    16-byte HOST buffers, read during the call only.  The IV is
+ *              the initial AES-CTR counter block (C13) and enters the hash
+ *              framing (C15): M_B = K||IV||be64(b)||A_b, M_C = K||IV||be64(b)||B'_b.
+ *   Device ptrs  caller-owned device memory (e.g. torch tensors), 16-byte
+ *              aligned (else SE_EALIGN), valid until the stream reaches the
+ *              work.  No call allocates device memory on the hot path.
+ *   stream     a cudaStream_t passed as void* (NULL = legacy default stream).
+ *              Calls are asynchronous on it; all run on the current device.
+ *   Errors     return se_status; nothing is printed.  Launch failures are
+ *              SE_ECUDA (cudaGetLastError).  Data-dependent corruption (wrong
+ *              key, damaged fragments) is NOT an error: recover reports it in
+ *              a device-resident se_report.
+ *   Threading  stateless and reentrant; concurrent calls on different streams
+ *              or devices are safe.
+ */
+#ifndef SE_H
+#define SE_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SE_OK = 0,
+    SE_EINVAL = -1,   /* null pointer, bad width/levels/mode, bad offsets    */
+    SE_EALIGN = -2,   /* device pointer not 16-byte aligned                  */
+    SE_ECUDA = -3,    /* CUDA launch / runtime failure                       */
+    SE_ENOTSUP = -4   /* combination not implemented                         */
+} se_status;
+
+enum { SE_MODE_BLOCK8 = 0,   /* per-8x8-block DWT: the paper   */
+       SE_MODE_FULL = 1 };   /* whole-matrix Mallat DWT: extension row a11       */
+
+enum { SE_FLAG_PUBLIC_PLAIN = 1u << 0 };  /* skip the SHA masks on B and C:
+                                             measurement mode (C26) */
+
+/* block_offset: global index of this input's first 8x8 block inside the
+ * logical file (0 for a whole file).  It is the hash nonce base (C16) and
+ * sets the CTR start counter IV + block_offset*a_bits/128, so it must make
+ * block_offset*a_bits a multiple of 128 (any multiple of 128 blocks does). */
+typedef struct {
+    uint64_t n_bytes;
+    uint32_t width, levels, mode, flags;
+    uint64_t block_offset;
+} se_geom;
+
+typedef struct {
+    uint64_t rows, n_blocks, a_bytes, b_bytes, c_bytes;
+    uint32_t a_bits, b_bits, c_bits;   /* bits per block record            */
+    uint32_t halo_rows;                /* input rows a stripe needs beyond
+                                          its own (0 in BLOCK8; FULL: 2(2^L-1)) */
+} se_layout;
+
+/* Device-resident corruption report written by fragment_recover.
+ * first_bad_block = -1 when clean, else the smallest local block index
+ * with a reconstructed sample outside [0, 255]; bad_blocks = their count. */
+typedef struct {
+    int64_t first_bad_block;
+    uint64_t bad_blocks;
+} se_report;
+
+/* ---- layout (host, pure) ------------------------------------------------
+ * Sizes of the matrix and of the three fragment streams (P:2243, P:2285,
+ * 40/124/480 bits per block = 7.8/24.2/93.8 % at L = 2). */
+int fragment_layout(const se_geom* g, se_layout* out);
+
+/* ---- protect: rows a1-a9 in one kernel -----------------------------------
+ * d_in: n_bytes input bytes (device).  d_a, d_b, d_c: device buffers of
+ * a_bytes, b_bytes, c_bytes (d_b may be NULL when b_bytes == 0).  Writes the
+ * protected streams A', B', C'.  n_bytes == 0 is a no-op. */
+int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
+                     const void* d_in, void* d_a, void* d_b, void* d_c, void* stream);
+
+/* ---- recover: row a10 -----------------------------------------------------
+ * Inverse of fragment_protect; writes exactly n_bytes bytes to d_out.
+ * d_report (nullable, device) receives the corruption report. */
+int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
+                     const void* d_a, const void* d_b, const void* d_c, void* d_out,
+                     se_report* d_report, void* stream);
+
+/* ---- batched protect / recover (many independent files, one launch) -----
+ * d_jobs: device array of n_jobs descriptors.  cta_begin must be the
+ * exclusive prefix sum over jobs of ceil(n_blocks_j / 128) (fragment_batch_plan
+ * computes it host-side); total_ctas is the sum.  Every job shares key,
+ * levels and flags; each has its own IV and block_offset. */
+typedef struct {
+    const uint8_t* in;        /* protect: input;  recover: output (cast)      */
+    uint8_t* out;             /* recover: output bytes (protect: unused)      */
+    uint8_t *a, *b, *c;       /* fragment streams                             */
+    uint64_t n_bytes;
+    uint64_t block_offset;
+    uint64_t cta_begin;       /* first CTA of this job in the launch           */
+    uint32_t width;
+    uint32_t pad_;
+    uint8_t iv[16];
+} se_job;
+
+/* Fill width-independent fields of jobs[i].cta_begin and return total CTAs
+ * (host helper, pure). Returns -1 on invalid geometry. */
+int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels);
+int fragment_protect_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas,
+                           uint32_t levels, uint32_t flags, const uint8_t key[16],
+                           void* stream);
+int fragment_recover_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas,
+                           uint32_t levels, uint32_t flags, const uint8_t key[16],
+                           se_report* d_report, void* stream);
+
+/* ---- host-resident streaming protect / recover (NEXT row f1) -------------
+ * h_* are HOST buffers (pinned or pageable).  The library stages chunks of
+ * whole 8-row block-rows through its own pinned + device buffers on
+ * n_streams CUDA streams, overlapping H2D copy, kernel and D2H copy
+ * (the paper's transfer/compute overlap).  Blocking: returns
+ * after the last D2H completes.  chunk_bytes = input bytes per chunk
+ * (rounded to whole 128-block groups; 0 = 32 MiB). */
+int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
+                          const void* h_in, void* h_a, void* h_b, void* h_c,
+                          uint64_t chunk_bytes, uint32_t n_streams);
+int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
+                          const void* h_a, const void* h_b, const void* h_c, void* h_out,
+                          se_report* h_report, uint64_t chunk_bytes, uint32_t n_streams);
+
+/* ---- transform only: rows a1-a4 / a11 ------------------------------------
+ * d_coef: R x W int16 (R = layout.rows).  BLOCK8: block (br, bc) coefficient
+ * (i, j) at [(8br+i)*W + 8bc+j], dyadic quadrants inside each block (LL top-
+ * left, HL top-right, LH bottom-left, HH bottom-right; C7).  FULL: Mallat
+ * layout over the whole matrix.  dwt_inv writes n_bytes bytes; samples
+ * outside [0,255] are stored modulo 256. */
+int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream);
+int dwt_inv(const se_geom* g, const int16_t* d_coef, void* d_out, void* stream);
+
+/* ---- cipher only: AES-128-CTR (row a6; the paper's full-AES comparator,
+ * P:219) ----------------------------------------------------
+ * out[i] = in[i] ^ KS[i], KS block j = AES_K(IV + ctr_block_offset + j),
+ * 128-bit big-endian counter (SP 800-38A).  In place allowed (d_in == d_out).
+ * cipher_decrypt is the same operation (CTR). */
+int cipher_encrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block_offset,
+                   const void* d_in, void* d_out, uint64_t n, void* stream);
+int cipher_decrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block_offset,
+                   const void* d_in, void* d_out, uint64_t n, void* stream);
+
+/* ---- misc ----------------------------------------------------------------- */
+const char* se_strerror(int status);
+/* Number of kernel launches issued by this thread since the last reset
+ * (bench/test evidence of native launches). */
+uint64_t se_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

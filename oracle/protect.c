@@ -169,16 +169,13 @@ static void mask_record(int use512, const uint8_t key[16], const uint8_t iv[16],
 /* A stream CTR over local bytes [p0, p1) (C12, C13) */
 static void ctr_range(const uint8_t key[16], const uint8_t iv[16], uint64_t base_byte,
                       uint8_t* a, uint64_t p0, uint64_t p1) {
-    uint8_t zero[16] = {0}, ks[16];
-    uint64_t cached = UINT64_MAX;
-    for (uint64_t p = p0; p < p1; ++p) {
-        uint64_t g = base_byte + p;
-        if (g / 16 != cached) {
-            cached = g / 16;
-            oracle_aes128_ctr(key, iv, cached, zero, ks, 16);   /* KS = AES_K(IV + j) */
-        }
-        a[p] ^= ks[g % 16];
-    }
+    if (p1 <= p0) return;
+    /* keystream for global A bytes [base+p0, base+p1): KS block j = AES_K(IV + j) */
+    uint64_t first = base_byte + p0, skip = first % 16, len = p1 - p0;
+    uint8_t* ks = (uint8_t*)calloc((size_t)(skip + len), 1);
+    oracle_aes128_ctr(key, iv, first / 16, ks, ks, skip + len);   /* 0 ^ KS = KS */
+    for (uint64_t p = p0; p < p1; ++p) a[p] ^= ks[skip + (p - p0)];
+    free(ks);
 }
 
 static int check_range_args(uint64_t nb, uint64_t b0, uint64_t b1) { return b0 <= b1 && b1 <= nb; }

@@ -1,0 +1,212 @@
+"""paper_1803_04880_b200 — B200-native agnostic selective encryption.
+
+Thin ctypes binding over ``libse.so`` (the C ABI in ``include/se.h``): every
+function here only marshals arguments — torch tensors supply device memory
+and the current CUDA stream; all work runs in the library's sm_100a kernels.
+There is no CPU fallback: if ``libse.so`` is missing or no CUDA device is
+present, calls raise.
+
+Names follow the C ABI and the paper's problem statement: protect
+maps a chunk D_i to its fragments (D_iA, D_iB, D_iC); recover maps them back.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+LIB_PATH = os.path.join(_HERE, "libse.so")
+CSRC = os.path.join(_HERE, "csrc")
+SOURCES = ["se_api.cu", "k_block8.cu", "k_full.cu", "k_cipher.cu", "k_batch.cu", "se_host.cu"]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
+
+SE_OK, SE_EINVAL, SE_EALIGN, SE_ECUDA, SE_ENOTSUP = 0, -1, -2, -3, -4
+MODE_BLOCK8, MODE_FULL = 0, 1
+FLAG_PUBLIC_PLAIN = 1
+
+
+def sources():
+    return [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libse.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    deps = sources() + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    deps.append(os.path.join(_ROOT, "include", "se.h"))
+    if not force and os.path.exists(LIB_PATH):
+        if os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(p) for p in deps):
+            return LIB_PATH
+    tmp = LIB_PATH + f".tmp{os.getpid()}"
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", tmp, *sources()]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.check_call(cmd, cwd=CSRC)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class Geom(C.Structure):
+    _fields_ = [("n_bytes", C.c_uint64), ("width", C.c_uint32), ("levels", C.c_uint32),
+                ("mode", C.c_uint32), ("flags", C.c_uint32), ("block_offset", C.c_uint64)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("n_blocks", C.c_uint64), ("a_bytes", C.c_uint64),
+                ("b_bytes", C.c_uint64), ("c_bytes", C.c_uint64), ("a_bits", C.c_uint32),
+                ("b_bits", C.c_uint32), ("c_bits", C.c_uint32), ("halo_rows", C.c_uint32)]
+
+
+class Job(C.Structure):
+    _fields_ = [("in_", C.c_void_p), ("out", C.c_void_p), ("a", C.c_void_p), ("b", C.c_void_p),
+                ("c", C.c_void_p), ("n_bytes", C.c_uint64), ("block_offset", C.c_uint64),
+                ("cta_begin", C.c_uint64), ("width", C.c_uint32), ("pad_", C.c_uint32),
+                ("iv", C.c_uint8 * 16)]
+
+
+SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_batch_plan",
+           "fragment_protect_batch", "fragment_recover_batch", "fragment_protect_host",
+           "fragment_recover_host", "dwt_fwd", "dwt_inv", "cipher_encrypt", "cipher_decrypt",
+           "se_strerror", "se_launch_count"]
+
+_lib = None
+
+
+def lib():
+    """Load libse.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libse.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        vp, u8p = C.c_void_p, C.c_char_p
+        gp = C.POINTER(Geom)
+        L.fragment_layout.argtypes = [gp, C.POINTER(Layout)]
+        L.fragment_protect.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp]
+        L.fragment_recover.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp, vp]
+        L.fragment_batch_plan.argtypes = [C.POINTER(Job), C.c_uint32, C.c_uint32]
+        L.fragment_batch_plan.restype = C.c_int64
+        L.fragment_protect_batch.argtypes = [C.c_uint32, vp, C.c_uint64, C.c_uint32, C.c_uint32, u8p, vp]
+        L.fragment_recover_batch.argtypes = [C.c_uint32, vp, C.c_uint64, C.c_uint32, C.c_uint32, u8p, vp, vp]
+        L.fragment_protect_host.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, C.c_uint64, C.c_uint32]
+        L.fragment_recover_host.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp, C.c_uint64, C.c_uint32]
+        L.dwt_fwd.argtypes = [gp, vp, vp, vp]
+        L.dwt_inv.argtypes = [gp, vp, vp, vp]
+        L.cipher_encrypt.argtypes = [u8p, u8p, C.c_uint64, vp, vp, C.c_uint64, vp]
+        L.cipher_decrypt.argtypes = [u8p, u8p, C.c_uint64, vp, vp, C.c_uint64, vp]
+        L.se_strerror.argtypes = [C.c_int]
+        L.se_strerror.restype = C.c_char_p
+        L.se_launch_count.argtypes = [C.c_int]
+        L.se_launch_count.restype = C.c_uint64
+        _lib = L
+    return _lib
+
+
+class SEError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {lib().se_strerror(status).decode()} ({status})")
+        self.status = status
+
+
+def _check(rc: int, what: str):
+    if rc != SE_OK:
+        raise SEError(rc, what)
+
+
+def _geom(n_bytes, width, levels, mode=MODE_BLOCK8, flags=0, block_offset=0) -> Geom:
+    return Geom(int(n_bytes), int(width), int(levels), int(mode), int(flags), int(block_offset))
+
+
+def _bytes16(x, name) -> bytes:
+    b = bytes(x)
+    if len(b) != 16:
+        raise ValueError(f"{name} must be 16 bytes")
+    return b
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def fragment_layout(n_bytes: int, width: int, levels: int, mode: int = MODE_BLOCK8,
+                    flags: int = 0, block_offset: int = 0) -> dict:
+    g = _geom(n_bytes, width, levels, mode, flags, block_offset)
+    out = Layout()
+    _check(lib().fragment_layout(C.byref(g), C.byref(out)), "fragment_layout")
+    return {k: int(getattr(out, k)) for k, _ in Layout._fields_}
+
+
+def _empty(n, device):
+    import torch
+    return torch.empty(max(int(n), 1), dtype=torch.uint8, device=device)[: int(n)] if n else \
+        torch.empty(16, dtype=torch.uint8, device=device)[:0]
+
+
+def fragment_protect(x, width: int, levels: int, key, iv, mode: int = MODE_BLOCK8, flags: int = 0,
+                     block_offset: int = 0, out=None, stream=None):
+    """x: 1-D uint8 CUDA tensor (n bytes).  Returns device tensors (A', B', C')."""
+    lay = fragment_layout(x.numel(), width, levels, mode, flags, block_offset)
+    a, b, c = out if out is not None else (_empty(lay["a_bytes"], x.device), _empty(lay["b_bytes"], x.device),
+                                           _empty(lay["c_bytes"], x.device))
+    g = _geom(x.numel(), width, levels, mode, flags, block_offset)
+    _check(lib().fragment_protect(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(x), _ptr(a),
+                                  _ptr(b) if b.numel() else None, _ptr(c), _stream(stream)), "fragment_protect")
+    return a, b, c
+
+
+def fragment_recover(a, b, c, n_bytes: int, width: int, levels: int, key, iv, mode: int = MODE_BLOCK8,
+                     flags: int = 0, block_offset: int = 0, out=None, report=None, stream=None):
+    """Returns (bytes tensor, report tensor int64[2] = [first_bad_block, bad_blocks])."""
+    import torch
+    dev = a.device
+    o = out if out is not None else _empty(n_bytes, dev)
+    rep = report if report is not None else torch.empty(2, dtype=torch.int64, device=dev)
+    g = _geom(n_bytes, width, levels, mode, flags, block_offset)
+    _check(lib().fragment_recover(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(a),
+                                  _ptr(b) if b is not None and b.numel() else None, _ptr(c), _ptr(o),
+                                  _ptr(rep), _stream(stream)), "fragment_recover")
+    return o, rep
+
+
+def dwt_fwd(x, width: int, levels: int, mode: int = MODE_BLOCK8, out=None, stream=None):
+    """Returns the R x W int16 coefficient matrix (device)."""
+    import torch
+    lay = fragment_layout(x.numel(), width, levels, mode)
+    coef = out if out is not None else torch.empty((lay["rows"], width), dtype=torch.int16, device=x.device)
+    g = _geom(x.numel(), width, levels, mode)
+    _check(lib().dwt_fwd(C.byref(g), _ptr(x), _ptr(coef), _stream(stream)), "dwt_fwd")
+    return coef
+
+
+def dwt_inv(coef, n_bytes: int, width: int, levels: int, mode: int = MODE_BLOCK8, out=None, stream=None):
+    o = out if out is not None else _empty(n_bytes, coef.device)
+    g = _geom(n_bytes, width, levels, mode)
+    _check(lib().dwt_inv(C.byref(g), _ptr(coef), _ptr(o), _stream(stream)), "dwt_inv")
+    return o
+
+
+def cipher_encrypt(key, iv, x, ctr_block_offset: int = 0, out=None, stream=None):
+    o = out if out is not None else _empty(x.numel(), x.device)
+    _check(lib().cipher_encrypt(_bytes16(key, "key"), _bytes16(iv, "iv"), int(ctr_block_offset), _ptr(x),
+                                _ptr(o), x.numel(), _stream(stream)), "cipher_encrypt")
+    return o
+
+
+def cipher_decrypt(key, iv, x, ctr_block_offset: int = 0, out=None, stream=None):
+    o = out if out is not None else _empty(x.numel(), x.device)
+    _check(lib().cipher_decrypt(_bytes16(key, "key"), _bytes16(iv, "iv"), int(ctr_block_offset), _ptr(x),
+                                _ptr(o), x.numel(), _stream(stream)), "cipher_decrypt")
+    return o
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().se_launch_count(1 if reset else 0))

@@ -1,0 +1,285 @@
+// se_api.cu — host side of libse.so: the C ABI declared in include/se.h.
+//
+// Validates geometry, derives everything that is the same
+// for every block once on the host — AES-128 key schedule (FIPS-197 §5.2),
+// the CTR start counter (C13), and the SHA-256 / SHA-512 midstates over the
+// constant message prefix K||IV (C15) — and launches the fused kernels on the
+// caller's stream.  No device allocation, no synchronisation on the hot path.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include "se_internal.h"
+#include "tables.h"
+
+namespace se {
+
+static thread_local uint64_t t_launches = 0;
+void note_launch() { ++t_launches; }
+
+static const uint8_t kSbox[256] = SE_AES_SBOX_INIT;
+static const uint32_t kK256[64] = SE_SHA256_K_INIT;
+static const uint32_t kH256[8] = SE_SHA256_H0_INIT;
+static const uint64_t kK512[80] = SE_SHA512_K_INIT;
+static const uint64_t kH512[8] = SE_SHA512_H0_INIT;
+
+static uint32_t be32(const uint8_t* p) {
+    return (uint32_t)p[0] << 24 | (uint32_t)p[1] << 16 | (uint32_t)p[2] << 8 | p[3];
+}
+
+// FIPS-197 §5.2 KeyExpansion (Nk = 4, Nr = 10), big-endian words.
+static void key_expansion(const uint8_t key[16], uint32_t rk[44]) {
+    for (int i = 0; i < 4; ++i) rk[i] = be32(key + 4 * i);
+    uint32_t rcon = 0x01;
+    for (int i = 4; i < 44; ++i) {
+        uint32_t t = rk[i - 1];
+        if (i % 4 == 0) {
+            t = (t << 8) | (t >> 24);                                        // RotWord
+            t = (uint32_t)kSbox[t >> 24] << 24 | (uint32_t)kSbox[(t >> 16) & 0xff] << 16 |
+                (uint32_t)kSbox[(t >> 8) & 0xff] << 8 | kSbox[t & 0xff];     // SubWord
+            t ^= rcon << 24;
+            rcon = ((rcon << 1) ^ ((rcon & 0x80) ? 0x1b : 0)) & 0xff;
+        }
+        rk[i] = rk[i - 4] ^ t;
+    }
+}
+
+static uint32_t ror32(uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
+static uint64_t ror64(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
+
+// SHA-256 rounds 0..7 over W0..W7 = K||IV (FIPS 180-4 §6.2.2 step 3).
+static void sha256_mid(const uint32_t w[8], uint32_t st[8]) {
+    uint32_t a = kH256[0], b = kH256[1], c = kH256[2], d = kH256[3];
+    uint32_t e = kH256[4], f = kH256[5], g = kH256[6], h = kH256[7];
+    for (int t = 0; t < 8; ++t) {
+        const uint32_t t1 = h + (ror32(e, 6) ^ ror32(e, 11) ^ ror32(e, 25)) + ((e & f) ^ (~e & g)) + kK256[t] + w[t];
+        const uint32_t t2 = (ror32(a, 2) ^ ror32(a, 13) ^ ror32(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));
+        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+    }
+    st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
+}
+
+// SHA-512 rounds 0..3 over W0..W3 = K||IV (FIPS 180-4 §6.4.2 step 3).
+static void sha512_mid(const uint64_t w[4], uint64_t st[8]) {
+    uint64_t a = kH512[0], b = kH512[1], c = kH512[2], d = kH512[3];
+    uint64_t e = kH512[4], f = kH512[5], g = kH512[6], h = kH512[7];
+    for (int t = 0; t < 4; ++t) {
+        const uint64_t t1 = h + (ror64(e, 14) ^ ror64(e, 18) ^ ror64(e, 41)) + ((e & f) ^ (~e & g)) + kK512[t] + w[t];
+        const uint64_t t2 = (ror64(a, 28) ^ ror64(a, 34) ^ ror64(a, 39)) + ((a & b) ^ (a & c) ^ (b & c));
+        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+    }
+    st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
+}
+
+// 128-bit big-endian IV + j (SP 800-38A counter), as 4 big-endian words.
+static void ctr_base(const uint8_t iv[16], uint64_t j, uint32_t out[4]) {
+    uint64_t hi = (uint64_t)be32(iv) << 32 | be32(iv + 4);
+    uint64_t lo = (uint64_t)be32(iv + 8) << 32 | be32(iv + 12);
+    const uint64_t nlo = lo + j;
+    if (nlo < lo) ++hi;
+    out[0] = (uint32_t)(hi >> 32); out[1] = (uint32_t)hi;
+    out[2] = (uint32_t)(nlo >> 32); out[3] = (uint32_t)nlo;
+}
+
+static void record_bits(uint32_t L, uint32_t mode, uint32_t bits[3]) {
+    // BLOCK8 (C21, C22) / FULL (C23): A, B, C bits per block
+    if (L == 1) { bits[0] = 160; bits[1] = 0; bits[2] = 480; return; }
+    if (L == 2) { bits[0] = 40; bits[1] = mode ? 132 : 124; bits[2] = 480; return; }
+    bits[0] = 10; bits[1] = mode ? 165 : 155; bits[2] = 480;
+}
+
+static int check_geom(const se_geom* g) {
+    if (!g) return SE_EINVAL;
+    if (g->width == 0 || g->width % 8) return SE_EINVAL;
+    if (g->levels < 1 || g->levels > 3) return SE_EINVAL;
+    if (g->mode > SE_MODE_FULL) return SE_EINVAL;
+    if (g->flags & ~(uint32_t)SE_FLAG_PUBLIC_PLAIN) return SE_EINVAL;
+    return SE_OK;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static void fill_fused(FusedParams& p, const se_geom* g, const se_layout& lay, const uint8_t key[16],
+                       const uint8_t iv[16]) {
+    memset(&p, 0, sizeof p);
+    p.n_bytes = g->n_bytes;
+    p.n_blocks = lay.n_blocks;
+    p.block_offset = g->block_offset;
+    p.a_bytes = lay.a_bytes; p.b_bytes = lay.b_bytes; p.c_bytes = lay.c_bytes;
+    p.width = g->width;
+    p.bpr = g->width / 8;
+    ctr_base(iv, g->block_offset * lay.a_bits / 128, p.ctr);
+    key_expansion(key, p.rk);
+    for (int i = 0; i < 4; ++i) { p.kiv[i] = be32(key + 4 * i); p.kiv[4 + i] = be32(iv + 4 * i); }
+    sha256_mid(p.kiv, p.mid256);
+    memcpy(p.h256, kH256, sizeof kH256);
+    uint64_t w[4];
+    for (int i = 0; i < 4; ++i) w[i] = (uint64_t)p.kiv[2 * i] << 32 | p.kiv[2 * i + 1];
+    sha512_mid(w, p.mid512);
+    memcpy(p.h512, kH512, sizeof kH512);
+}
+
+}  // namespace se
+
+using namespace se;
+
+extern "C" {
+
+const char* se_strerror(int s) {
+    switch (s) {
+        case SE_OK: return "ok";
+        case SE_EINVAL: return "invalid argument";
+        case SE_EALIGN: return "device pointer not 16-byte aligned";
+        case SE_ECUDA: return "CUDA error";
+        case SE_ENOTSUP: return "not supported";
+        default: return "unknown status";
+    }
+}
+
+uint64_t se_launch_count(int reset) {
+    const uint64_t v = t_launches;
+    if (reset) t_launches = 0;
+    return v;
+}
+
+int fragment_layout(const se_geom* g, se_layout* out) {
+    int rc = check_geom(g);
+    if (rc) return rc;
+    if (!out) return SE_EINVAL;
+    uint32_t bits[3];
+    record_bits(g->levels, g->mode, bits);
+    const uint64_t R = ((g->n_bytes + g->width - 1) / g->width + 7) / 8 * 8;
+    const uint64_t nb = (R / 8) * (g->width / 8);
+    out->rows = R;
+    out->n_blocks = nb;
+    out->a_bits = bits[0]; out->b_bits = bits[1]; out->c_bits = bits[2];
+    out->a_bytes = (nb * bits[0] + 7) / 8;
+    out->b_bytes = (nb * bits[1] + 7) / 8;
+    out->c_bytes = (nb * bits[2] + 7) / 8;
+    out->halo_rows = g->mode == SE_MODE_FULL ? 2u * ((1u << g->levels) - 1u) : 0u;
+    return SE_OK;
+}
+
+static int fused_checks(const se_geom* g, const uint8_t* key, const uint8_t* iv, se_layout& lay) {
+    int rc = fragment_layout(g, &lay);
+    if (rc) return rc;
+    if (!key || !iv) return SE_EINVAL;
+    if ((g->block_offset * lay.a_bits) % 128) return SE_EINVAL;
+    if (g->mode != SE_MODE_BLOCK8) return SE_ENOTSUP;
+    return SE_OK;
+}
+
+int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in,
+                     void* d_a, void* d_b, void* d_c, void* stream) {
+    se_layout lay;
+    int rc = fused_checks(g, key, iv, lay);
+    if (rc) return rc;
+    if (g->n_bytes == 0) return SE_OK;
+    if (!d_in || !d_a || !d_c || (lay.b_bytes && !d_b)) return SE_EINVAL;
+    if (!aligned16(d_in) || !aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
+    FusedParams p;
+    fill_fused(p, g, lay, key, iv);
+    p.in = (const uint8_t*)d_in;
+    p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
+    const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
+    return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+}
+
+int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
+                     const void* d_b, const void* d_c, void* d_out, se_report* d_report, void* stream) {
+    se_layout lay;
+    int rc = fused_checks(g, key, iv, lay);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (d_report) {   // first_bad_block = -1 (all ones), bad_blocks = 0
+        if (cudaMemsetAsync(&d_report->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
+            cudaMemsetAsync(&d_report->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
+            return SE_ECUDA;
+    }
+    if (g->n_bytes == 0) return SE_OK;
+    if (!d_out || !d_a || !d_c || (lay.b_bytes && !d_b)) return SE_EINVAL;
+    if (!aligned16(d_out) || !aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
+    FusedParams p;
+    fill_fused(p, g, lay, key, iv);
+    p.out = (uint8_t*)d_out;
+    p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
+    p.report = d_report;
+    const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
+    return launch_recover_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+}
+
+int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream) {
+    se_layout lay;
+    int rc = fragment_layout(g, &lay);
+    if (rc) return rc;
+    if (g->mode != SE_MODE_BLOCK8) return SE_ENOTSUP;
+    if (g->n_bytes == 0) return SE_OK;
+    if (!d_in || !d_coef) return SE_EINVAL;
+    if (!aligned16(d_in) || !aligned16(d_coef)) return SE_EALIGN;
+    DwtParams p;
+    memset(&p, 0, sizeof p);
+    p.in = (const uint8_t*)d_in; p.coef = d_coef;
+    p.n_bytes = g->n_bytes; p.n_blocks = lay.n_blocks;
+    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows;
+    return launch_dwt_fwd_block8(p, g->levels, stream) ? SE_ECUDA : SE_OK;
+}
+
+int dwt_inv(const se_geom* g, const int16_t* d_coef, void* d_out, void* stream) {
+    se_layout lay;
+    int rc = fragment_layout(g, &lay);
+    if (rc) return rc;
+    if (g->mode != SE_MODE_BLOCK8) return SE_ENOTSUP;
+    if (g->n_bytes == 0) return SE_OK;
+    if (!d_out || !d_coef) return SE_EINVAL;
+    if (!aligned16(d_out) || !aligned16(d_coef)) return SE_EALIGN;
+    DwtParams p;
+    memset(&p, 0, sizeof p);
+    p.out = (uint8_t*)d_out; p.coef = (int16_t*)d_coef;
+    p.n_bytes = g->n_bytes; p.n_blocks = lay.n_blocks;
+    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows;
+    return launch_dwt_inv_block8(p, g->levels, stream) ? SE_ECUDA : SE_OK;
+}
+
+int cipher_encrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block_offset, const void* d_in,
+                   void* d_out, uint64_t n, void* stream) {
+    if (!key || !iv) return SE_EINVAL;
+    if (n == 0) return SE_OK;
+    if (!d_in || !d_out) return SE_EINVAL;
+    if (!aligned16(d_in) || !aligned16(d_out)) return SE_EALIGN;
+    CipherParams p;
+    memset(&p, 0, sizeof p);
+    p.in = (const uint8_t*)d_in; p.out = (uint8_t*)d_out; p.n = n;
+    ctr_base(iv, ctr_block_offset, p.ctr);
+    key_expansion(key, p.rk);
+    return launch_cipher_ctr(p, stream) ? SE_ECUDA : SE_OK;
+}
+
+int cipher_decrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block_offset, const void* d_in,
+                   void* d_out, uint64_t n, void* stream) {
+    return cipher_encrypt(key, iv, ctr_block_offset, d_in, d_out, n, stream);
+}
+
+int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels) {
+    (void)jobs; (void)n_jobs; (void)levels;
+    return SE_ENOTSUP;
+}
+
+int fragment_protect_batch(uint32_t, const se_job*, uint64_t, uint32_t, uint32_t, const uint8_t*, void*) {
+    return SE_ENOTSUP;
+}
+
+int fragment_recover_batch(uint32_t, const se_job*, uint64_t, uint32_t, uint32_t, const uint8_t*, se_report*,
+                           void*) {
+    return SE_ENOTSUP;
+}
+
+int fragment_protect_host(const se_geom*, const uint8_t*, const uint8_t*, const void*, void*, void*, void*,
+                          uint64_t, uint32_t) {
+    return SE_ENOTSUP;
+}
+
+int fragment_recover_host(const se_geom*, const uint8_t*, const uint8_t*, const void*, const void*, const void*,
+                          void*, se_report*, uint64_t, uint32_t) {
+    return SE_ENOTSUP;
+}
+
+}  // extern "C"

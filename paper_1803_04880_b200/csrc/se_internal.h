@@ -1,0 +1,64 @@
+// se_internal.h — kernel parameter blocks and launcher prototypes shared by
+// the host API (se_api.cu) and the kernel translation units.  Not installed.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/se.h"
+
+namespace se {
+
+constexpr int kBlocksPerCta = 128;   // one thread per 8x8 block, 128 blocks per CTA
+
+// Everything a fused protect/recover launch needs (passed by value; lives in
+// the constant bank, so round keys and midstates are uniform operands).
+struct FusedParams {
+    const uint8_t* in;        // protect: input bytes; recover: unused
+    uint8_t* out;             // recover: output bytes
+    uint8_t* a;               // A' stream
+    uint8_t* b;               // B' stream
+    uint8_t* c;               // C' stream
+    se_report* report;        // recover only, nullable
+    uint64_t n_bytes;
+    uint64_t n_blocks;
+    uint64_t block_offset;    // global index of local block 0 (hash nonce, C16)
+    uint64_t a_bytes, b_bytes, c_bytes;
+    uint32_t width;
+    uint32_t bpr;             // 8x8 blocks per block-row = width / 8
+    uint32_t ctr[4];          // IV + block_offset*a_bits/128, big-endian words
+    uint32_t rk[44];          // AES-128 round keys, big-endian words
+    uint32_t kiv[8];          // K || IV as big-endian words (SHA W0..W7)
+    uint32_t mid256[8];       // SHA-256 state after rounds 0..7 over K||IV
+    uint32_t h256[8];         // SHA-256 H(0)
+    uint64_t mid512[8];       // SHA-512 state after rounds 0..3 over K||IV
+    uint64_t h512[8];         // SHA-512 H(0)
+};
+
+struct CipherParams {
+    const uint8_t* in;
+    uint8_t* out;
+    uint64_t n;
+    uint32_t ctr[4];          // IV + ctr_block_offset
+    uint32_t rk[44];
+};
+
+struct DwtParams {
+    const uint8_t* in;
+    uint8_t* out;
+    int16_t* coef;
+    uint64_t n_bytes;
+    uint64_t n_blocks;
+    uint32_t width;
+    uint32_t bpr;
+    uint32_t rows;
+};
+
+// launchers (return cudaError_t as int)
+int launch_protect_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
+int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
+int launch_dwt_fwd_block8(const DwtParams& p, uint32_t levels, void* stream);
+int launch_dwt_inv_block8(const DwtParams& p, uint32_t levels, void* stream);
+int launch_cipher_ctr(const CipherParams& p, void* stream);
+
+void note_launch();
+
+}  // namespace se

@@ -1,0 +1,168 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle.
+
+Everything on this path is integer or bytewise, so the bar is bit-exact on
+every output: DWT coefficients, each fragment stream, ciphertext and the
+recovered bytes (BASELINE.json north_star).  Small cases
+span several 128-block CTAs and ragged tails; the BASELINE configs run at
+full size in the bench's launch configuration and are compared on sampled
+128-block groups the oracle computes one range at a time, plus the round-trip
+property on every byte.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1803_04880_b200 as se  # noqa: E402
+
+KEY = synth.KEY
+IV = bytes.fromhex("0011223344556677ffffffffffffff00")   # counter carries inside the CTA
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    se.lib()
+    return torch.device("cuda:0")
+
+
+def to_dev(x, dev):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+# n, W, L — tiny, ragged (n not a multiple of W; partial block-rows), several CTAs
+SMALL = [(1, 8, 2), (63, 8, 1), (64, 8, 3), (65, 8, 2), (511, 16, 2), (1000, 24, 3), (4096, 64, 1),
+         (5000, 128, 2), (64 * 64 * 3 + 17, 192, 3), (128 * 64 + 64 * 5, 1024, 2),
+         (8 * 1032 * 3 + 100, 1032, 2), (40000, 40, 1), (129 * 64, 8, 2)]
+
+
+def make_input(n, seed, kind):
+    if kind == "random":
+        return synth.random_bytes(n, seed)
+    if kind == "text":
+        return synth.text_like(n, seed)
+    w = 64
+    h = -(-n // (3 * w)) + 1
+    return synth.bitmap(h, w, 3, seed).reshape(-1)[:n]
+
+
+@pytest.mark.parametrize("n,W,L", SMALL)
+def test_dwt_fwd_inv_parity(dev, orc, n, W, L):
+    x = make_input(n, n + L, "random")
+    coef = se.dwt_fwd(to_dev(x, dev), W, L)
+    ref = orc.dwt_fwd(x, W, L)
+    assert np.array_equal(coef.cpu().numpy().astype(np.int32), ref)
+    back = se.dwt_inv(coef, n, W, L)
+    assert np.array_equal(back.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("kind", ["random", "bitmap", "text"])
+@pytest.mark.parametrize("n,W,L", SMALL)
+def test_protect_recover_parity(dev, orc, n, W, L, kind):
+    x = make_input(n, 7 * n + L, kind)
+    for flags in (0, se.FLAG_PUBLIC_PLAIN):
+        for block_offset in (0, 128 * 5):
+            a, b, c = se.fragment_protect(to_dev(x, dev), W, L, KEY, IV, flags=flags, block_offset=block_offset)
+            oa, ob, oc = orc.protect(x, W, L, KEY, IV, flags=flags, block_offset=block_offset)
+            assert np.array_equal(a.cpu().numpy(), oa), "A'"
+            assert np.array_equal(b.cpu().numpy(), ob), "B'"
+            assert np.array_equal(c.cpu().numpy(), oc), "C'"
+            back, rep = se.fragment_recover(a, b, c, n, W, L, KEY, IV, flags=flags, block_offset=block_offset)
+            assert np.array_equal(back.cpu().numpy(), x)
+            assert rep.cpu().tolist() == [-1, 0]
+
+
+def test_recover_of_oracle_fragments(dev, orc):
+    """The GPU recovers fragments produced by the oracle (and vice versa)."""
+    x = make_input(20000, 3, "bitmap")
+    oa, ob, oc = orc.protect(x, 160, 2, KEY, IV)
+    back, rep = se.fragment_recover(to_dev(oa, dev), to_dev(ob, dev), to_dev(oc, dev), x.size, 160, 2, KEY, IV)
+    assert np.array_equal(back.cpu().numpy(), x) and rep.cpu().tolist() == [-1, 0]
+
+
+def test_corruption_report_matches_oracle(dev, orc):
+    x = make_input(64 * 1024, 4, "bitmap")
+    W, L = 256, 2
+    a, b, c = orc.protect(x, W, L, KEY, IV)
+    bad_key = bytes([KEY[0] ^ 0x80]) + KEY[1:]
+    back, rep = se.fragment_recover(to_dev(a, dev), to_dev(b, dev), to_dev(c, dev), x.size, W, L, bad_key, IV)
+    oback, orep = orc.recover(a, b, c, x.size, W, L, bad_key, IV)
+    assert np.array_equal(back.cpu().numpy(), oback)
+    assert tuple(rep.cpu().tolist()) == orep and orep[1] > 0
+    # single flipped bit in C': confined to one block, same bytes as the oracle
+    c2 = c.copy()
+    c2[480 * 77 // 8 + 3] ^= 0x10
+    back, rep = se.fragment_recover(to_dev(a, dev), to_dev(b, dev), to_dev(c2, dev), x.size, W, L, KEY, IV)
+    oback, orep = orc.recover(a, b, c2, x.size, W, L, KEY, IV)
+    assert np.array_equal(back.cpu().numpy(), oback) and tuple(rep.cpu().tolist()) == orep
+
+
+@pytest.mark.parametrize("n", [0, 1, 15, 16, 17, 1000, 4096 + 7, 1 << 20])
+def test_cipher_parity(dev, orc, n):
+    x = synth.random_bytes(n, n)
+    for off in (0, 3, (1 << 64) - 2):
+        iv = bytes.fromhex("f0f1f2f3f4f5f6f7f8f9fafbfcfdfeff")
+        got = se.cipher_encrypt(KEY, iv, to_dev(x, dev), ctr_block_offset=off) if n else None
+        if n:
+            assert np.array_equal(got.cpu().numpy(), orc.aes128_ctr(KEY, iv, x, ctr_offset=off))
+            back = se.cipher_decrypt(KEY, iv, got, ctr_block_offset=off)
+            assert np.array_equal(back.cpu().numpy(), x)
+
+
+def test_launch_evidence(dev):
+    x = to_dev(synth.random_bytes(1 << 16, 1), dev)
+    se.launch_count(reset=True)
+    a, b, c = se.fragment_protect(x, 256, 2, KEY, IV)
+    se.fragment_recover(a, b, c, x.numel(), 256, 2, KEY, IV)
+    torch.cuda.synchronize()
+    assert se.launch_count() == 2
+
+
+# ---------------------------------------------------------------- full-size configs
+
+def sampled_ranges(nb, k=6, seed=0):
+    """k 128-block groups: first, last, and random ones in between."""
+    groups = (nb + 127) // 128
+    rng = np.random.default_rng(seed)
+    picks = {0, groups - 1} | set(int(g) for g in rng.integers(0, groups, size=k))
+    return [(g * 128, min(nb, (g + 1) * 128)) for g in sorted(picks)]
+
+
+def check_sampled(orc, x, W, L, a, b, c, iv, seed):
+    lay = orc.layout(x.size, W, L)
+    ha, hb, hc = a.cpu().numpy(), b.cpu().numpy(), c.cpu().numpy()
+    bits = (lay["a_bits"], lay["b_bits"], lay["c_bits"])
+    for b0, b1 in sampled_ranges(lay["n_blocks"], seed=seed):
+        bufs = [np.zeros(lay[k], np.uint8) for k in ("a_bytes", "b_bytes", "c_bytes")]
+        orc.protect(x, W, L, KEY, iv, block_range=(b0, b1), out=bufs)
+        for s, (got, ref) in enumerate(zip((ha, hb, hc), bufs)):
+            lo, hi = b0 * bits[s] // 8, -(-b1 * bits[s] // 8)
+            assert np.array_equal(got[lo:hi], ref[lo:hi]), ("stream", s, "blocks", b0, b1)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 33, 4])
+def test_config_full_size(dev, orc, cfg):
+    base = 4 if cfg == 4 else 3 if cfg == 33 else cfg
+    c = synth.CONFIGS[base]
+    x = synth.config_input(cfg)
+    W, L, iv = c["width"], c["levels"], synth.iv_for(base)
+    xt = to_dev(x, dev)
+    a, b, cc = se.fragment_protect(xt, W, L, KEY, iv)
+    if cfg in (1, 2):          # small enough for the whole oracle
+        oa, ob, oc = orc.protect(x, W, L, KEY, iv)
+        assert np.array_equal(a.cpu().numpy(), oa)
+        assert np.array_equal(b.cpu().numpy(), ob)
+        assert np.array_equal(cc.cpu().numpy(), oc)
+    else:
+        check_sampled(orc, x, W, L, a, b, cc, iv, seed=cfg)
+    back, rep = se.fragment_recover(a, b, cc, x.size, W, L, KEY, iv)
+    assert rep.cpu().tolist() == [-1, 0]
+    assert torch.equal(back, xt)
+    del a, b, cc, back, xt
+    torch.cuda.empty_cache()
