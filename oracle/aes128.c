@@ -128,11 +128,14 @@ static void counter_add(const uint8_t iv[16], uint64_t j, uint8_t out[16]) {
 
 void oracle_aes128_ctr(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_offset,
                        const uint8_t* in, uint8_t* out, uint64_t n) {
-    uint8_t sbox[256], w[176], ctr[16], ks[16];
+    uint8_t sbox[256], w[176], base[16], ctr[16], ks[16];
     oracle_aes128_sbox(sbox);
     key_expansion(key, sbox, w);
+    /* counter of block j = IV + ctr_offset + j, all mod 2^128 (two 128-bit adds,
+     * so ctr_offset + j may exceed 2^64) */
+    counter_add(iv, ctr_offset, base);
     for (uint64_t i = 0; i < n; i += 16) {
-        counter_add(iv, ctr_offset + i / 16, ctr);
+        counter_add(base, i / 16, ctr);
         cipher(w, sbox, ctr, ks);
         for (uint64_t k = 0; k < 16 && i + k < n; ++k) out[i + k] = in[i + k] ^ ks[k];
     }

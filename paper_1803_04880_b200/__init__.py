@@ -32,20 +32,42 @@ def sources():
     return [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libse.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile libse.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+    ``defines``/``out`` build a tuning variant (e.g. ("SE_MIN_CTAS=5",)) to
+    another in-tree path, selectable at load time with SE_LIB_PATH."""
+    target = out or LIB_PATH
     deps = sources() + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     deps.append(os.path.join(_ROOT, "include", "se.h"))
-    if not force and os.path.exists(LIB_PATH):
-        if os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(p) for p in deps):
-            return LIB_PATH
-    tmp = LIB_PATH + f".tmp{os.getpid()}"
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", tmp, *sources()]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd, cwd=CSRC)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    if not force and os.path.exists(target):
+        if os.path.getmtime(target) >= max(os.path.getmtime(p) for p in deps):
+            return target
+    # compile translation units in parallel, then link the shared library
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(_HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + f".{os.getpid()}.o")
+        cmd = ["nvcc", *compile_flags, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+        if r.returncode != 0 or verbose:
+            print(r.stdout + r.stderr)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}")
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    tmp = target + f".tmp{os.getpid()}"
+    subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
+    for o in objs:
+        os.remove(o)
+    os.replace(tmp, target)
+    return target
 
 
 class Geom(C.Structure):
@@ -78,9 +100,10 @@ def lib():
     """Load libse.so (raises if it was not built: there is no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"libse.so not built ({LIB_PATH}); run __graft_entry__.build()")
-        L = C.CDLL(LIB_PATH)
+        path = os.environ.get("SE_LIB_PATH", LIB_PATH)
+        if not os.path.exists(path):
+            raise RuntimeError(f"libse.so not built ({path}); run __graft_entry__.build()")
+        L = C.CDLL(path)
         vp, u8p = C.c_void_p, C.c_char_p
         gp = C.POINTER(Geom)
         L.fragment_layout.argtypes = [gp, C.POINTER(Layout)]

@@ -107,6 +107,7 @@ static void fill_fused(FusedParams& p, const se_geom* g, const se_layout& lay, c
     p.a_bytes = lay.a_bytes; p.b_bytes = lay.b_bytes; p.c_bytes = lay.c_bytes;
     p.width = g->width;
     p.bpr = g->width / 8;
+    p.one = 1;
     ctr_base(iv, g->block_offset * lay.a_bits / 128, p.ctr);
     key_expansion(key, p.rk);
     for (int i = 0; i < 4; ++i) { p.kiv[i] = be32(key + 4 * i); p.kiv[4 + i] = be32(iv + 4 * i); }
@@ -219,7 +220,7 @@ int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream) {
     memset(&p, 0, sizeof p);
     p.in = (const uint8_t*)d_in; p.coef = d_coef;
     p.n_bytes = g->n_bytes; p.n_blocks = lay.n_blocks;
-    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows;
+    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows; p.one = 1;
     return launch_dwt_fwd_block8(p, g->levels, stream) ? SE_ECUDA : SE_OK;
 }
 
@@ -235,7 +236,7 @@ int dwt_inv(const se_geom* g, const int16_t* d_coef, void* d_out, void* stream) 
     memset(&p, 0, sizeof p);
     p.out = (uint8_t*)d_out; p.coef = (int16_t*)d_coef;
     p.n_bytes = g->n_bytes; p.n_blocks = lay.n_blocks;
-    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows;
+    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows; p.one = 1;
     return launch_dwt_inv_block8(p, g->levels, stream) ? SE_ECUDA : SE_OK;
 }
 

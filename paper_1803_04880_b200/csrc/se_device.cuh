@@ -15,25 +15,46 @@
 #include <stdint.h>
 
 #include "se_internal.h"
+#include "sha2_device.cuh"
 #include "tables.h"
 
 namespace se {
 
+// ------------------------------------------------------------------ FMA-pipe integer ops
+// `one` is a kernel parameter equal to 1 that ptxas cannot fold, so these stay
+// IMADs and issue on the FMA pipe, leaving the ALU pipe (the path's limit:
+// SHF/LOP3 of SHA-2) free.  See sha2_device.cuh and DESIGN.md §5.
+__device__ __forceinline__ int iadd(int a, int b, uint32_t one) {
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+    return r;
+}
+__device__ __forceinline__ int isub(int a, int b, int m1) {       // a - b, m1 = -1 (opaque)
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(m1), "r"(a));
+    return r;
+}
+
 // ------------------------------------------------------------------ lifting
 // Forward 1-D lifting of n samples in place: output [s(0..n/2) | d(0..n/2)].
+// Samples are NOT centered: lifting commutes exactly with adding a constant
+// c to every sample (predict cancels it, update passes it through: both
+// floors see an integer shift), so centering (C8) only moves the final LL
+// band by -128 and is folded into the A-field offset (records) or applied to
+// LL alone (dwt_fwd).
 template <int N>
-__device__ __forceinline__ void lift_fwd(int (&x)[N]) {
+__device__ __forceinline__ void lift_fwd(int (&x)[N], uint32_t one, int m1) {
     constexpr int H = N / 2;
     int s[H], d[H];
 #pragma unroll
     for (int k = 0; k < H; ++k) {
-        const int right = (2 * k + 2 < N) ? x[2 * k + 2] : x[2 * k];   // x(N) = x(N-2)
-        d[k] = x[2 * k + 1] - ((x[2 * k] + right) >> 1);                  // Eq. 5.1
+        if (2 * k + 2 < N) d[k] = isub(x[2 * k + 1], iadd(x[2 * k], x[2 * k + 2], one) >> 1, m1);   // Eq. 5.1
+        else d[k] = isub(x[2 * k + 1], x[2 * k], m1);                 // x(N) = x(N-2)
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) {
-        const int dm1 = (k == 0) ? d[0] : d[k - 1];                       // d(-1) = d(0)
-        s[k] = x[2 * k] + ((dm1 + d[k] + 2) >> 2);                        // Eq. 5.2 (+)
+        const int dm1 = (k == 0) ? d[0] : d[k - 1];                   // d(-1) = d(0)
+        s[k] = iadd(x[2 * k], iadd(iadd(dm1, d[k], one), 2, one) >> 2, one);   // Eq. 5.2 (+)
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) { x[k] = s[k]; x[H + k] = d[k]; }
@@ -41,18 +62,18 @@ __device__ __forceinline__ void lift_fwd(int (&x)[N]) {
 
 // Exact inverse: undo the update, then undo the predict.
 template <int N>
-__device__ __forceinline__ void lift_inv(int (&y)[N]) {
+__device__ __forceinline__ void lift_inv(int (&y)[N], uint32_t one, int m1) {
     constexpr int H = N / 2;
     int x[N];
 #pragma unroll
     for (int k = 0; k < H; ++k) {
         const int dm1 = (k == 0) ? y[H] : y[H + k - 1];
-        x[2 * k] = y[k] - ((dm1 + y[H + k] + 2) >> 2);
+        x[2 * k] = isub(y[k], iadd(iadd(dm1, y[H + k], one), 2, one) >> 2, m1);
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) {
-        const int right = (2 * k + 2 < N) ? x[2 * k + 2] : x[2 * k];
-        x[2 * k + 1] = y[H + k] + ((x[2 * k] + right) >> 1);
+        if (2 * k + 2 < N) x[2 * k + 1] = iadd(y[H + k], iadd(x[2 * k], x[2 * k + 2], one) >> 1, one);
+        else x[2 * k + 1] = iadd(y[H + k], x[2 * k], one);
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) y[k] = x[k];
@@ -60,13 +81,13 @@ __device__ __forceinline__ void lift_inv(int (&y)[N]) {
 
 // One 2-D level on the top-left M x M region: rows, then columns (C5).
 template <int M>
-__device__ __forceinline__ void dwt2_level_fwd(int (&v)[8][8]) {
+__device__ __forceinline__ void dwt2_level_fwd(int (&v)[8][8], uint32_t one, int m1) {
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         int t[M];
 #pragma unroll
         for (int j = 0; j < M; ++j) t[j] = v[i][j];
-        lift_fwd<M>(t);
+        lift_fwd<M>(t, one, m1);
 #pragma unroll
         for (int j = 0; j < M; ++j) v[i][j] = t[j];
     }
@@ -75,20 +96,20 @@ __device__ __forceinline__ void dwt2_level_fwd(int (&v)[8][8]) {
         int t[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) t[i] = v[i][j];
-        lift_fwd<M>(t);
+        lift_fwd<M>(t, one, m1);
 #pragma unroll
         for (int i = 0; i < M; ++i) v[i][j] = t[i];
     }
 }
 
 template <int M>
-__device__ __forceinline__ void dwt2_level_inv(int (&v)[8][8]) {
+__device__ __forceinline__ void dwt2_level_inv(int (&v)[8][8], uint32_t one, int m1) {
 #pragma unroll
     for (int j = 0; j < M; ++j) {
         int t[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) t[i] = v[i][j];
-        lift_inv<M>(t);
+        lift_inv<M>(t, one, m1);
 #pragma unroll
         for (int i = 0; i < M; ++i) v[i][j] = t[i];
     }
@@ -97,24 +118,26 @@ __device__ __forceinline__ void dwt2_level_inv(int (&v)[8][8]) {
         int t[M];
 #pragma unroll
         for (int j = 0; j < M; ++j) t[j] = v[i][j];
-        lift_inv<M>(t);
+        lift_inv<M>(t, one, m1);
 #pragma unroll
         for (int j = 0; j < M; ++j) v[i][j] = t[j];
     }
 }
 
 template <int L>
-__device__ __forceinline__ void dwt8_fwd(int (&v)[8][8]) {
-    dwt2_level_fwd<8>(v);
-    if (L >= 2) dwt2_level_fwd<4>(v);
-    if (L >= 3) dwt2_level_fwd<2>(v);
+__device__ __forceinline__ void dwt8_fwd(int (&v)[8][8], uint32_t one) {
+    const int m1 = -(int)one;
+    dwt2_level_fwd<8>(v, one, m1);
+    if (L >= 2) dwt2_level_fwd<4>(v, one, m1);
+    if (L >= 3) dwt2_level_fwd<2>(v, one, m1);
 }
 
 template <int L>
-__device__ __forceinline__ void dwt8_inv(int (&v)[8][8]) {
-    if (L >= 3) dwt2_level_inv<2>(v);
-    if (L >= 2) dwt2_level_inv<4>(v);
-    dwt2_level_inv<8>(v);
+__device__ __forceinline__ void dwt8_inv(int (&v)[8][8], uint32_t one) {
+    const int m1 = -(int)one;
+    if (L >= 3) dwt2_level_inv<2>(v, one, m1);
+    if (L >= 2) dwt2_level_inv<4>(v, one, m1);
+    dwt2_level_inv<8>(v, one, m1);
 }
 
 // ------------------------------------------------------------------ records
@@ -130,26 +153,45 @@ struct Rec {
     static constexpr int BBYTES = (BBITS + 7) / 8;
 };
 
-// OR a w-bit field u (already offset-binary, < 2^w) at MSB-first bit `pos`.
+// Place value v as a w-bit offset-binary field u = v + off (C9) at MSB-first
+// bit `pos`.  Fields never overlap, so OR == ADD and a field inside one word
+// is one multiply-add by an (opaque) power of two on the FMA pipe; a field
+// straddling two words costs one shift on the ALU pipe.
 template <int NW>
-__device__ __forceinline__ void put_field(uint32_t (&r)[NW], int pos, uint32_t u, int w) {
+__device__ __forceinline__ void put_field(uint32_t (&r)[NW], int pos, int v, int off, int w, uint32_t one) {
     const int word = pos >> 5, end = (pos & 31) + w;
+    const uint32_t u = (uint32_t)iadd(v, off, one);
     if (end <= 32) {
-        r[word] |= u << (32 - end);
+        uint32_t t;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(u), "r"(one << (32 - end)), "r"(r[word]));
+        r[word] = t;
     } else {
         r[word] |= u >> (end - 32);
-        r[word + 1] |= u << (64 - end);
+        uint32_t t;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(u), "r"(one << (64 - end)), "r"(r[word + 1]));
+        r[word + 1] = t;
     }
 }
 
+// Inverse: v = field - off.  A field at the top of its word is one IMAD.HI
+// (r * 2^w) >> 32 with the -off folded in as the addend; elsewhere the
+// field is isolated with one LOP3 and shifted down by IMAD.HI.
 template <int NW>
-__device__ __forceinline__ int get_field(const uint32_t (&r)[NW], int pos, int w) {
-    const int word = pos >> 5, end = (pos & 31) + w;
-    uint32_t u;
-    if (end <= 32) u = r[word] >> (32 - end);
-    else u = (r[word] << (end - 32)) | (r[word + 1] >> (64 - end));
-    u &= (1u << w) - 1u;
-    return (int)u - (1 << (w - 1));
+__device__ __forceinline__ int get_field(const uint32_t (&r)[NW], int pos, int off, int w, uint32_t one) {
+    const int word = pos >> 5, start = pos & 31, end = start + w;
+    int v;
+    if (end <= 32) {
+        const uint32_t masked = (start == 0) ? r[word] : (r[word] & (0xffffffffu >> start));
+        if (end == 32) {
+            v = isub((int)masked, off, -(int)one);
+        } else {
+            asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(v) : "r"(masked), "r"(one << end), "r"(-off));
+        }
+    } else {
+        const uint32_t u = ((r[word] << (end - 32)) | (r[word + 1] >> (64 - end))) & ((1u << w) - 1u);
+        v = isub((int)u, off, -(int)one);
+    }
+    return v;
 }
 
 // Visit every field of the three records in the canonical order (C10):
@@ -193,77 +235,6 @@ __device__ __forceinline__ void for_each_field(F&& f) {
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) { f(2, pos, 4 + i, 4 + j, 10); pos += 10; }
-}
-
-// ------------------------------------------------------------------ SHA-2
-__device__ __forceinline__ uint32_t rotr32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
-
-__device__ __forceinline__ uint64_t rotr64(uint64_t x, int n) {
-    const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
-    uint32_t nlo, nhi;
-    if (n < 32) { nlo = __funnelshift_r(lo, hi, n); nhi = __funnelshift_r(hi, lo, n); }
-    else { nlo = __funnelshift_r(hi, lo, n - 32); nhi = __funnelshift_r(lo, hi, n - 32); }
-    return ((uint64_t)nhi << 32) | nlo;
-}
-
-// per-translation-unit copies (no relocatable device code needed)
-static __constant__ uint32_t c_sha256_k[64] = SE_SHA256_K_INIT;
-static __constant__ uint64_t c_sha512_k[80] = SE_SHA512_K_INIT;
-
-// SHA-256 over one 64-byte block whose words W[0..7] were already consumed
-// by the host midstate.  st = state after round 7; h0 = initial hash value.
-// Returns the digest words in H.
-__device__ __forceinline__ void sha256_from_round8(const uint32_t (&st)[8], const uint32_t (&h0)[8],
-                                                   uint32_t (&W)[16], uint32_t (&H)[8]) {
-    uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
-#pragma unroll
-    for (int t = 8; t < 64; ++t) {
-        uint32_t w;
-        if (t < 16) {
-            w = W[t];
-        } else {
-            const uint32_t w2 = W[(t - 2) & 15], w15 = W[(t - 15) & 15];
-            const uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
-            const uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
-            w = s1 + W[(t - 7) & 15] + s0 + W[t & 15];
-            W[t & 15] = w;
-        }
-        const uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
-        const uint32_t ch = (e & f) ^ (~e & g);
-        const uint32_t t1 = h + S1 + ch + c_sha256_k[t] + w;
-        const uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
-        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
-        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
-    }
-    H[0] = h0[0] + a; H[1] = h0[1] + b; H[2] = h0[2] + c; H[3] = h0[3] + d;
-    H[4] = h0[4] + e; H[5] = h0[5] + f; H[6] = h0[6] + g; H[7] = h0[7] + h;
-}
-
-// SHA-512 resuming after round 3 (W[0..3] = K||IV consumed by the host).
-__device__ __forceinline__ void sha512_from_round4(const uint64_t (&st)[8], const uint64_t (&h0)[8],
-                                                   uint64_t (&W)[16], uint64_t (&H)[8]) {
-    uint64_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
-#pragma unroll
-    for (int t = 4; t < 80; ++t) {
-        uint64_t w;
-        if (t < 16) {
-            w = W[t];
-        } else {
-            const uint64_t w2 = W[(t - 2) & 15], w15 = W[(t - 15) & 15];
-            const uint64_t s1 = rotr64(w2, 19) ^ rotr64(w2, 61) ^ (w2 >> 6);
-            const uint64_t s0 = rotr64(w15, 1) ^ rotr64(w15, 8) ^ (w15 >> 7);
-            w = s1 + W[(t - 7) & 15] + s0 + W[t & 15];
-            W[t & 15] = w;
-        }
-        const uint64_t S1 = rotr64(e, 14) ^ rotr64(e, 18) ^ rotr64(e, 41);
-        const uint64_t ch = (e & f) ^ (~e & g);
-        const uint64_t t1 = h + S1 + ch + c_sha512_k[t] + w;
-        const uint64_t S0 = rotr64(a, 28) ^ rotr64(a, 34) ^ rotr64(a, 39);
-        const uint64_t mj = (a & b) ^ (a & c) ^ (b & c);
-        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
-    }
-    H[0] = h0[0] + a; H[1] = h0[1] + b; H[2] = h0[2] + c; H[3] = h0[3] + d;
-    H[4] = h0[4] + e; H[5] = h0[5] + f; H[6] = h0[6] + g; H[7] = h0[7] + h;
 }
 
 // ------------------------------------------------------------------ AES

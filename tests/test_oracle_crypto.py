@@ -59,6 +59,18 @@ def test_ctr_random_vs_openssl(orc):
         assert orc.aes128_ctr(key, iv, data).tobytes() == enc.update(data) + enc.finalize()
 
 
+@pytest.mark.parametrize("offset", [3, (1 << 64) - 2, (1 << 64) - 1])
+def test_ctr_offset_is_128_bit(orc, offset):
+    """SP 800-38A: counter = IV + j mod 2^128, also when IV + offset + j crosses 2^64."""
+    from cryptography.hazmat.primitives.ciphers import Cipher, algorithms, modes
+    key = bytes(range(16))
+    iv = bytes.fromhex("f0f1f2f3f4f5f6f7f8f9fafbfcfdfeff")
+    start = ((int.from_bytes(iv, "big") + offset) % (1 << 128)).to_bytes(16, "big")
+    data = bytes(range(200))
+    enc = Cipher(algorithms.AES(key), modes.CTR(start)).encryptor()
+    assert orc.aes128_ctr(key, iv, data, ctr_offset=offset).tobytes() == enc.update(data)
+
+
 def test_sha_fips180_vectors(orc):
     for ln in golden_lines("fips180_4_sha.txt"):
         alg, msg, dig = ln.split()
