@@ -109,31 +109,36 @@ int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
                      se_report* d_report, void* stream);
 
 /* ---- batched protect / recover (many independent files, one launch) -----
- * d_jobs: device array of n_jobs descriptors.  cta_begin must be the
- * exclusive prefix sum over jobs of ceil(n_blocks_j / 128) (fragment_batch_plan
- * computes it host-side); total_ctas is the sum.  Every job shares key,
- * levels and flags; each has its own IV and block_offset. */
+ * "batch of 10,000 mixed-size files ... sharded by file" (BASELINE.json C5;
+ * the paper's chunks D_i are independent).  The caller fills one
+ * se_job per file in HOST memory (pointers are device pointers; IV per file),
+ * calls fragment_batch_plan (host, pure: validates every job, assigns each its
+ * first CTA and derives the per-file counter base and SHA midstates into
+ * `derived`), copies the array to device memory, then launches.  All jobs of
+ * a batch share the key, levels and flags.  Mode is BLOCK8. */
 typedef struct {
-    const uint8_t* in;        /* protect: input;  recover: output (cast)      */
-    uint8_t* out;             /* recover: output bytes (protect: unused)      */
-    uint8_t *a, *b, *c;       /* fragment streams                             */
+    const uint8_t* in;        /* protect: input bytes (device)                */
+    uint8_t* out;             /* recover: output bytes (device)               */
+    uint8_t *a, *b, *c;       /* fragment streams (device), sized per layout  */
     uint64_t n_bytes;
-    uint64_t block_offset;
-    uint64_t cta_begin;       /* first CTA of this job in the launch           */
-    uint32_t width;
-    uint32_t pad_;
+    uint64_t block_offset;    /* as se_geom.block_offset                      */
+    uint32_t width;           /* matrix width W of this file                  */
+    uint32_t reserved0;
     uint8_t iv[16];
+    uint64_t cta_begin;       /* set by fragment_batch_plan                   */
+    uint32_t derived[36];     /* set by fragment_batch_plan (library-private) */
 } se_job;
 
-/* Fill width-independent fields of jobs[i].cta_begin and return total CTAs
- * (host helper, pure). Returns -1 on invalid geometry. */
-int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels);
+/* Returns the total number of CTAs of the launch (>= 0), or a negative
+ * se_status (SE_EINVAL: bad geometry / alignment / pointers in a job). */
+int64_t fragment_batch_plan(se_job* h_jobs, uint32_t n_jobs, uint32_t levels, const uint8_t key[16]);
 int fragment_protect_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas,
                            uint32_t levels, uint32_t flags, const uint8_t key[16],
                            void* stream);
+/* d_reports: nullable device array of n_jobs reports (one per file). */
 int fragment_recover_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas,
                            uint32_t levels, uint32_t flags, const uint8_t key[16],
-                           se_report* d_report, void* stream);
+                           se_report* d_reports, void* stream);
 
 /* ---- host-resident streaming protect / recover (NEXT row f1) -------------
  * h_* are HOST buffers (pinned or pageable).  The library stages chunks of

@@ -84,8 +84,8 @@ class Layout(C.Structure):
 class Job(C.Structure):
     _fields_ = [("in_", C.c_void_p), ("out", C.c_void_p), ("a", C.c_void_p), ("b", C.c_void_p),
                 ("c", C.c_void_p), ("n_bytes", C.c_uint64), ("block_offset", C.c_uint64),
-                ("cta_begin", C.c_uint64), ("width", C.c_uint32), ("pad_", C.c_uint32),
-                ("iv", C.c_uint8 * 16)]
+                ("width", C.c_uint32), ("reserved0", C.c_uint32), ("iv", C.c_uint8 * 16),
+                ("cta_begin", C.c_uint64), ("derived", C.c_uint32 * 36)]
 
 
 SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_batch_plan",
@@ -109,7 +109,7 @@ def lib():
         L.fragment_layout.argtypes = [gp, C.POINTER(Layout)]
         L.fragment_protect.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp]
         L.fragment_recover.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp, vp]
-        L.fragment_batch_plan.argtypes = [C.POINTER(Job), C.c_uint32, C.c_uint32]
+        L.fragment_batch_plan.argtypes = [C.POINTER(Job), C.c_uint32, C.c_uint32, u8p]
         L.fragment_batch_plan.restype = C.c_int64
         L.fragment_protect_batch.argtypes = [C.c_uint32, vp, C.c_uint64, C.c_uint32, C.c_uint32, u8p, vp]
         L.fragment_recover_batch.argtypes = [C.c_uint32, vp, C.c_uint64, C.c_uint32, C.c_uint32, u8p, vp, vp]
@@ -233,3 +233,52 @@ def cipher_decrypt(key, iv, x, ctr_block_offset: int = 0, out=None, stream=None)
 
 def launch_count(reset: bool = False) -> int:
     return int(lib().se_launch_count(1 if reset else 0))
+
+
+# ---------------------------------------------------------------- batches of files (C5)
+
+class Batch:
+    """Device-resident job table for fragment_protect_batch / fragment_recover_batch.
+
+    files: list of 1-D uint8 CUDA tensors (inputs); widths: per-file W; ivs:
+    per-file 16-byte IVs.  Allocates the fragment streams (and recover
+    outputs) and plans the launch with fragment_batch_plan."""
+
+    def __init__(self, files, widths, ivs, levels: int, key, flags: int = 0, block_offsets=None):
+        import torch
+        self.levels, self.flags, self.key = int(levels), int(flags), _bytes16(key, "key")
+        self.files = list(files)
+        n = len(self.files)
+        dev = self.files[0].device if n else torch.device("cuda")
+        self.jobs = (Job * max(n, 1))()
+        self.outs, self.streams = [], []
+        for i, (x, w, iv) in enumerate(zip(self.files, widths, ivs)):
+            lay = fragment_layout(x.numel(), w, levels)
+            a, b, c = _empty(lay["a_bytes"], dev), _empty(lay["b_bytes"], dev), _empty(lay["c_bytes"], dev)
+            o = _empty(x.numel(), dev)
+            self.streams.append((a, b, c))
+            self.outs.append(o)
+            j = self.jobs[i]
+            j.in_, j.out = x.data_ptr(), o.data_ptr()
+            j.a, j.b, j.c = a.data_ptr(), (b.data_ptr() if b.numel() else 0), c.data_ptr()
+            j.n_bytes, j.width = x.numel(), int(w)
+            j.block_offset = int(block_offsets[i]) if block_offsets is not None else 0
+            j.iv[:] = list(_bytes16(iv, "iv"))
+        total = lib().fragment_batch_plan(self.jobs, n, self.levels, self.key)
+        if total < 0:
+            raise SEError(int(total), "fragment_batch_plan")
+        self.total_ctas = int(total)
+        self.n = n
+        raw = bytes(C.string_at(C.addressof(self.jobs), C.sizeof(Job) * max(n, 1)))
+        self.d_jobs = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
+        self.reports = torch.empty((max(n, 1), 2), dtype=torch.int64, device=dev)
+
+    def protect(self, stream=None):
+        _check(lib().fragment_protect_batch(self.n, _ptr(self.d_jobs), self.total_ctas, self.levels, self.flags,
+                                            self.key, _stream(stream)), "fragment_protect_batch")
+        return self.streams
+
+    def recover(self, stream=None):
+        _check(lib().fragment_recover_batch(self.n, _ptr(self.d_jobs), self.total_ctas, self.levels, self.flags,
+                                            self.key, _ptr(self.reports), _stream(stream)), "fragment_recover_batch")
+        return self.outs, self.reports[: self.n]

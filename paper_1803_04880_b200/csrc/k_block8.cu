@@ -228,9 +228,10 @@ __device__ __forceinline__ void mask_c(const FusedParams& p, uint64_t gb, const 
 
 // ---------------------------------------------------------------- protect
 
+// One CTA of protect: 128 consecutive blocks starting at local block cta*128
+// of the file described by p (kernel parameters, or a batch job in smem).
 template <int L, bool MASK>
-__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
-k_protect_block8(const __grid_constant__ FusedParams p) {
+__device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L>;
     constexpr int SA_W = 4 * R::ABITS;             // 16*ABITS bytes per CTA
     constexpr int SB_W = R::BBITS ? 4 * R::BBITS : 4;
@@ -242,7 +243,6 @@ k_protect_block8(const __grid_constant__ FusedParams p) {
     __shared__ __align__(16) uint32_t sc[SC_W];
 
     const int tid = threadIdx.x;
-    const uint64_t cta = blockIdx.x;
     const uint64_t blk = cta * kBlocksPerCta + tid;
     for (int i = tid; i < SA_W; i += kBlocksPerCta) sa[i] = 0;
     for (int i = tid; i < SB_W; i += kBlocksPerCta) sb[i] = 0;
@@ -300,8 +300,7 @@ k_protect_block8(const __grid_constant__ FusedParams p) {
 // ---------------------------------------------------------------- recover
 
 template <int L, bool MASK>
-__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
-k_recover_block8(const __grid_constant__ FusedParams p) {
+__device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L>;
     constexpr int SA_W = 4 * R::ABITS;
     constexpr int SB_W = R::BBITS ? 4 * R::BBITS : 4;
@@ -314,7 +313,6 @@ k_recover_block8(const __grid_constant__ FusedParams p) {
     __shared__ unsigned int s_bad;
 
     const int tid = threadIdx.x;
-    const uint64_t cta = blockIdx.x;
     const uint64_t blk = cta * kBlocksPerCta + tid;
     const uint64_t a0 = cta * 16ull * R::ABITS, c0 = cta * 16ull * R::CBITS;
     if (tid == 0) { s_first = ~0ull; s_bad = 0; }
@@ -375,6 +373,83 @@ k_recover_block8(const __grid_constant__ FusedParams p) {
             atomicAdd(reinterpret_cast<unsigned long long*>(&p.report->bad_blocks), (unsigned long long)s_bad);
         }
     }
+}
+
+// ---------------------------------------------------------------- kernels
+
+template <int L, bool MASK>
+__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
+k_protect_block8(const __grid_constant__ FusedParams p) {
+    protect_cta<L, MASK>(p, blockIdx.x);
+}
+
+template <int L, bool MASK>
+__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
+k_recover_block8(const __grid_constant__ FusedParams p) {
+    recover_cta<L, MASK>(p, blockIdx.x);
+}
+
+// Many independent files in one launch (C5; SURVEY §8.6 "sharded by file").
+// Each CTA finds its job by binary search over cta_begin, assembles that job's
+// parameters in shared memory (the per-job counter base and SHA midstates were
+// derived on the host by fragment_batch_plan) and runs the same CTA body.
+template <int L, bool MASK, bool RECOVER>
+__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
+k_batch_block8(const __grid_constant__ BatchParams bp) {
+    __shared__ FusedParams sp;
+    __shared__ uint32_t s_job;
+    using R = Rec<L>;
+    const uint32_t x = blockIdx.x;
+    if (threadIdx.x == 0) {
+        uint32_t lo = 0, hi = bp.n_jobs - 1;          // largest j with cta_begin <= x
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) / 2;
+            if (bp.jobs[mid].cta_begin <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        s_job = lo;
+    }
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(&bp.base);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&sp);
+        for (uint32_t i = threadIdx.x; i < sizeof(FusedParams) / 4; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const se_job& job = bp.jobs[s_job];
+    const JobDerived& dv = *reinterpret_cast<const JobDerived*>(job.derived);
+    const uint32_t t = threadIdx.x;
+    if (t == 0) {
+        sp.in = job.in;
+        sp.out = job.out;
+        sp.a = job.a; sp.b = job.b; sp.c = job.c;
+        sp.report = bp.reports ? bp.reports + s_job : nullptr;
+        sp.n_bytes = job.n_bytes;
+        sp.width = job.width;
+        sp.bpr = job.width / 8;
+        const uint64_t rows = ((job.n_bytes + job.width - 1) / job.width + 7) / 8 * 8;
+        sp.n_blocks = rows / 8 * sp.bpr;
+        sp.block_offset = job.block_offset;
+        sp.a_bytes = (sp.n_blocks * R::ABITS + 7) / 8;
+        sp.b_bytes = (sp.n_blocks * R::BBITS + 7) / 8;
+        sp.c_bytes = (sp.n_blocks * R::CBITS + 7) / 8;
+    } else if (t >= 32 && t < 36) {
+        sp.ctr[t - 32] = dv.ctr[t - 32];
+    } else if (t >= 36 && t < 44) {
+        sp.kiv[t - 36] = dv.kiv[t - 36];
+    } else if (t >= 44 && t < 52) {
+        sp.mid256[t - 44] = dv.mid256[t - 44];
+    } else if (t >= 52 && t < 60) {
+        sp.mid512[t - 52] = dv.mid512[t - 52];
+    }
+    __syncthreads();
+    const uint64_t cta = x - job.cta_begin;
+    if (RECOVER) recover_cta<L, MASK>(sp, cta);
+    else protect_cta<L, MASK>(sp, cta);
+}
+
+__global__ void k_report_init(se_report* r, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) { r[i].first_bad_block = -1; r[i].bad_blocks = 0; }
 }
 
 // ---------------------------------------------------------------- transform only
@@ -459,6 +534,33 @@ int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void
     if (levels == 1) recover_l<1>(p, mask, s);
     else if (levels == 2) recover_l<2>(p, mask, s);
     else recover_l<3>(p, mask, s);
+    note_launch();
+    return (int)cudaGetLastError();
+}
+
+template <int L, bool RECOVER>
+static void batch_l(const BatchParams& bp, uint64_t ctas, bool mask, cudaStream_t s) {
+    if (mask) k_batch_block8<L, true, RECOVER><<<(unsigned)ctas, kBlocksPerCta, 0, s>>>(bp);
+    else k_batch_block8<L, false, RECOVER><<<(unsigned)ctas, kBlocksPerCta, 0, s>>>(bp);
+}
+
+int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,
+                        void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (recover && bp.reports) {
+        k_report_init<<<(bp.n_jobs + 255) / 256, 256, 0, s>>>(bp.reports, bp.n_jobs);
+        note_launch();
+    }
+    if (total_ctas == 0) return (int)cudaGetLastError();
+    if (recover) {
+        if (levels == 1) batch_l<1, true>(bp, total_ctas, mask, s);
+        else if (levels == 2) batch_l<2, true>(bp, total_ctas, mask, s);
+        else batch_l<3, true>(bp, total_ctas, mask, s);
+    } else {
+        if (levels == 1) batch_l<1, false>(bp, total_ctas, mask, s);
+        else if (levels == 2) batch_l<2, false>(bp, total_ctas, mask, s);
+        else batch_l<3, false>(bp, total_ctas, mask, s);
+    }
     note_launch();
     return (int)cudaGetLastError();
 }

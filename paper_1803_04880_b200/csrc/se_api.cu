@@ -259,18 +259,61 @@ int cipher_decrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_blo
     return cipher_encrypt(key, iv, ctr_block_offset, d_in, d_out, n, stream);
 }
 
-int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels) {
-    (void)jobs; (void)n_jobs; (void)levels;
-    return SE_ENOTSUP;
+int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels, const uint8_t key[16]) {
+    if (!jobs || !key || levels < 1 || levels > 3) return SE_EINVAL;
+    uint64_t cta = 0;
+    for (uint32_t j = 0; j < n_jobs; ++j) {
+        se_job& job = jobs[j];
+        se_geom g = {job.n_bytes, job.width, levels, SE_MODE_BLOCK8, 0, job.block_offset};
+        se_layout lay;
+        if (fragment_layout(&g, &lay) != SE_OK) return SE_EINVAL;
+        if ((job.block_offset * lay.a_bits) % 128) return SE_EINVAL;
+        if (job.n_bytes && (!job.a || !job.c || (lay.b_bytes && !job.b))) return SE_EINVAL;
+        job.cta_begin = cta;
+        cta += (lay.n_blocks + kBlocksPerCta - 1) / kBlocksPerCta;
+        // per-file constants: counter base and SHA midstates over K || IV (C13, C15)
+        FusedParams p;
+        fill_fused(p, &g, lay, key, job.iv);
+        JobDerived d;
+        memcpy(d.ctr, p.ctr, sizeof d.ctr);
+        memcpy(d.kiv, p.kiv, sizeof d.kiv);
+        memcpy(d.mid256, p.mid256, sizeof d.mid256);
+        memcpy(d.mid512, p.mid512, sizeof d.mid512);
+        memset(job.derived, 0, sizeof job.derived);
+        memcpy(job.derived, &d, sizeof d);
+    }
+    if (cta > 0x7fffffffull) return SE_EINVAL;       // one launch: grid.x < 2^31
+    return (int64_t)cta;
 }
 
-int fragment_protect_batch(uint32_t, const se_job*, uint64_t, uint32_t, uint32_t, const uint8_t*, void*) {
-    return SE_ENOTSUP;
+static int batch_common(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas, uint32_t levels,
+                        uint32_t flags, const uint8_t key[16], se_report* d_reports, bool recover, void* stream) {
+    if (!key || levels < 1 || levels > 3 || (flags & ~(uint32_t)SE_FLAG_PUBLIC_PLAIN)) return SE_EINVAL;
+    if (n_jobs == 0) return SE_OK;
+    if (!d_jobs) return SE_EINVAL;
+    if (!aligned16(d_jobs)) return SE_EALIGN;
+    BatchParams bp;
+    memset(&bp, 0, sizeof bp);
+    bp.jobs = d_jobs;
+    bp.reports = d_reports;
+    bp.n_jobs = n_jobs;
+    se_geom g = {0, 8, levels, SE_MODE_BLOCK8, flags, 0};
+    se_layout lay;
+    fragment_layout(&g, &lay);
+    const uint8_t zero_iv[16] = {0};
+    fill_fused(bp.base, &g, lay, key, zero_iv);       // shared fields: round keys, H(0), one
+    const bool mask = !(flags & SE_FLAG_PUBLIC_PLAIN);
+    return launch_batch_block8(bp, total_ctas, levels, mask, recover, stream) ? SE_ECUDA : SE_OK;
 }
 
-int fragment_recover_batch(uint32_t, const se_job*, uint64_t, uint32_t, uint32_t, const uint8_t*, se_report*,
-                           void*) {
-    return SE_ENOTSUP;
+int fragment_protect_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas, uint32_t levels,
+                           uint32_t flags, const uint8_t key[16], void* stream) {
+    return batch_common(n_jobs, d_jobs, total_ctas, levels, flags, key, nullptr, false, stream);
+}
+
+int fragment_recover_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas, uint32_t levels,
+                           uint32_t flags, const uint8_t key[16], se_report* d_reports, void* stream) {
+    return batch_common(n_jobs, d_jobs, total_ctas, levels, flags, key, d_reports, true, stream);
 }
 
 int fragment_protect_host(const se_geom*, const uint8_t*, const uint8_t*, const void*, void*, void*, void*,

@@ -34,6 +34,23 @@ struct FusedParams {
     uint64_t h512[8];         // SHA-512 H(0)
 };
 
+// Library-private layout of se_job.derived[] (filled by fragment_batch_plan).
+struct JobDerived {
+    uint32_t ctr[4];          // IV + block_offset*a_bits/128
+    uint32_t kiv[8];          // K || IV words
+    uint32_t mid256[8];       // SHA-256 midstate over K||IV
+    uint64_t mid512[8];       // SHA-512 midstate over K||IV
+};
+static_assert(sizeof(JobDerived) <= sizeof(((se_job*)0)->derived), "se_job.derived too small");
+
+struct BatchParams {
+    const se_job* jobs;       // device array, sorted by cta_begin
+    se_report* reports;       // recover: one per job, nullable
+    uint32_t n_jobs;
+    uint32_t pad_;
+    FusedParams base;         // shared fields: rk, h256, h512, one
+};
+
 struct CipherParams {
     const uint8_t* in;
     uint8_t* out;
@@ -57,6 +74,8 @@ struct DwtParams {
 // launchers (return cudaError_t as int)
 int launch_protect_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
 int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
+int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,
+                        void* stream);
 int launch_dwt_fwd_block8(const DwtParams& p, uint32_t levels, void* stream);
 int launch_dwt_inv_block8(const DwtParams& p, uint32_t levels, void* stream);
 int launch_cipher_ctr(const CipherParams& p, void* stream);

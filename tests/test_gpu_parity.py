@@ -166,3 +166,70 @@ def test_config_full_size(dev, orc, cfg):
     assert torch.equal(back, xt)
     del a, b, cc, back, xt
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- batches (C5) and stripes (row e)
+
+def c5_subset(count, seed, max_size):
+    rng = np.random.default_rng(seed)
+    sizes = np.exp(rng.uniform(np.log(1024), np.log(max_size), size=count)).astype(np.int64)
+    sizes[0] = 1                      # degenerate: one byte
+    sizes[1] = 64 * 1024              # exact power-of-two file
+    return [synth.c5_file(i, int(s)) for i, s in enumerate(sizes)]
+
+
+@pytest.mark.parametrize("levels,flags", [(2, 0), (3, 0), (1, 0), (2, 1)])
+def test_batch_files_parity(dev, orc, levels, flags):
+    files = c5_subset(24, 50 + levels, 1 << 20)
+    widths = [synth.width_rule(f.size) for f in files]
+    ivs = [synth.iv_for(5, i) for i in range(len(files))]
+    batch = se.Batch([to_dev(f, dev) for f in files], widths, ivs, levels, KEY, flags=flags)
+    streams = batch.protect()
+    for f, w, iv, (a, b, c) in zip(files, widths, ivs, streams):
+        oa, ob, oc = orc.protect(f, w, levels, KEY, iv, flags=flags)
+        assert np.array_equal(a.cpu().numpy(), oa)
+        assert np.array_equal(b.cpu().numpy(), ob)
+        assert np.array_equal(c.cpu().numpy(), oc)
+    outs, reps = batch.recover()
+    for f, o in zip(files, outs):
+        assert np.array_equal(o.cpu().numpy(), f)
+    assert (reps.cpu().numpy() == np.array([-1, 0])).all()
+
+
+def test_batch_reports_per_file(dev, orc):
+    files = c5_subset(6, 7, 1 << 18)
+    widths = [synth.width_rule(f.size) for f in files]
+    ivs = [synth.iv_for(5, i) for i in range(len(files))]
+    batch = se.Batch([to_dev(f, dev) for f in files], widths, ivs, 2, KEY)
+    streams = batch.protect()
+    # corrupt file 3's private fragment: only its report may flag blocks
+    streams[3][0][0] ^= 0xFF
+    outs, reps = batch.recover()
+    r = reps.cpu().numpy()
+    oback, orep = orc.recover(streams[3][0].cpu().numpy(), streams[3][1].cpu().numpy(), streams[3][2].cpu().numpy(),
+                              files[3].size, widths[3], 2, KEY, ivs[3])
+    assert tuple(r[3]) == orep
+    assert np.array_equal(outs[3].cpu().numpy(), oback)
+    for i in range(len(files)):
+        if i != 3:
+            assert tuple(r[i]) == (-1, 0) and np.array_equal(outs[i].cpu().numpy(), files[i])
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_virtual_stripes_equal_whole(dev, world):
+    """Row-stripe sharding run serially on one GPU: the concatenated stripe
+    streams equal the whole-file streams (what each of `world` GPUs computes)."""
+    from paper_1803_04880_b200 import shard
+    n, W, L = 8 * 1024 * 1024 + 12345, 1024, 2
+    x = to_dev(synth.random_bytes(n, 99), dev)
+    whole = se.fragment_protect(x, W, L, KEY, IV)
+    parts = [[], [], []]
+    for p in shard.plan_stripes(n, W, L, world):
+        xs = x[p["byte_begin"]: p["byte_end"]].clone()
+        st = se.fragment_protect(xs, W, L, KEY, IV, block_offset=p["block_offset"])
+        for s in range(3):
+            parts[s].append(st[s])
+        back, rep = se.fragment_recover(*st, xs.numel(), W, L, KEY, IV, block_offset=p["block_offset"])
+        assert torch.equal(back, xs) and rep.cpu().tolist() == [-1, 0]
+    for s in range(3):
+        assert torch.equal(torch.cat(parts[s]), whole[s])
