@@ -165,8 +165,27 @@ static int fused_checks(const se_geom* g, const uint8_t* key, const uint8_t* iv,
     if (rc) return rc;
     if (!key || !iv) return SE_EINVAL;
     if ((g->block_offset * lay.a_bits) % 128) return SE_EINVAL;
-    if (g->mode != SE_MODE_BLOCK8) return SE_ENOTSUP;
+    // FULL mode transforms the whole matrix: a stripe would need its
+    // neighbours' halo rows, which this entry point does not take.
+    if (g->mode == SE_MODE_FULL && g->block_offset) return SE_ENOTSUP;
     return SE_OK;
+}
+
+static DwtParams dwt_params(const se_geom* g, const se_layout& lay) {
+    DwtParams p;
+    memset(&p, 0, sizeof p);
+    p.n_bytes = g->n_bytes; p.n_blocks = lay.n_blocks;
+    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows; p.one = 1;
+    return p;
+}
+
+// FULL mode needs an R x W int16 coefficient workspace between the transform
+// and the footprint kernels; it comes from the stream-ordered pool
+// (cudaMallocAsync / cudaFreeAsync on the caller's stream: no device sync).
+static int16_t* ws_alloc(const se_layout& lay, uint32_t width, cudaStream_t s) {
+    void* ws = nullptr;
+    if (cudaMallocAsync(&ws, lay.rows * width * sizeof(int16_t), s) != cudaSuccess) return nullptr;
+    return (int16_t*)ws;
 }
 
 int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in,
@@ -182,7 +201,17 @@ int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     p.in = (const uint8_t*)d_in;
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
-    return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+    if (g->mode == SE_MODE_BLOCK8) return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int16_t* ws = ws_alloc(lay, g->width, s);
+    if (!ws) return SE_ECUDA;
+    DwtParams dp = dwt_params(g, lay);
+    dp.in = p.in; dp.coef = ws;
+    p.ws = ws; p.rows = lay.rows;
+    const int e1 = launch_dwt_full_fwd(dp, g->levels, stream);
+    const int e2 = e1 ? e1 : launch_protect_full(p, g->levels, mask, stream);
+    cudaFreeAsync(ws, s);
+    return (e1 || e2) ? SE_ECUDA : SE_OK;
 }
 
 int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
@@ -205,39 +234,44 @@ int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     p.report = d_report;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
-    return launch_recover_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+    if (g->mode == SE_MODE_BLOCK8) return launch_recover_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+    int16_t* ws = ws_alloc(lay, g->width, s);
+    if (!ws) return SE_ECUDA;
+    p.ws = ws; p.rows = lay.rows;
+    DwtParams dp = dwt_params(g, lay);
+    dp.out = p.out; dp.coef = ws;
+    const int e1 = launch_recover_full(p, g->levels, mask, stream);             // unmask + scatter
+    const int e2 = e1 ? e1 : launch_dwt_full_inv(dp, g->levels, d_report, stream);   // inverse + report
+    cudaFreeAsync(ws, s);
+    return (e1 || e2) ? SE_ECUDA : SE_OK;
 }
 
 int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream) {
     se_layout lay;
     int rc = fragment_layout(g, &lay);
     if (rc) return rc;
-    if (g->mode != SE_MODE_BLOCK8) return SE_ENOTSUP;
     if (g->n_bytes == 0) return SE_OK;
     if (!d_in || !d_coef) return SE_EINVAL;
     if (!aligned16(d_in) || !aligned16(d_coef)) return SE_EALIGN;
-    DwtParams p;
-    memset(&p, 0, sizeof p);
+    DwtParams p = dwt_params(g, lay);
     p.in = (const uint8_t*)d_in; p.coef = d_coef;
-    p.n_bytes = g->n_bytes; p.n_blocks = lay.n_blocks;
-    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows; p.one = 1;
-    return launch_dwt_fwd_block8(p, g->levels, stream) ? SE_ECUDA : SE_OK;
+    const int e = g->mode == SE_MODE_BLOCK8 ? launch_dwt_fwd_block8(p, g->levels, stream)
+                                            : launch_dwt_full_fwd(p, g->levels, stream);
+    return e ? SE_ECUDA : SE_OK;
 }
 
 int dwt_inv(const se_geom* g, const int16_t* d_coef, void* d_out, void* stream) {
     se_layout lay;
     int rc = fragment_layout(g, &lay);
     if (rc) return rc;
-    if (g->mode != SE_MODE_BLOCK8) return SE_ENOTSUP;
     if (g->n_bytes == 0) return SE_OK;
     if (!d_out || !d_coef) return SE_EINVAL;
     if (!aligned16(d_out) || !aligned16(d_coef)) return SE_EALIGN;
-    DwtParams p;
-    memset(&p, 0, sizeof p);
+    DwtParams p = dwt_params(g, lay);
     p.out = (uint8_t*)d_out; p.coef = (int16_t*)d_coef;
-    p.n_bytes = g->n_bytes; p.n_blocks = lay.n_blocks;
-    p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows; p.one = 1;
-    return launch_dwt_inv_block8(p, g->levels, stream) ? SE_ECUDA : SE_OK;
+    const int e = g->mode == SE_MODE_BLOCK8 ? launch_dwt_inv_block8(p, g->levels, stream)
+                                            : launch_dwt_full_inv(p, g->levels, nullptr, stream);
+    return e ? SE_ECUDA : SE_OK;
 }
 
 int cipher_encrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block_offset, const void* d_in,

@@ -141,10 +141,10 @@ __device__ __forceinline__ void dwt8_inv(int (&v)[8][8], uint32_t one) {
 }
 
 // ------------------------------------------------------------------ records
-template <int L>
+template <int L, int MODE = 0>
 struct Rec {
     static constexpr int ABITS = (L == 1) ? 160 : (L == 2) ? 40 : 10;
-    static constexpr int BBITS = (L == 1) ? 0 : (L == 2) ? 124 : 155;
+    static constexpr int BBITS = (L == 1) ? 0 : (L == 2) ? (MODE ? 132 : 124) : (MODE ? 165 : 155);
     static constexpr int CBITS = 480;
     static constexpr int AW = (ABITS + 31) / 32;
     static constexpr int BW = BBITS ? (BBITS + 31) / 32 : 1;
@@ -196,10 +196,13 @@ __device__ __forceinline__ int get_field(const uint32_t (&r)[NW], int pos, int o
 
 // Visit every field of the three records in the canonical order (C10):
 // A = LL_L; B = HL_l, LH_l, HH_l for l = L..2; C = HL1, LH1, HH1; row-major
-// inside each band.  f(stream, pos, row, col, width).
-template <int L, typename F>
+// inside each band.  f(stream, pos, row, col, width) with (row, col) in the
+// 8x8 dyadic block layout.  Widths (C22/C23): BLOCK8 HH_l (l >= 2) 11 bits,
+// all else 10; FULL mode every B field 11 bits.
+template <int L, int MODE = 0, typename F>
 __device__ __forceinline__ void for_each_field(F&& f) {
     constexpr int sL = 8 >> L;
+    constexpr int wb = MODE ? 11 : 10;
     int pos = 0;
 #pragma unroll
     for (int i = 0; i < sL; ++i)
@@ -212,11 +215,11 @@ __device__ __forceinline__ void for_each_field(F&& f) {
 #pragma unroll
         for (int i = 0; i < s; ++i)
 #pragma unroll
-            for (int j = 0; j < s; ++j) { f(1, pos, i, s + j, 10); pos += 10; }   // HL
+            for (int j = 0; j < s; ++j) { f(1, pos, i, s + j, wb); pos += wb; }   // HL
 #pragma unroll
         for (int i = 0; i < s; ++i)
 #pragma unroll
-            for (int j = 0; j < s; ++j) { f(1, pos, s + i, j, 10); pos += 10; }   // LH
+            for (int j = 0; j < s; ++j) { f(1, pos, s + i, j, wb); pos += wb; }   // LH
 #pragma unroll
         for (int i = 0; i < s; ++i)
 #pragma unroll

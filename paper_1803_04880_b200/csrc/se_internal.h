@@ -18,6 +18,8 @@ struct FusedParams {
     uint8_t* b;               // B' stream
     uint8_t* c;               // C' stream
     se_report* report;        // recover only, nullable
+    int16_t* ws;              // FULL mode: R x W Mallat coefficient workspace
+    uint64_t rows;            // R (FULL mode)
     uint64_t n_bytes;
     uint64_t n_blocks;
     uint64_t block_offset;    // global index of local block 0 (hash nonce, C16)
@@ -77,6 +79,11 @@ int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void
 int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,
                         void* stream);
 int launch_dwt_fwd_block8(const DwtParams& p, uint32_t levels, void* stream);
+// FULL mode (row a11): whole-matrix transform kernels and the footprint CTA kernels
+int launch_dwt_full_fwd(const DwtParams& p, uint32_t levels, void* stream);
+int launch_dwt_full_inv(const DwtParams& p, uint32_t levels, se_report* report, void* stream);
+int launch_protect_full(const FusedParams& p, uint32_t levels, bool mask, void* stream);
+int launch_recover_full(const FusedParams& p, uint32_t levels, bool mask, void* stream);
 int launch_dwt_inv_block8(const DwtParams& p, uint32_t levels, void* stream);
 int launch_cipher_ctr(const CipherParams& p, void* stream);
 

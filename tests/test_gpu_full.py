@@ -1,0 +1,96 @@
+"""GPU parity of FULL-matrix mode (row a11) against the oracle, bit-exact:
+whole-matrix Mallat coefficients (tiles with halos, borders reflected per
+level), footprint fragments with the FULL widths (C23), recover and the
+corruption report.  Sizes span several 64 x 128 tiles in both directions,
+ragged tails and matrices smaller than one tile."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1803_04880_b200 as se  # noqa: E402
+
+KEY = synth.KEY
+IV = bytes.fromhex("8899aabbccddeeff0011223344556677")
+FULL = se.MODE_FULL
+
+# (n, W): several tiles wide/tall, ragged tails, tiny matrices
+CASES = [(64, 8), (8 * 24, 24), (1000, 40), (384 * 200 - 7, 384), (256 * 136, 256), (520 * 72 + 5, 520),
+         (128 * 129, 128), (1024 * 96, 1024)]
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    se.lib()
+    return torch.device("cuda:0")
+
+
+def to_dev(x, dev):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+def data(n, seed):
+    w = 64
+    return synth.bitmap(-(-n // (3 * w)) + 1, w, 3, seed).reshape(-1)[:n] if seed % 2 else synth.random_bytes(n, seed)
+
+
+@pytest.mark.parametrize("L", [1, 2, 3])
+@pytest.mark.parametrize("n,W", CASES)
+def test_dwt_full_parity(dev, orc, n, W, L):
+    x = data(n, n + W + L)
+    coef = se.dwt_fwd(to_dev(x, dev), W, L, mode=FULL)
+    ref = orc.dwt_fwd(x, W, L, orc.MODE_FULL)
+    got = coef.cpu().numpy().astype(np.int32)
+    if not np.array_equal(got, ref):
+        bad = np.argwhere(got != ref)
+        pytest.fail(f"{len(bad)} coefficients differ, first at {bad[:5].tolist()}")
+    back = se.dwt_inv(coef, n, W, L, mode=FULL)
+    assert np.array_equal(back.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("L", [1, 2, 3])
+@pytest.mark.parametrize("n,W", CASES[:6])
+def test_protect_recover_full_parity(dev, orc, n, W, L):
+    x = data(n, 3 * n + L)
+    for flags in (0, se.FLAG_PUBLIC_PLAIN):
+        a, b, c = se.fragment_protect(to_dev(x, dev), W, L, KEY, IV, mode=FULL, flags=flags)
+        oa, ob, oc = orc.protect(x, W, L, KEY, IV, mode=orc.MODE_FULL, flags=flags)
+        assert np.array_equal(a.cpu().numpy(), oa), "A'"
+        assert np.array_equal(b.cpu().numpy(), ob), "B'"
+        assert np.array_equal(c.cpu().numpy(), oc), "C'"
+        back, rep = se.fragment_recover(a, b, c, n, W, L, KEY, IV, mode=FULL, flags=flags)
+        assert np.array_equal(back.cpu().numpy(), x)
+        assert rep.cpu().tolist() == [-1, 0]
+
+
+def test_full_corruption_report(dev, orc):
+    n, W, L = 384 * 200, 384, 2
+    x = data(n, 5)
+    a, b, c = orc.protect(x, W, L, KEY, IV, mode=orc.MODE_FULL)
+    c2 = c.copy()
+    c2[480 * 300 // 8] ^= 0xF0           # damage footprint 300's level-1 details
+    back, rep = se.fragment_recover(to_dev(a, dev), to_dev(b, dev), to_dev(c2, dev), n, W, L, KEY, IV, mode=FULL)
+    oback, orep = orc.recover(a, b, c2, n, W, L, KEY, IV, mode=orc.MODE_FULL)
+    assert np.array_equal(back.cpu().numpy(), oback)
+    assert tuple(rep.cpu().tolist()) == orep
+
+
+def test_full_c4_shape_sampled(dev, orc):
+    """C4-FULL geometry at reduced height (W = 32768 as in SURVEY §8.2.1): the
+    whole-matrix transform round-trips and sampled footprints match the oracle."""
+    W, R, L = 32768, 64, 2
+    x = synth.random_bytes(W * R, 4)
+    xt = to_dev(x, dev)
+    a, b, c = se.fragment_protect(xt, W, L, KEY, IV, mode=FULL)
+    oa, ob, oc = orc.protect(x, W, L, KEY, IV, mode=orc.MODE_FULL)
+    assert np.array_equal(a.cpu().numpy(), oa) and np.array_equal(b.cpu().numpy(), ob)
+    assert np.array_equal(c.cpu().numpy(), oc)
+    back, rep = se.fragment_recover(a, b, c, x.size, W, L, KEY, IV, mode=FULL)
+    assert torch.equal(back, xt) and rep.cpu().tolist() == [-1, 0]
