@@ -282,3 +282,42 @@ class Batch:
         _check(lib().fragment_recover_batch(self.n, _ptr(self.d_jobs), self.total_ctas, self.levels, self.flags,
                                             self.key, _ptr(self.reports), _stream(stream)), "fragment_recover_batch")
         return self.outs, self.reports[: self.n]
+
+
+# ---------------------------------------------------------------- host-resident streaming (f1)
+
+class Report(C.Structure):
+    _fields_ = [("first_bad_block", C.c_int64), ("bad_blocks", C.c_uint64)]
+
+
+def _host_empty(n, pin=True):
+    import torch
+    t = torch.empty(max(int(n), 1), dtype=torch.uint8)
+    if pin:
+        t = t.pin_memory()
+    return t[: int(n)]
+
+
+def fragment_protect_host(x, width: int, levels: int, key, iv, mode: int = MODE_BLOCK8, flags: int = 0,
+                          block_offset: int = 0, out=None, chunk_bytes: int = 0, n_streams: int = 0):
+    """x: 1-D uint8 CPU tensor (pinned for overlap).  Returns CPU tensors (A', B', C')."""
+    lay = fragment_layout(x.numel(), width, levels, mode, flags, block_offset)
+    a, b, c = out if out is not None else (_host_empty(lay["a_bytes"]), _host_empty(lay["b_bytes"]),
+                                           _host_empty(lay["c_bytes"]))
+    g = _geom(x.numel(), width, levels, mode, flags, block_offset)
+    _check(lib().fragment_protect_host(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(x), _ptr(a),
+                                       _ptr(b) if b.numel() else None, _ptr(c), int(chunk_bytes), int(n_streams)),
+           "fragment_protect_host")
+    return a, b, c
+
+
+def fragment_recover_host(a, b, c, n_bytes: int, width: int, levels: int, key, iv, mode: int = MODE_BLOCK8,
+                          flags: int = 0, block_offset: int = 0, out=None, chunk_bytes: int = 0, n_streams: int = 0):
+    """Returns (CPU uint8 tensor, (first_bad_block, bad_blocks))."""
+    o = out if out is not None else _host_empty(n_bytes)
+    rep = Report()
+    g = _geom(n_bytes, width, levels, mode, flags, block_offset)
+    _check(lib().fragment_recover_host(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(a),
+                                       _ptr(b) if b is not None and b.numel() else None, _ptr(c), _ptr(o),
+                                       C.byref(rep), int(chunk_bytes), int(n_streams)), "fragment_recover_host")
+    return o, (int(rep.first_bad_block), int(rep.bad_blocks))

@@ -350,14 +350,5 @@ int fragment_recover_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total
     return batch_common(n_jobs, d_jobs, total_ctas, levels, flags, key, d_reports, true, stream);
 }
 
-int fragment_protect_host(const se_geom*, const uint8_t*, const uint8_t*, const void*, void*, void*, void*,
-                          uint64_t, uint32_t) {
-    return SE_ENOTSUP;
-}
-
-int fragment_recover_host(const se_geom*, const uint8_t*, const uint8_t*, const void*, const void*, const void*,
-                          void*, se_report*, uint64_t, uint32_t) {
-    return SE_ENOTSUP;
-}
 
 }  // extern "C"
