@@ -27,13 +27,13 @@ namespace se {
 template <int L, bool MASK>
 __global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
 k_protect_block8(const __grid_constant__ FusedParams p) {
-    protect_cta<L, MASK>(p, blockIdx.x);
+    protect_cta<L, MASK, 0, true>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
 __global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
 k_recover_block8(const __grid_constant__ FusedParams p) {
-    recover_cta<L, MASK>(p, blockIdx.x);
+    recover_cta<L, MASK, 0, true>(p, blockIdx.x);
 }
 
 // Many independent files in one launch (C5; SURVEY §8.6 "sharded by file").
@@ -152,19 +152,38 @@ __global__ void __launch_bounds__(kBlocksPerCta) k_dwt_inv_block8(const __grid_c
 
 // ---------------------------------------------------------------- launchers
 
+// Launch with programmatic stream serialization: the kernel may start while
+// the preceding keystream kernel (k_cipher_ctr) still runs; it synchronises
+// with griddepcontrol.wait where it needs the keystream (fused_cta.cuh).
+template <typename P>
+void launch_pdl(void (*kernel)(P), unsigned grid, unsigned block, cudaStream_t s, const P& p) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, p);
+}
+template void launch_pdl<FusedParams>(void (*)(FusedParams), unsigned, unsigned, cudaStream_t, const FusedParams&);
+
 static unsigned grid_for(uint64_t n_blocks) {
     return (unsigned)((n_blocks + kBlocksPerCta - 1) / kBlocksPerCta);
 }
 
 template <int L>
 static void protect_l(const FusedParams& p, bool mask, cudaStream_t s) {
-    if (mask) k_protect_block8<L, true><<<grid_for(p.n_blocks), kBlocksPerCta, 0, s>>>(p);
-    else k_protect_block8<L, false><<<grid_for(p.n_blocks), kBlocksPerCta, 0, s>>>(p);
+    if (mask) launch_pdl(k_protect_block8<L, true>, grid_for(p.n_blocks), kBlocksPerCta, s, p);
+    else launch_pdl(k_protect_block8<L, false>, grid_for(p.n_blocks), kBlocksPerCta, s, p);
 }
 template <int L>
 static void recover_l(const FusedParams& p, bool mask, cudaStream_t s) {
-    if (mask) k_recover_block8<L, true><<<grid_for(p.n_blocks), kBlocksPerCta, 0, s>>>(p);
-    else k_recover_block8<L, false><<<grid_for(p.n_blocks), kBlocksPerCta, 0, s>>>(p);
+    if (mask) launch_pdl(k_recover_block8<L, true>, grid_for(p.n_blocks), kBlocksPerCta, s, p);
+    else launch_pdl(k_recover_block8<L, false>, grid_for(p.n_blocks), kBlocksPerCta, s, p);
 }
 
 int launch_protect_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream) {

@@ -11,7 +11,12 @@ namespace se {
 
 constexpr int kCipherThreads = 256;
 
+// p.in == nullptr: write the keystream itself (used by the fused kernels,
+// which then XOR it into the private fragment, see fused_cta.cuh).
 __global__ void __launch_bounds__(kCipherThreads) k_cipher_ctr(const __grid_constant__ CipherParams p) {
+    // a dependent kernel launched with programmatic stream serialization may
+    // start now; it waits (griddepcontrol.wait) before reading our output
+    asm volatile("griddepcontrol.launch_dependents;");
     __shared__ AesSmem aes;
     aes_load_tables(aes, threadIdx.x, kCipherThreads);
     __syncthreads();
@@ -23,7 +28,7 @@ __global__ void __launch_bounds__(kCipherThreads) k_cipher_ctr(const __grid_cons
         aes128_block(aes, p.rk, x);
         const uint64_t off = j * 16;
         if (off + 16 <= p.n) {
-            const uint4 q = __ldg(reinterpret_cast<const uint4*>(p.in + off));
+            const uint4 q = p.in ? __ldg(reinterpret_cast<const uint4*>(p.in + off)) : make_uint4(0, 0, 0, 0);
             uint4 r;
             r.x = q.x ^ bswap32(x[0]);
             r.y = q.y ^ bswap32(x[1]);
@@ -33,7 +38,7 @@ __global__ void __launch_bounds__(kCipherThreads) k_cipher_ctr(const __grid_cons
         } else {
             for (uint64_t k = off; k < p.n; ++k) {
                 const uint32_t w = x[(k - off) / 4];
-                p.out[k] = p.in[k] ^ (uint8_t)(w >> (24 - 8 * ((k - off) % 4)));
+                p.out[k] = (p.in ? p.in[k] : 0) ^ (uint8_t)(w >> (24 - 8 * ((k - off) % 4)));
             }
         }
     }

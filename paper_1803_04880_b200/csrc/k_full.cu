@@ -184,12 +184,12 @@ __global__ void __launch_bounds__(kFullThreads) k_dwt_full_inv(const __grid_cons
 
 template <int L, bool MASK>
 __global__ void __launch_bounds__(kBlocksPerCta, 4) k_protect_full(const __grid_constant__ FusedParams p) {
-    protect_cta<L, MASK, 1>(p, blockIdx.x);
+    protect_cta<L, MASK, 1, true>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
 __global__ void __launch_bounds__(kBlocksPerCta, 4) k_recover_full(const __grid_constant__ FusedParams p) {
-    recover_cta<L, MASK, 1>(p, blockIdx.x);
+    recover_cta<L, MASK, 1, true>(p, blockIdx.x);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -228,15 +228,15 @@ int launch_dwt_full_inv(const DwtParams& p, uint32_t levels, se_report* report, 
 template <int L>
 static void prot_full_l(const FusedParams& p, bool mask, cudaStream_t s) {
     const unsigned g = (unsigned)((p.n_blocks + kBlocksPerCta - 1) / kBlocksPerCta);
-    if (mask) k_protect_full<L, true><<<g, kBlocksPerCta, 0, s>>>(p);
-    else k_protect_full<L, false><<<g, kBlocksPerCta, 0, s>>>(p);
+    if (mask) launch_pdl(k_protect_full<L, true>, g, kBlocksPerCta, s, p);
+    else launch_pdl(k_protect_full<L, false>, g, kBlocksPerCta, s, p);
 }
 
 template <int L>
 static void rec_full_l(const FusedParams& p, bool mask, cudaStream_t s) {
     const unsigned g = (unsigned)((p.n_blocks + kBlocksPerCta - 1) / kBlocksPerCta);
-    if (mask) k_recover_full<L, true><<<g, kBlocksPerCta, 0, s>>>(p);
-    else k_recover_full<L, false><<<g, kBlocksPerCta, 0, s>>>(p);
+    if (mask) launch_pdl(k_recover_full<L, true>, g, kBlocksPerCta, s, p);
+    else launch_pdl(k_recover_full<L, false>, g, kBlocksPerCta, s, p);
 }
 
 int launch_protect_full(const FusedParams& p, uint32_t levels, bool mask, void* stream) {

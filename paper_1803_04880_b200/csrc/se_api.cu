@@ -179,6 +179,35 @@ static DwtParams dwt_params(const se_geom* g, const se_layout& lay) {
     return p;
 }
 
+// Keep the stream-ordered pool's memory across calls (default release
+// threshold 0 would hand it back to the OS at every synchronisation).
+static void keep_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
+// Row a6, keystream half: AES-128-CTR keystream of the whole A stream
+// (counter base p.ctr) written to `out`; the fused kernel that follows is
+// launched with programmatic stream serialization and XORs it in.
+static int launch_keystream(const FusedParams& p, uint8_t* out, uint64_t n, void* stream) {
+    CipherParams cp;
+    memset(&cp, 0, sizeof cp);
+    cp.in = nullptr;
+    cp.out = out;
+    cp.n = n;
+    memcpy(cp.ctr, p.ctr, sizeof cp.ctr);
+    memcpy(cp.rk, p.rk, sizeof cp.rk);
+    return launch_cipher_ctr(cp, stream);
+}
+
 // FULL mode needs an R x W int16 coefficient workspace between the transform
 // and the footprint kernels; it comes from the stream-ordered pool
 // (cudaMallocAsync / cudaFreeAsync on the caller's stream: no device sync).
@@ -201,17 +230,22 @@ int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     p.in = (const uint8_t*)d_in;
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
-    if (g->mode == SE_MODE_BLOCK8) return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+    if (g->mode == SE_MODE_BLOCK8) {
+        if (launch_keystream(p, p.a, lay.a_bytes, stream)) return SE_ECUDA;
+        return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+    }
+    keep_pool();
     cudaStream_t s = (cudaStream_t)stream;
     int16_t* ws = ws_alloc(lay, g->width, s);
     if (!ws) return SE_ECUDA;
     DwtParams dp = dwt_params(g, lay);
     dp.in = p.in; dp.coef = ws;
     p.ws = ws; p.rows = lay.rows;
-    const int e1 = launch_dwt_full_fwd(dp, g->levels, stream);
-    const int e2 = e1 ? e1 : launch_protect_full(p, g->levels, mask, stream);
+    int e = launch_dwt_full_fwd(dp, g->levels, stream);
+    if (!e) e = launch_keystream(p, p.a, lay.a_bytes, stream);
+    if (!e) e = launch_protect_full(p, g->levels, mask, stream);
     cudaFreeAsync(ws, s);
-    return (e1 || e2) ? SE_ECUDA : SE_OK;
+    return e ? SE_ECUDA : SE_OK;
 }
 
 int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
@@ -234,16 +268,30 @@ int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     p.report = d_report;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
-    if (g->mode == SE_MODE_BLOCK8) return launch_recover_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
-    int16_t* ws = ws_alloc(lay, g->width, s);
-    if (!ws) return SE_ECUDA;
+    keep_pool();
+    // keystream scratch (a_bytes, 7.8% of n at L = 2) from the stream-ordered pool
+    void* ks = nullptr;
+    if (cudaMallocAsync(&ks, lay.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
+    p.ks = (const uint8_t*)ks;
+    int e = launch_keystream(p, (uint8_t*)ks, lay.a_bytes, stream);
+    if (g->mode == SE_MODE_BLOCK8) {
+        if (!e) e = launch_recover_block8(p, g->levels, mask, stream);
+        cudaFreeAsync(ks, s);
+        return e ? SE_ECUDA : SE_OK;
+    }
+    int16_t* ws = e ? nullptr : ws_alloc(lay, g->width, s);
+    if (!ws) {
+        cudaFreeAsync(ks, s);
+        return SE_ECUDA;
+    }
     p.ws = ws; p.rows = lay.rows;
     DwtParams dp = dwt_params(g, lay);
     dp.out = p.out; dp.coef = ws;
-    const int e1 = launch_recover_full(p, g->levels, mask, stream);             // unmask + scatter
-    const int e2 = e1 ? e1 : launch_dwt_full_inv(dp, g->levels, d_report, stream);   // inverse + report
+    e = launch_recover_full(p, g->levels, mask, stream);                      // unmask + scatter
+    if (!e) e = launch_dwt_full_inv(dp, g->levels, d_report, stream);         // inverse + report
     cudaFreeAsync(ws, s);
-    return (e1 || e2) ? SE_ECUDA : SE_OK;
+    cudaFreeAsync(ks, s);
+    return e ? SE_ECUDA : SE_OK;
 }
 
 int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream) {

@@ -1,6 +1,7 @@
 // se_internal.h — kernel parameter blocks and launcher prototypes shared by
 // the host API (se_api.cu) and the kernel translation units.  Not installed.
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "../../include/se.h"
@@ -19,6 +20,7 @@ struct FusedParams {
     uint8_t* c;               // C' stream
     se_report* report;        // recover only, nullable
     int16_t* ws;              // FULL mode: R x W Mallat coefficient workspace
+    const uint8_t* ks;        // recover: AES-CTR keystream of the A stream (scratch)
     uint64_t rows;            // R (FULL mode)
     uint64_t n_bytes;
     uint64_t n_blocks;
@@ -88,5 +90,7 @@ int launch_dwt_inv_block8(const DwtParams& p, uint32_t levels, void* stream);
 int launch_cipher_ctr(const CipherParams& p, void* stream);
 
 void note_launch();
+template <typename P>
+void launch_pdl(void (*kernel)(P), unsigned grid, unsigned block, cudaStream_t s, const P& p);
 
 }  // namespace se
