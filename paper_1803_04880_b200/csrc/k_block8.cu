@@ -17,7 +17,7 @@
 #include "fused_cta.cuh"
 
 #ifndef SE_MIN_CTAS
-#define SE_MIN_CTAS 4      // resident 128-thread CTAs per SM the register budget must allow
+#define SE_MIN_CTAS 5      // resident 128-thread CTAs per SM the register budget must allow (96 regs)
 #endif
 
 namespace se {
