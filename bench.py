@@ -246,7 +246,8 @@ def run_se(args):
         ms_step = total_ms / args.steps
 
     # ---- e2e: same metric with host buffers, H2D/D2H inside the timed region
-    e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, args.e2e_steps)
+    e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, args.e2e_steps) if args.e2e_steps > 0 else \
+        {"value": None, "unit": "GB/s", "note": "skipped (--e2e-steps 0, profiling runs only)"}
 
     # ---- comparator: full-file AES-128-CTR on the same GPU (paper methodology)
     aes_gbs = None
@@ -329,6 +330,132 @@ def run_se(args):
     if world > 1:
         dist.destroy_process_group()
     return line
+
+
+def run_multi(args):
+    """BASELINE.json's multi-GPU configs: C4 (1 GiB file, row stripes, one per
+    rank: strong scaling) and C5 (10,000 files 1 KiB-16 MiB, LPT by file bytes,
+    one batched launch per rank per direction: strong scaling).  No data-path
+    collective; NCCL only for the barrier and the max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1803_04880_b200 as se
+    from paper_1803_04880_b200 import shard
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    se.lib()
+    key, L = synth.KEY, 2
+    if args.config == 4:
+        c = synth.CONFIGS[4]
+        n, W = c["n_bytes"], c["width"]
+        plan = shard.plan_stripes(n, W, L, world)[rank]
+        x_np = synth.config_input(4)[plan["byte_begin"]: plan["byte_end"]]
+        x = torch.from_numpy(np.ascontiguousarray(x_np)).to(dev)
+        del x_np
+        iv = synth.iv_for(4)
+        nloc = x.numel()
+        lay = se.fragment_layout(nloc, W, L, block_offset=plan["block_offset"])
+        frag = (se._empty(lay["a_bytes"], dev), se._empty(lay["b_bytes"], dev), se._empty(lay["c_bytes"], dev))
+        out = se._empty(nloc, dev)
+        rep = torch.empty(2, dtype=torch.int64, device=dev)
+
+        def protect():
+            se.fragment_protect(x, W, L, key, iv, block_offset=plan["block_offset"], out=frag)
+
+        def recover():
+            se.fragment_recover(*frag, nloc, W, L, key, iv, block_offset=plan["block_offset"], out=out, report=rep)
+
+        def check():
+            return torch.equal(out, x) and rep.cpu().tolist() == [-1, 0]
+        total_bytes, n_blocks_local = n, lay["n_blocks"]
+        workload = f"{c['name']} row stripes ({world} stripes of whole block-rows, block_offset per stripe)"
+        extra = {"stripe_bytes": nloc, "block_offset": plan["block_offset"]}
+    else:
+        sizes = synth.c5_file_sizes(10000, 5)
+        mine = shard.plan_files(sizes, world)[rank]
+        gen = torch.Generator(device=dev)
+        files = []
+        for i in mine:
+            gen.manual_seed(5_000_000 + i)
+            files.append(torch.randint(0, 256, (int(sizes[i]),), dtype=torch.uint8, device=dev, generator=gen))
+        widths = [synth.width_rule(int(sizes[i])) for i in mine]
+        ivs = [synth.iv_for(5, i) for i in mine]
+        batch = se.Batch(files, widths, ivs, L, key)
+
+        def protect():
+            batch.protect()
+
+        def recover():
+            batch.recover()
+
+        def check():
+            outs, reps = batch.recover()
+            return all(torch.equal(o, f) for o, f in zip(outs, files)) and bool((reps[:, 1] == 0).all())
+        total_bytes = int(sizes.sum())
+        n_blocks_local = sum(se.fragment_layout(f.numel(), w, L)["n_blocks"] for f, w in zip(files, widths))
+        workload = "C5-10000-files-1KiB-16MiB-L2 (LPT by bytes; content uniform random bytes generated on device)"
+        extra = {"files_total": len(sizes), "files_this_rank": len(files), "bytes_this_rank": int(sum(sizes[mine]))}
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+    protect()
+    recover()
+    torch.cuda.synchronize()
+    assert check(), "recover(protect(x)) != x"
+    clocks = ClockSampler(local)
+    clocks.start()
+    i, t_end = 0, time.time() + args.soak          # >= W steps and ~soak s of load for the clock samples
+    while i < args.warmup or time.time() < t_end:
+        protect()
+        recover()
+        torch.cuda.synchronize()
+        i += 1
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    se.launch_count(reset=True)
+    for k in range(args.steps):
+        flush.fill_(k)
+        ev[k][0].record()
+        protect()
+        ev[k][1].record()
+        recover()
+        ev[k][2].record()
+    torch.cuda.synchronize()
+    launches = se.launch_count()
+    clocks.stop()
+    t_p = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    t_r = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    t = torch.tensor([t_p + t_r, t_p, t_r], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    ms, mp, mr = (float(v) for v in t.tolist())
+    peaks, peak_src = load_peaks()
+    peak_alu = NUM_SMS * ALU_LANES_PER_SM_CLK * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+    achieved = alu_ops_per_block(L, True) * n_blocks_local / (max(mp, mr) / 1e3) / 1e9
+    return {
+        "metric": "protect+recover GB/s per GPU and at 1/2/4/8 B200; % of HBM roofline",
+        "value": round(total_bytes / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": dict({"workload": workload, "n_bytes_total": total_bytes, "levels": L, "mode": "BLOCK8",
+                        "parallelism": f"dp{world} ({'row stripes' if args.config == 4 else 'by file'})",
+                        "l2": "flushed between steps"}, **extra),
+        "roofline": {"bound": "alu", "kernel": "k_protect/k_recover (rank 0 slowest)", "achieved": round(achieved, 1),
+                     "peak": round(peak_alu, 1), "unit": "Gop/s", "frac": round(achieved / peak_alu, 4),
+                     "traffic": None, "peak_source": f"guide ALU pipe x {peaks.get('sm_max_mhz')} MHz ({peak_src})"},
+        "protect_gbs": round(total_bytes / (mp / 1e3) / 1e9, 3), "recover_gbs": round(total_bytes / (mr / 1e3) / 1e9, 3),
+        "e2e": {"value": None, "unit": "GB/s", "note": "multi-file / stripe modes are device-resident; e2e is measured "
+                                                       "on the default config"},
+        "gpu_launches": int(launches), "clocks": clocks.summary(),
+    }
 
 
 def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=2 << 20, n_streams=4):
@@ -462,7 +589,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--stripes", action="store_true", help="C4: split the one file into per-rank row stripes")
     ap.add_argument("--impl", default="se", choices=["se", "reference"])
     ap.add_argument("--plain", action="store_true", help="PUBLIC_PLAIN measurement mode (C26)")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of sustained warm-up load")
@@ -473,7 +601,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    line = run_reference(args) if args.impl == "reference" else run_se(args)
+    if args.impl == "reference":
+        line = run_reference(args)
+    elif args.config == 5 or (args.config == 4 and args.stripes):
+        line = run_multi(args)
+    else:
+        line = run_se(args)
     if line is not None:
         print(json.dumps(line), flush=True)
 

@@ -113,30 +113,6 @@ __device__ __forceinline__ void copy_s2g(uint8_t* __restrict__ g, const uint32_t
     for (uint32_t i = nv * 16 + tid; i < len; i += kBlocksPerCta) g[i] = sb[i];
 }
 
-// The AES-CTR keystream of the CTA's A bytes, in memory byte order.
-template <int ABITS>
-__device__ __forceinline__ void ctr_keystream_cta(const FusedParams& p, const AesSmem& aes, uint32_t* ks,
-                                                  uint64_t cta, int tid) {
-    for (int t = tid; t < ABITS; t += kBlocksPerCta) {
-        uint32_t x[4];
-        ctr_add(p.ctr, cta * (uint64_t)ABITS + (uint64_t)t, x);
-        aes128_block(aes, p.rk, x);
-        reinterpret_cast<uint4*>(ks)[t] = make_uint4(bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3]));
-    }
-}
-
-__device__ __forceinline__ void copy_s2g_xor(uint8_t* __restrict__ g, const uint32_t* s, const uint32_t* ks,
-                                             uint64_t len, int tid) {
-    const uint32_t nv = (uint32_t)(len / 16);
-    for (uint32_t i = tid; i < nv; i += kBlocksPerCta) {
-        const uint4 a = reinterpret_cast<const uint4*>(s)[i], k = reinterpret_cast<const uint4*>(ks)[i];
-        reinterpret_cast<uint4*>(g)[i] = make_uint4(a.x ^ k.x, a.y ^ k.y, a.z ^ k.z, a.w ^ k.w);
-    }
-    const uint8_t* sb = reinterpret_cast<const uint8_t*>(s);
-    const uint8_t* kb = reinterpret_cast<const uint8_t*>(ks);
-    for (uint32_t i = nv * 16 + tid; i < len; i += kBlocksPerCta) g[i] = sb[i] ^ kb[i];
-}
-
 // A' = A ^ KS where the keystream already sits at the destination in global
 // memory (written there by k_cipher_ctr); each CTA reads and rewrites only its
 // own slice.
@@ -161,20 +137,6 @@ __device__ __forceinline__ void xor_g2s(uint32_t* s, const uint8_t* __restrict__
     }
     uint8_t* sb = reinterpret_cast<uint8_t*>(s);
     for (uint32_t i = nv * 16 + tid; i < len; i += kBlocksPerCta) sb[i] ^= ks[i];
-}
-
-// XOR the AES-CTR keystream over the CTA's A bytes held in shared memory.
-template <int ABITS>
-__device__ __forceinline__ void ctr_xor_cta(const FusedParams& p, const AesSmem& aes, uint32_t* sa,
-                                            uint64_t cta, int tid) {
-    // CTA A offset = cta * 128 * ABITS bits = cta * ABITS AES blocks
-    for (int t = tid; t < ABITS; t += kBlocksPerCta) {
-        uint32_t x[4];
-        ctr_add(p.ctr, cta * (uint64_t)ABITS + (uint64_t)t, x);
-        aes128_block(aes, p.rk, x);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sa[4 * t + k] ^= bswap32(x[k]);
-    }
 }
 
 // SHA-256 mask of B from the plain A record (framing C15: K||IV||be64(b)||A).
@@ -300,21 +262,18 @@ __device__ __forceinline__ void footprint_full(const FusedParams& p, uint64_t br
 // MODE 0 (BLOCK8): load + per-block lifting.  MODE 1 (FULL): gather the
 // footprint from the whole-matrix coefficients in p.ws (k_full.cu).
 //
-// EXT_KS: the AES-CTR keystream of the whole A stream was written into p.a by
-// k_cipher_ctr, launched just before this kernel with programmatic stream
-// serialization; the CTA waits for it (griddepcontrol.wait) only at the
-// copy-out, so the keystream kernel overlaps the lifting and hashing and the
-// fused kernel carries no AES tables.  !EXT_KS (batch kernels): the CTA
-// computes its own keystream with shared-memory T-tables.
-template <int L, bool MASK, int MODE = 0, bool EXT_KS = false>
+// Row a6: the AES-CTR keystream of the whole A stream was written into p.a by
+// k_cipher_ctr (k_batch_keystream for batches), launched just before this
+// kernel with programmatic stream serialization; the CTA waits for it
+// (griddepcontrol.wait) only at the copy-out, so the keystream kernel overlaps
+// the lifting and hashing and the fused kernel carries no AES tables.
+template <int L, bool MASK, int MODE = 0>
 __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
     constexpr int SA_W = 4 * R::ABITS;             // 16*ABITS bytes per CTA
     constexpr int SB_W = R::BBITS ? 4 * R::BBITS : 4;
     constexpr int SC_W = 4 * R::CBITS;
-    __shared__ AesSmem aes;                          // unreferenced (dropped) when EXT_KS
     __shared__ __align__(16) uint32_t sa[SA_W];
-    __shared__ __align__(16) uint32_t sks[EXT_KS ? 4 : SA_W];   // in-CTA keystream (!EXT_KS)
     __shared__ __align__(16) uint32_t sb[SB_W];
     __shared__ __align__(16) uint32_t sc[SC_W];
 
@@ -322,11 +281,7 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
     const uint64_t blk = cta * kBlocksPerCta + tid;
     for (int i = tid; i < SA_W; i += kBlocksPerCta) sa[i] = 0;
     for (int i = tid; i < SB_W; i += kBlocksPerCta) sb[i] = 0;
-    if constexpr (!EXT_KS) aes_load_tables(aes, tid, kBlocksPerCta);
     __syncthreads();
-    // row a6, keystream half: the CTA's a_bits counter blocks, computed first so
-    // the few warps doing AES overlap with the others' lifting and hashing.
-    if constexpr (!EXT_KS) ctr_keystream_cta<R::ABITS>(p, aes, sks, cta, tid);
 
     if (blk < p.n_blocks) {
         const uint32_t b32 = (uint32_t)blk;                 // < 2^32 blocks per call (256 GiB)
@@ -370,12 +325,8 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
     // row a9: 128-bit coalesced stores of the CTA's slice of each stream;
     // A' = A ^ keystream on the way out (row a6, XOR half)
     const uint64_t a0 = cta * 16ull * R::ABITS, c0 = cta * 16ull * R::CBITS;
-    if (EXT_KS) {
-        asm volatile("griddepcontrol.wait;" ::: "memory");          // keystream kernel complete
-        copy_s2g_xor_global(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
-    } else {
-        copy_s2g_xor(p.a + a0, sa, sks, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
-    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");              // keystream kernel complete
+    copy_s2g_xor_global(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
     if (R::BBITS) {
         const uint64_t b0 = cta * 16ull * R::BBITS;
         copy_s2g(p.b + b0, sb, min((uint64_t)SB_W * 4, p.b_bytes - b0), tid);
@@ -388,16 +339,15 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
 // MODE 0: unmask, unpack, inverse lifting, store bytes, report.  MODE 1:
 // unmask, unpack and scatter the footprint's coefficients into p.ws; the
 // whole-matrix inverse (and the report) follow in k_full.cu.
-// EXT_KS: the keystream of the whole A stream sits in p.ks (k_cipher_ctr,
-// launched before with programmatic stream serialization); it is waited for
-// and applied after the SHA-512 unmask of C, which does not need A.
-template <int L, bool MASK, int MODE = 0, bool EXT_KS = false>
+// The keystream of the whole A stream sits in p.ks (k_cipher_ctr, launched
+// before with programmatic stream serialization); it is waited for and
+// applied after the SHA-512 unmask of C, which does not need A.
+template <int L, bool MASK, int MODE = 0>
 __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
     constexpr int SA_W = 4 * R::ABITS;
     constexpr int SB_W = R::BBITS ? 4 * R::BBITS : 4;
     constexpr int SC_W = 4 * R::CBITS;
-    __shared__ AesSmem aes;                          // unreferenced (dropped) when EXT_KS
     __shared__ __align__(16) uint32_t sa[SA_W];
     __shared__ __align__(16) uint32_t sb[SB_W];
     __shared__ __align__(16) uint32_t sc[SC_W];
@@ -415,11 +365,9 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         copy_g2s(sb, p.b + b0, min((uint64_t)SB_W * 4, p.b_bytes - b0), SB_W * 4, tid);
     }
     copy_g2s(sc, p.c + c0, min((uint64_t)SC_W * 4, p.c_bytes - c0), SC_W * 4, tid);
-    if constexpr (!EXT_KS) aes_load_tables(aes, tid, kBlocksPerCta);
     __syncthreads();
-    if constexpr (!EXT_KS) ctr_xor_cta<R::ABITS>(p, aes, sa, cta, tid);    // A' -> A (few warps)
 
-    // C needs only B' (C19), so its SHA-512 unmask runs while the AES warps work
+    // C needs only B' (C19): its SHA-512 unmask runs before the keystream is needed
     const bool valid = blk < p.n_blocks;
     const uint64_t gb = p.block_offset + blk;
     uint32_t A[R::AW], B[R::BW], C[R::CW];
@@ -429,10 +377,8 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         smem_get_record<R::CW, R::CBITS>(sc, SC_W, (uint32_t)tid * R::CBITS, C);
         if (MASK && R::BBITS) mask_c<R::BW, R::BBYTES>(p, gb, B, C);          // C from B'
     }
-    if constexpr (EXT_KS) {
-        asm volatile("griddepcontrol.wait;" ::: "memory");                  // keystream kernel complete
-        xor_g2s(sa, p.ks + a0, alen, tid);                                   // A' -> A
-    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");                      // keystream kernel complete
+    xor_g2s(sa, p.ks + a0, alen, tid);                                       // A' -> A
     __syncthreads();                                                         // plain A ready
 
     bool bad = false;

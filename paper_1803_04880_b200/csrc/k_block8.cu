@@ -27,13 +27,13 @@ namespace se {
 template <int L, bool MASK>
 __global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
 k_protect_block8(const __grid_constant__ FusedParams p) {
-    protect_cta<L, MASK, 0, true>(p, blockIdx.x);
+    protect_cta<L, MASK, 0>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
 __global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
 k_recover_block8(const __grid_constant__ FusedParams p) {
-    recover_cta<L, MASK, 0, true>(p, blockIdx.x);
+    recover_cta<L, MASK, 0>(p, blockIdx.x);
 }
 
 // Many independent files in one launch (C5; SURVEY §8.6 "sharded by file").
@@ -87,11 +87,13 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
         sp.mid256[t - 44] = dv.mid256[t - 44];
     } else if (t >= 52 && t < 60) {
         sp.mid512[t - 52] = dv.mid512[t - 52];
+    } else if (t == 60) {
+        sp.ks = bp.ks ? bp.ks + job.cta_begin * 16ull * R::ABITS : nullptr;
     }
     __syncthreads();
     const uint64_t cta = x - job.cta_begin;
-    if (RECOVER) recover_cta<L, MASK>(sp, cta);
-    else protect_cta<L, MASK>(sp, cta);
+    if (RECOVER) recover_cta<L, MASK, 0>(sp, cta);
+    else protect_cta<L, MASK, 0>(sp, cta);
 }
 
 __global__ void k_report_init(se_report* r, uint32_t n) {
@@ -206,8 +208,8 @@ int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void
 
 template <int L, bool RECOVER>
 static void batch_l(const BatchParams& bp, uint64_t ctas, bool mask, cudaStream_t s) {
-    if (mask) k_batch_block8<L, true, RECOVER><<<(unsigned)ctas, kBlocksPerCta, 0, s>>>(bp);
-    else k_batch_block8<L, false, RECOVER><<<(unsigned)ctas, kBlocksPerCta, 0, s>>>(bp);
+    if (mask) launch_pdl(k_batch_block8<L, true, RECOVER>, (unsigned)ctas, kBlocksPerCta, s, bp);
+    else launch_pdl(k_batch_block8<L, false, RECOVER>, (unsigned)ctas, kBlocksPerCta, s, bp);
 }
 
 int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,

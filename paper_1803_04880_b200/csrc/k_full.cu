@@ -184,12 +184,12 @@ __global__ void __launch_bounds__(kFullThreads) k_dwt_full_inv(const __grid_cons
 
 template <int L, bool MASK>
 __global__ void __launch_bounds__(kBlocksPerCta, 4) k_protect_full(const __grid_constant__ FusedParams p) {
-    protect_cta<L, MASK, 1, true>(p, blockIdx.x);
+    protect_cta<L, MASK, 1>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
 __global__ void __launch_bounds__(kBlocksPerCta, 4) k_recover_full(const __grid_constant__ FusedParams p) {
-    recover_cta<L, MASK, 1, true>(p, blockIdx.x);
+    recover_cta<L, MASK, 1>(p, blockIdx.x);
 }
 
 // ---------------------------------------------------------------- launchers

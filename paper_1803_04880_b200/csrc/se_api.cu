@@ -351,6 +351,9 @@ int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels, cons
         if (fragment_layout(&g, &lay) != SE_OK) return SE_EINVAL;
         if ((job.block_offset * lay.a_bits) % 128) return SE_EINVAL;
         if (job.n_bytes && (!job.a || !job.c || (lay.b_bytes && !job.b))) return SE_EINVAL;
+        if (job.n_bytes && (!aligned16(job.a) || !aligned16(job.c) || (job.b && !aligned16(job.b)) ||
+                            !aligned16(job.in ? (const void*)job.in : (const void*)job.out)))
+            return SE_EALIGN;
         job.cta_begin = cta;
         cta += (lay.n_blocks + kBlocksPerCta - 1) / kBlocksPerCta;
         // per-file constants: counter base and SHA midstates over K || IV (C13, C15)
@@ -384,8 +387,19 @@ static int batch_common(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ct
     fragment_layout(&g, &lay);
     const uint8_t zero_iv[16] = {0};
     fill_fused(bp.base, &g, lay, key, zero_iv);       // shared fields: round keys, H(0), one
+    bp.total_ctas = total_ctas;
     const bool mask = !(flags & SE_FLAG_PUBLIC_PLAIN);
-    return launch_batch_block8(bp, total_ctas, levels, mask, recover, stream) ? SE_ECUDA : SE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    void* ks = nullptr;
+    if (recover && total_ctas) {                      // keystream scratch for every file's A stream
+        keep_pool();
+        if (cudaMallocAsync(&ks, total_ctas * 16ull * lay.a_bits + 16, s) != cudaSuccess) return SE_ECUDA;
+        bp.ks = (uint8_t*)ks;
+    }
+    int e = total_ctas ? launch_batch_keystream(bp, lay.a_bits, stream) : 0;
+    if (!e) e = launch_batch_block8(bp, total_ctas, levels, mask, recover, stream);
+    if (ks) cudaFreeAsync(ks, s);
+    return e ? SE_ECUDA : SE_OK;
 }
 
 int fragment_protect_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas, uint32_t levels,

@@ -50,6 +50,8 @@ static_assert(sizeof(JobDerived) <= sizeof(((se_job*)0)->derived), "se_job.deriv
 struct BatchParams {
     const se_job* jobs;       // device array, sorted by cta_begin
     se_report* reports;       // recover: one per job, nullable
+    uint8_t* ks;              // recover: keystream scratch, file j at cta_begin_j*16*a_bits
+    uint64_t total_ctas;
     uint32_t n_jobs;
     uint32_t pad_;
     FusedParams base;         // shared fields: rk, h256, h512, one
@@ -80,6 +82,7 @@ int launch_protect_block8(const FusedParams& p, uint32_t levels, bool mask, void
 int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
 int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,
                         void* stream);
+int launch_batch_keystream(const BatchParams& bp, uint32_t a_bits, void* stream);
 int launch_dwt_fwd_block8(const DwtParams& p, uint32_t levels, void* stream);
 // FULL mode (row a11): whole-matrix transform kernels and the footprint CTA kernels
 int launch_dwt_full_fwd(const DwtParams& p, uint32_t levels, void* stream);

@@ -9,12 +9,12 @@ timeout 600 python bench.py > gpurun_out/ev/bench.json 2> gpurun_out/ev/bench.er
 timeout 600 python bench.py --plain --no-cpu-baseline > gpurun_out/ev/bench_plain.json 2>> gpurun_out/ev/bench.err
 timeout 900 python bench.py --config 4 --steps 10 --no-cpu-baseline > gpurun_out/ev/bench_c4.json 2>> gpurun_out/ev/bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/ev/bench_ref.json 2>> gpurun_out/ev/bench.err
-CMD="python bench.py --steps 3 --warmup 3 --soak 0 --no-cpu-baseline --no-comparator --e2e-steps 1"
+CMD="python bench.py --steps 3 --warmup 3 --soak 0 --no-cpu-baseline --no-comparator --e2e-steps 0"
 $CMD > gpurun_out/ev/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/ev/launches.csv $CMD > gpurun_out/ev/ncu_launches.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_protect_block8 -s 2 -c 1 -o gpurun_out/ev/protect $CMD > gpurun_out/ev/ncu_p.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_recover_block8 -s 2 -c 1 -o gpurun_out/ev/recover $CMD > gpurun_out/ev/ncu_r.log 2>&1
-CMD2="python bench.py --steps 3 --warmup 3 --soak 0 --no-cpu-baseline --e2e-steps 1"
+CMD2="python tools/prof_cipher.py"
 $CMD2 > gpurun_out/ev/plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_cipher_ctr -s 2 -c 1 -o gpurun_out/ev/cipher $CMD2 > gpurun_out/ev/ncu_c.log 2>&1
 echo evidence done
