@@ -88,12 +88,116 @@ __device__ __forceinline__ uint32_t fshr(uint32_t x, int n, uint32_t one) {
 #endif
 }
 
+#ifndef SE_ROT_WIDE
+#define SE_ROT_WIDE 0
+#endif
+__device__ __forceinline__ void mulw(uint32_t x, uint32_t pw, uint32_t& lo, uint32_t& hi) {
+    uint64_t r;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(x), "r"(pw));
+    lo = (uint32_t)r;
+    hi = (uint32_t)(r >> 32);
+}
+
+// rotr64(v, N) = t1 ^ t2 (disjoint pieces), two IMAD.WIDE
+template <int N>
+__device__ __forceinline__ void ror64w(W64 v, uint32_t one, W64& t1, W64& t2) {
+    const uint32_t lo = N < 32 ? v.lo : v.hi, hi = N < 32 ? v.hi : v.lo;
+    constexpr int n = N < 32 ? N : N - 32;
+    uint32_t pl, ph, ql, qh;
+    mulw(lo, one << (32 - n), pl, ph);               // ph = lo >> n, pl = lo << (32-n)
+    mulw(hi, one << (32 - n), ql, qh);               // qh = hi >> n, ql = hi << (32-n)
+    t1 = W64{ph, qh};
+    t2 = W64{ql, pl};
+}
+__device__ __forceinline__ W64 x64(W64 a, W64 b) { return W64{a.lo ^ b.lo, a.hi ^ b.hi}; }
+
 template <int N>
 __device__ __forceinline__ W64 shr64(W64 v, uint32_t one) {   // N < 32
     return W64{__funnelshift_r(v.lo, v.hi, N), fshr(v.hi, N, one)};
 }
 
 __device__ __forceinline__ uint32_t ror32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+// ---------------------------------------------------------------- rotations on the FMA pipe
+// x * 2^k as a 64-bit product is {hi: x >> (32-k), lo: x << k}: one IMAD.WIDE
+// (FMA pipe, two issue slots) yields both pieces of a rotation, which enter
+// the XOR tree separately.  Trades ~1 ALU op for ~4 FMA slots (SE_ROT_WIDE
+// bit mask).  Measured on B200 (C2 protect, GB/s): off 182, schedule sigmas
+// 166, all 149 — IMAD.WIDE costs more than its issue slots (latency, register
+// pairs), so the default is off; kept for future re-tuning.
+// rotr32(x, n) = a ^ b (disjoint pieces)
+__device__ __forceinline__ void ror32w(uint32_t x, int n, uint32_t one, uint32_t& a, uint32_t& b) {
+    mulw(x, one << (32 - n), b, a);                   // a = x >> n, b = x << (32-n)
+}
+
+// FIPS 180-4 §4.1.2 / §4.1.3 functions.  SE_ROT_WIDE bits: 1 SHA-512 sigma
+// (schedule), 2 SHA-512 Sigma, 4 SHA-256 Sigma, 8 SHA-256 sigma: two of the
+// three rotations through IMAD.WIDE.
+__device__ __forceinline__ uint32_t Sig0_256(uint32_t a, uint32_t one) {
+#if SE_ROT_WIDE & 4
+    uint32_t p, q, r, t;
+    ror32w(a, 2, one, p, q);
+    ror32w(a, 13, one, r, t);
+    return p ^ q ^ r ^ t ^ ror32(a, 22);
+#else
+    (void)one;
+    return ror32(a, 2) ^ ror32(a, 13) ^ ror32(a, 22);
+#endif
+}
+__device__ __forceinline__ uint32_t Sig1_256(uint32_t e, uint32_t one) {
+#if SE_ROT_WIDE & 4
+    uint32_t p, q, r, t;
+    ror32w(e, 6, one, p, q);
+    ror32w(e, 11, one, r, t);
+    return p ^ q ^ r ^ t ^ ror32(e, 25);
+#else
+    (void)one;
+    return ror32(e, 6) ^ ror32(e, 11) ^ ror32(e, 25);
+#endif
+}
+__device__ __forceinline__ uint32_t sig0_256(uint32_t w, uint32_t one) {
+#if SE_ROT_WIDE & 8
+    uint32_t p, q, r, t;
+    ror32w(w, 7, one, p, q);
+    ror32w(w, 18, one, r, t);
+    return p ^ q ^ r ^ t ^ fshr(w, 3, one);
+#else
+    return ror32(w, 7) ^ ror32(w, 18) ^ fshr(w, 3, one);
+#endif
+}
+__device__ __forceinline__ uint32_t sig1_256(uint32_t w, uint32_t one) {
+#if SE_ROT_WIDE & 8
+    uint32_t p, q, r, t;
+    ror32w(w, 17, one, p, q);
+    ror32w(w, 19, one, r, t);
+    return p ^ q ^ r ^ t ^ fshr(w, 10, one);
+#else
+    return ror32(w, 17) ^ ror32(w, 19) ^ fshr(w, 10, one);
+#endif
+}
+template <int A, int B, int C, bool WIDE>
+__device__ __forceinline__ W64 sig3_512(W64 v, uint32_t one) {       // ror A ^ ror B ^ ror C
+    if constexpr (WIDE) {
+        W64 p, q, r, t;
+        ror64w<A>(v, one, p, q);
+        ror64w<B>(v, one, r, t);
+        return x64(x64(p, q), x64(x64(r, t), ror64<C>(v)));
+    } else {
+        return xor3(ror64<A>(v), ror64<B>(v), ror64<C>(v));
+    }
+}
+template <int A, int B, int S, bool WIDE>
+__device__ __forceinline__ W64 sig2s_512(W64 v, uint32_t one) {     // ror A ^ ror B ^ shr S
+    if constexpr (WIDE) {
+        W64 p, q, r, t;
+        ror64w<A>(v, one, p, q);
+        ror64w<B>(v, one, r, t);
+        return x64(x64(p, q), x64(x64(r, t), shr64<S>(v, one)));
+    } else {
+        return xor3(ror64<A>(v), ror64<B>(v), shr64<S>(v, one));
+    }
+}
+
 
 // ---------------------------------------------------------------- SHA-256
 
@@ -109,10 +213,10 @@ __device__ __forceinline__ void sha256_round(uint32_t (&S)[8], uint32_t kw, uint
     uint32_t& f = S[(5 - T) & 7];
     uint32_t& g = S[(6 - T) & 7];
     uint32_t& h = S[(7 - T) & 7];
-    const uint32_t S1 = ror32(e, 6) ^ ror32(e, 11) ^ ror32(e, 25);
+    const uint32_t S1 = Sig1_256(e, one);
     const uint32_t ch = (e & f) ^ (~e & g);
     const uint32_t t1 = fadd(fadd(fadd(h, S1, one), ch, one), kw, one);
-    const uint32_t S0 = ror32(a, 2) ^ ror32(a, 13) ^ ror32(a, 22);
+    const uint32_t S0 = Sig0_256(a, one);
     const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
     d = fadd(d, t1, one);                  // new e
     h = fadd(fadd(t1, S0, one), mj, one);  // new a
@@ -121,8 +225,8 @@ __device__ __forceinline__ void sha256_round(uint32_t (&S)[8], uint32_t kw, uint
 template <int J>
 __device__ __forceinline__ uint32_t sha256_sched(uint32_t (&W)[16], uint32_t one) {
     const uint32_t w2 = W[(J - 2) & 15], w15 = W[(J - 15) & 15];
-    const uint32_t s1 = ror32(w2, 17) ^ ror32(w2, 19) ^ fshr(w2, 10, one);
-    const uint32_t s0 = ror32(w15, 7) ^ ror32(w15, 18) ^ fshr(w15, 3, one);
+    const uint32_t s1 = sig1_256(w2, one);
+    const uint32_t s0 = sig0_256(w15, one);
     const uint32_t w = fadd(fadd(fadd(s1, W[(J - 7) & 15], one), s0, one), W[J & 15], one);
     W[J & 15] = w;
     return w;
@@ -161,8 +265,8 @@ __device__ __forceinline__ void sha256_sched8_rounds(uint32_t (&S)[8], uint32_t 
                                                      const uint32_t* k, uint32_t one) {
     if constexpr (J < 8) {
         const uint32_t w2 = win32<J - 2>(W, N), w15 = win32<J - 15>(W, N);
-        const uint32_t s1 = ror32(w2, 17) ^ ror32(w2, 19) ^ fshr(w2, 10, one);
-        const uint32_t s0 = ror32(w15, 7) ^ ror32(w15, 18) ^ fshr(w15, 3, one);
+        const uint32_t s1 = sig1_256(w2, one);
+        const uint32_t s0 = sig0_256(w15, one);
         N[J] = fadd(fadd(fadd(s1, win32<J - 7>(W, N), one), s0, one), win32<J - 16>(W, N), one);
         sha256_round<J>(S, fadd(N[J], k[J], one), one);
         sha256_sched8_rounds<J + 1>(S, W, N, k, one);
@@ -212,10 +316,10 @@ __device__ __forceinline__ void sha512_round(W64 (&S)[8], W64 kw, uint32_t one) 
     W64& f = S[(5 - T) & 7];
     W64& g = S[(6 - T) & 7];
     W64& h = S[(7 - T) & 7];
-    const W64 S1 = xor3(ror64<14>(e), ror64<18>(e), ror64<41>(e));
+    const W64 S1 = sig3_512<14, 18, 41, (SE_ROT_WIDE & 2) != 0>(e, one);
     const W64 ch = W64{(e.lo & f.lo) ^ (~e.lo & g.lo), (e.hi & f.hi) ^ (~e.hi & g.hi)};
     const W64 t1 = fadd64(fadd64(fadd64(h, S1, one), ch, one), kw, one);
-    const W64 S0 = xor3(ror64<28>(a), ror64<34>(a), ror64<39>(a));
+    const W64 S0 = sig3_512<34, 39, 28, (SE_ROT_WIDE & 2) != 0>(a, one);
     const W64 mj = W64{(a.lo & b.lo) ^ (a.lo & c.lo) ^ (b.lo & c.lo), (a.hi & b.hi) ^ (a.hi & c.hi) ^ (b.hi & c.hi)};
     d = fadd64(d, t1, one);
     h = fadd64(fadd64(t1, S0, one), mj, one);
@@ -224,8 +328,8 @@ __device__ __forceinline__ void sha512_round(W64 (&S)[8], W64 kw, uint32_t one) 
 template <int J>
 __device__ __forceinline__ W64 sha512_sched(W64 (&W)[16], uint32_t one) {
     const W64 w2 = W[(J - 2) & 15], w15 = W[(J - 15) & 15];
-    const W64 s1 = xor3(ror64<19>(w2), ror64<61>(w2), shr64<6>(w2, one));
-    const W64 s0 = xor3(ror64<1>(w15), ror64<8>(w15), shr64<7>(w15, one));
+    const W64 s1 = sig2s_512<19, 61, 6, (SE_ROT_WIDE & 1) != 0>(w2, one);
+    const W64 s0 = sig2s_512<1, 8, 7, (SE_ROT_WIDE & 1) != 0>(w15, one);
     const W64 w = fadd64(fadd64(fadd64(s1, W[(J - 7) & 15], one), s0, one), W[J & 15], one);
     W[J & 15] = w;
     return w;
@@ -266,8 +370,8 @@ __device__ __forceinline__ void sha512_sched8_rounds(W64 (&S)[8], W64 (&W)[16], 
                                                      uint32_t one) {
     if constexpr (J < 8) {
         const W64 w2 = win<J - 2>(W, N), w15 = win<J - 15>(W, N);
-        const W64 s1 = xor3(ror64<19>(w2), ror64<61>(w2), shr64<6>(w2, one));
-        const W64 s0 = xor3(ror64<1>(w15), ror64<8>(w15), shr64<7>(w15, one));
+        const W64 s1 = sig2s_512<19, 61, 6, (SE_ROT_WIDE & 1) != 0>(w2, one);
+        const W64 s0 = sig2s_512<1, 8, 7, (SE_ROT_WIDE & 1) != 0>(w15, one);
         N[J] = fadd64(fadd64(fadd64(s1, win<J - 7>(W, N), one), s0, one), win<J - 16>(W, N), one);
         sha512_round<J>(S, fadd64(N[J], w64(k[J]), one), one);
         sha512_sched8_rounds<J + 1>(S, W, N, k, one);
