@@ -458,7 +458,7 @@ def run_multi(args):
     }
 
 
-def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=2 << 20, n_streams=4):
+def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=8 << 20, n_streams=4):
     """The same metric end to end through the public host API: one step =
     fragment_protect_host (pinned input -> H2D -> fused kernel -> D2H of the three
     fragments) + fragment_recover_host (H2D fragments -> kernel -> D2H bytes);
