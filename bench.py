@@ -266,6 +266,27 @@ def run_se(args):
         aes_gbs = n * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
         del y
 
+    # ---- NEXT row f2: security battery on the protected public fragment C'
+    #      vs the original (one pass of se_stats_accumulate), timed + metrics
+    battery = None
+    if not args.no_comparator:
+        xs = x[: cc.numel()]
+        st, jt = se.stats_accumulate(cc, W, x=xs, stream=stream)
+        stream.synchronize()
+        metrics = se.stats_metrics(st, jt)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(5):
+                st.zero_()
+                jt.zero_()
+                se.stats_accumulate(cc, W, x=xs, stats=st, joint=jt, stream=stream)
+            e1.record(stream)
+        stream.synchronize()
+        battery = {"input_gbs": round(2 * cc.numel() * 5 / (e0.elapsed_time(e1) / 1e3) / 1e9, 2),
+                   "on": "C' vs original (first |C'| bytes)",
+                   **{k: (round(v, 6) if isinstance(v, float) else v) for k, v in metrics.items()}}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -321,6 +342,7 @@ def run_se(args):
         "protect_gbs": round(n / (mp / 1e3) / 1e9, 3),
         "recover_gbs": round(n / (mr / 1e3) / 1e9, 3),
         "comparator_aes128_ctr_gbs": None if aes_gbs is None else round(aes_gbs, 2),
+        "security_battery": battery,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,

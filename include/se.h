@@ -173,6 +173,31 @@ int cipher_encrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_blo
 int cipher_decrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block_offset,
                    const void* d_in, void* d_out, uint64_t n, void* stream);
 
+/* ---- security battery (NEXT row f2) --------------------------------------
+ * The paper validates the public fragments statistically (PAPER.md "Security
+ * analysis"): PDF / uniformity, entropy Eq. 5.6
+ * (P:2454-2463), correlation r_xy Eq. 5.8 between original and fragment
+ * and between adjacent elements h / v / d, bit
+ * difference Dif, NMI, key sensitivity KS = bit difference
+ * of the fragments under two keys one bit apart.
+ * se_stats_accumulate makes ONE pass over two equal-length byte sequences
+ * x and y (y also read as a W-wide matrix for the adjacency sums) and ADDS
+ * exact integer sums into a caller-zeroed, device-resident se_stats (and,
+ * if d_joint != NULL, into a 65536-bin joint histogram indexed x*256 + y,
+ * for NMI).  The metrics are plain arithmetic on these sums (binding:
+ * paper_1803_04880_b200.stats_metrics).  d_x may be NULL (y-only sums). */
+typedef struct {
+    uint64_t n;                      /* byte pairs accumulated                 */
+    uint64_t hist_x[256], hist_y[256];
+    uint64_t sx, sy, sxx, syy, sxy;  /* moments of x, y over the n pairs       */
+    uint64_t diff_bits;              /* popcount(x ^ y)                        */
+    uint64_t adj[3][6];              /* y pairs (a, b) horizontal, vertical,
+                                        diagonal: count, sa, sb, saa, sbb, sab */
+} se_stats;
+
+int se_stats_accumulate(const void* d_x, const void* d_y, uint64_t n, uint32_t width, se_stats* d_stats,
+                        uint32_t* d_joint, void* stream);
+
 /* ---- misc ----------------------------------------------------------------- */
 const char* se_strerror(int status);
 /* Number of kernel launches issued by this thread since the last reset

@@ -16,7 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
-SOURCES = ["dwt53.c", "aes128.c", "sha2.c", "protect.c"]
+SOURCES = ["dwt53.c", "aes128.c", "sha2.c", "protect.c", "stats.c"]
 
 MODE_BLOCK8 = 0
 MODE_FULL = 1
@@ -70,6 +70,7 @@ def lib():
                                            _u8p, _u8p, _u8p, _u8p, _i64p, u64, u64]
         L.oracle_dwt2_fwd_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
         L.oracle_dwt2_inv_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
+        L.oracle_stats.argtypes = [_u8p, _u8p, u64, u32, _u64p, _u64p]
         L.oracle_record_fields.argtypes = [u32, u32, C.c_int, _i32p, _i32p, _i32p, _i32p, _i32p]
         _lib = L
     return _lib
@@ -223,3 +224,18 @@ def recover(a, b, c, n_bytes: int, width: int, levels: int, key: bytes, iv: byte
     if rc:
         raise ValueError(f"oracle_recover failed rc={rc}")
     return o[:n_bytes], (int(rep[0]), int(rep[1]))
+
+
+STATS_WORDS = 1 + 256 + 256 + 6 + 18
+
+
+def stats(y, width: int, x=None, joint: bool = True):
+    """The security-battery sums (oracle/stats.c): (words uint64[STATS_WORDS], joint uint64[65536] or None)."""
+    yy = _u8(y)
+    xx = _u8(x) if x is not None else None
+    n = yy.size if xx is None else min(xx.size, yy.size)
+    out = np.zeros(STATS_WORDS, dtype=np.uint64)
+    jt = np.zeros(65536, dtype=np.uint64) if (joint and xx is not None) else None
+    lib().oracle_stats(_p(xx, _u8p) if xx is not None else None, _p(yy, _u8p), n, width, _p(out, _u64p),
+                       _p(jt, _u64p) if jt is not None else None)
+    return out, jt

@@ -101,6 +101,11 @@ int oracle_recover(uint64_t n_bytes, uint32_t width, uint32_t levels,
                    const uint8_t* a, const uint8_t* b, const uint8_t* c,
                    uint8_t* out, int64_t report[2]);
 
+/* ---- security battery sums (NEXT row f2) -------------------- */
+#define ORACLE_STATS_WORDS (1 + 256 + 256 + 6 + 18)
+void oracle_stats(const uint8_t* x, const uint8_t* y, uint64_t n, uint32_t width, uint64_t* out,
+                  uint64_t* joint);
+
 /* ---- exposed internals used by the pins --------------------------------- */
 /* Multi-level dyadic 2-D lifting in place on the top-left rows x cols region
  * of an int32 array with row stride `stride` (any magnitude; used by the

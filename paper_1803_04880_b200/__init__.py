@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libse.so")
 CSRC = os.path.join(_HERE, "csrc")
-SOURCES = ["se_api.cu", "k_block8.cu", "k_full.cu", "k_cipher.cu", "k_batch.cu", "se_host.cu"]
+SOURCES = ["se_api.cu", "k_block8.cu", "k_full.cu", "k_cipher.cu", "k_stats.cu", "se_host.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
 
@@ -91,7 +91,7 @@ class Job(C.Structure):
 SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_batch_plan",
            "fragment_protect_batch", "fragment_recover_batch", "fragment_protect_host",
            "fragment_recover_host", "dwt_fwd", "dwt_inv", "cipher_encrypt", "cipher_decrypt",
-           "se_strerror", "se_launch_count"]
+           "se_stats_accumulate", "se_strerror", "se_launch_count"]
 
 _lib = None
 
@@ -119,6 +119,7 @@ def lib():
         L.dwt_inv.argtypes = [gp, vp, vp, vp]
         L.cipher_encrypt.argtypes = [u8p, u8p, C.c_uint64, vp, vp, C.c_uint64, vp]
         L.cipher_decrypt.argtypes = [u8p, u8p, C.c_uint64, vp, vp, C.c_uint64, vp]
+        L.se_stats_accumulate.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp, vp]
         L.se_strerror.argtypes = [C.c_int]
         L.se_strerror.restype = C.c_char_p
         L.se_launch_count.argtypes = [C.c_int]
@@ -321,3 +322,69 @@ def fragment_recover_host(a, b, c, n_bytes: int, width: int, levels: int, key, i
                                        _ptr(b) if b is not None and b.numel() else None, _ptr(c), _ptr(o),
                                        C.byref(rep), int(chunk_bytes), int(n_streams)), "fragment_recover_host")
     return o, (int(rep.first_bad_block), int(rep.bad_blocks))
+
+
+# ---------------------------------------------------------------- security battery (f2)
+
+STATS_WORDS = 1 + 256 + 256 + 6 + 18          # se_stats as uint64 words
+
+
+def stats_accumulate(y, width: int, x=None, stats=None, joint=None, stream=None):
+    """One pass of se_stats_accumulate over device byte tensors x (optional) and y.
+    Returns (stats int64 tensor of STATS_WORDS, joint int32 tensor of 65536 or None);
+    pass the returned tensors back in to accumulate more data."""
+    import torch
+    dev = y.device
+    st = stats if stats is not None else torch.zeros(STATS_WORDS, dtype=torch.int64, device=dev)
+    jt = joint if joint is not None else (torch.zeros(65536, dtype=torch.int32, device=dev) if x is not None else None)
+    n = y.numel() if x is None else min(x.numel(), y.numel())
+    _check(lib().se_stats_accumulate(_ptr(x), _ptr(y), n, int(width), _ptr(st), _ptr(jt), _stream(stream)),
+           "se_stats_accumulate")
+    return st, jt
+
+
+def stats_metrics(stats, joint=None) -> dict:
+    """The paper's metrics from the exact sums (host arithmetic):
+    entropy Eq. 5.6 and chi^2 of y's byte PDF, r_xy Eq. 5.8, bit difference
+    Dif (= KS when x, y are fragments under two keys),
+    adjacent-pair correlation of y (h, v, d), NMI as
+    I(X;Y) / sqrt(H(X) H(Y))."""
+    import math
+    s = [int(v) for v in (stats.tolist() if hasattr(stats, "tolist") else stats)]
+    n = s[0]
+    hx, hy = s[1:257], s[257:513]
+    sx, sy, sxx, syy, sxy, diff = s[513:519]
+    adj = [s[519 + 6 * d: 525 + 6 * d] for d in range(3)]
+
+    def ent(h):
+        t = sum(h)
+        return -sum(c / t * math.log2(c / t) for c in h if c) if t else 0.0
+
+    def corr(cnt, a, b, aa, bb, ab):
+        if cnt == 0:
+            return float("nan")
+        ea, eb = a / cnt, b / cnt
+        da, db = aa / cnt - ea * ea, bb / cnt - eb * eb
+        cov = ab / cnt - ea * eb
+        return cov / math.sqrt(da * db) if da > 0 and db > 0 else float("nan")
+    m = {"n": n, "entropy_y": ent(hy), "entropy_x": ent(hx) if any(hx) else None,
+         "chi2_y": sum((c - n / 256) ** 2 / (n / 256) for c in hy) if n else None,
+         "r_xy": corr(n, sx, sy, sxx, syy, sxy) if any(hx) else None,
+         "dif_bits_pct": 100.0 * diff / (8 * n) if n and any(hx) else None,
+         "rho_h": corr(*adj[0]), "rho_v": corr(*adj[1]), "rho_d": corr(*adj[2])}
+    if joint is not None:
+        j = [int(v) for v in joint.tolist()]
+        tot = sum(j)
+        mi = 0.0
+        for xi in range(256):
+            px = hx[xi] / tot if tot else 0
+            if not px:
+                continue
+            for yi in range(256):
+                c = j[xi * 256 + yi]
+                if c:
+                    pxy = c / tot
+                    mi += pxy * math.log2(pxy / (px * hy[yi] / tot))
+        hxe, hye = ent(hx), ent(hy)
+        m["nmi"] = mi / math.sqrt(hxe * hye) if hxe > 0 and hye > 0 else 0.0
+    return m

@@ -341,6 +341,14 @@ int cipher_decrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_blo
     return cipher_encrypt(key, iv, ctr_block_offset, d_in, d_out, n, stream);
 }
 
+int se_stats_accumulate(const void* d_x, const void* d_y, uint64_t n, uint32_t width, se_stats* d_stats,
+                        uint32_t* d_joint, void* stream) {
+    if (width == 0 || !d_stats) return SE_EINVAL;
+    if (n == 0) return SE_OK;
+    if (!d_y) return SE_EINVAL;
+    return launch_stats(d_x, d_y, n, width, d_stats, d_x ? d_joint : nullptr, stream) ? SE_ECUDA : SE_OK;
+}
+
 int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels, const uint8_t key[16]) {
     if (!jobs || !key || levels < 1 || levels > 3) return SE_EINVAL;
     uint64_t cta = 0;

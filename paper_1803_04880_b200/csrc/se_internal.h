@@ -92,6 +92,9 @@ int launch_recover_full(const FusedParams& p, uint32_t levels, bool mask, void* 
 int launch_dwt_inv_block8(const DwtParams& p, uint32_t levels, void* stream);
 int launch_cipher_ctr(const CipherParams& p, void* stream);
 
+int launch_stats(const void* x, const void* y, uint64_t n, uint32_t width, se_stats* out, uint32_t* joint,
+                 void* stream);
+
 void note_launch();
 template <typename P>
 void launch_pdl(void (*kernel)(P), unsigned grid, unsigned block, cudaStream_t s, const P& p);
