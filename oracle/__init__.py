@@ -16,7 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
-SOURCES = ["dwt53.c", "aes128.c", "sha2.c", "protect.c", "stats.c"]
+SOURCES = ["dwt53.c", "aes128.c", "sha2.c", "protect.c", "stats.c", "dct.c"]
 
 MODE_BLOCK8 = 0
 MODE_FULL = 1
@@ -33,7 +33,7 @@ def build(force: bool = False) -> str:
             return LIB_PATH
     tmp = LIB_PATH + f".tmp{os.getpid()}"
     cmd = ["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
-           "-o", tmp] + srcs
+           "-o", tmp] + srcs + ["-lm"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
@@ -71,6 +71,14 @@ def lib():
         L.oracle_dwt2_fwd_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
         L.oracle_dwt2_inv_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
         L.oracle_stats.argtypes = [_u8p, _u8p, u64, u32, _u64p, _u64p]
+        _f64p = C.POINTER(C.c_double)
+        L.oracle_dct_basis.argtypes = [_f64p]
+        L.oracle_dct8_fwd.argtypes = [_f64p, _f64p]
+        L.oracle_dct8_inv.argtypes = [_f64p, _f64p]
+        L.oracle_dct_layout.argtypes = [u32, u32, u32, _u64p]
+        L.oracle_dct_select.argtypes = [u32, u32, u32, _u8p, _f64p]
+        L.oracle_dct_protect.argtypes = [u32, u32, u32, u32, u32, u64, _u8p, _u8p, _u8p, _u8p, _u8p, _f64p]
+        L.oracle_dct_recover.argtypes = [u32, u32, u32, u32, u32, u64, _u8p, _u8p, _u8p, _u8p, _u8p, _f64p]
         L.oracle_record_fields.argtypes = [u32, u32, C.c_int, _i32p, _i32p, _i32p, _i32p, _i32p]
         _lib = L
     return _lib
@@ -239,3 +247,82 @@ def stats(y, width: int, x=None, joint: bool = True):
     lib().oracle_stats(_p(xx, _u8p) if xx is not None else None, _p(yy, _u8p), n, width, _p(out, _u64p),
                        _p(jt, _u64p) if jt is not None else None)
     return out, jt
+
+
+# ---------------------------------------------------------------- Chapter 4 DCT SE (NEXT row f3, dct.c)
+
+DCT_KEYED = 1
+_f64p = C.POINTER(C.c_double)
+
+
+def dct_basis() -> np.ndarray:
+    """Eq. 4.6 layout: m[x, u] = alpha(u) cos(pi (2x+1) u / 16)."""
+    m = np.zeros((8, 8))
+    lib().oracle_dct_basis(_p(m, _f64p))
+    return m
+
+
+def dct8_fwd(f) -> np.ndarray:
+    f = np.ascontiguousarray(f, dtype=np.float64).reshape(8, 8)
+    c = np.zeros((8, 8))
+    lib().oracle_dct8_fwd(_p(f, _f64p), _p(c, _f64p))
+    return c
+
+
+def dct8_inv(c) -> np.ndarray:
+    c = np.ascontiguousarray(c, dtype=np.float64).reshape(8, 8)
+    f = np.zeros((8, 8))
+    lib().oracle_dct8_inv(_p(c, _f64p), _p(f, _f64p))
+    return f
+
+
+def dct_layout(width: int, height: int, channels: int = 1) -> dict:
+    out = np.zeros(4, dtype=np.uint64)
+    if lib().oracle_dct_layout(width, height, channels, _p(out, _u64p)):
+        raise ValueError(f"invalid DCT geometry {width}x{height}x{channels}")
+    return dict(zip(["records", "bits", "a_bytes", "p_bytes"], (int(v) for v in out)))
+
+
+def dct_select(img, width: int, height: int, channels: int = 1) -> np.ndarray:
+    """(records, 6) real coefficients [0,0],[0,1],[1,0],[2,0],[1,1],[0,2]."""
+    lay = dct_layout(width, height, channels)
+    x = _u8(img)
+    assert x.size == lay["p_bytes"]
+    out = np.zeros((lay["records"], 6))
+    assert lib().oracle_dct_select(width, height, channels, _p(x, _u8p), _p(out, _f64p)) == 0
+    return out
+
+
+def dct_protect(img, width: int, height: int, channels: int, level: int, key: bytes, iv: bytes,
+                flags: int = 0, block_offset: int = 0, real: bool = False):
+    """Returns (a, p) or (a, p, p_real[records, 64]) — p_real before rounding and masking."""
+    lay = dct_layout(width, height, channels)
+    x = _u8(img)
+    assert x.size == lay["p_bytes"]
+    a = np.zeros(max(lay["a_bytes"], 1), dtype=np.uint8)
+    p = np.zeros(lay["p_bytes"], dtype=np.uint8)
+    pr = np.zeros((lay["records"], 64)) if real else None
+    k, v = _u8(key), _u8(iv)
+    rc = lib().oracle_dct_protect(width, height, channels, level, flags, block_offset, _p(k, _u8p), _p(v, _u8p),
+                                  _p(x, _u8p), _p(a, _u8p), _p(p, _u8p), _p(pr, _f64p) if real else None)
+    if rc:
+        raise ValueError(f"oracle_dct_protect failed rc={rc}")
+    return (a[:lay["a_bytes"]], p, pr) if real else (a[:lay["a_bytes"]], p)
+
+
+def dct_recover(a, p, width: int, height: int, channels: int, level: int, key: bytes, iv: bytes,
+                flags: int = 0, block_offset: int = 0, real: bool = False):
+    """Returns out or (out, out_real[records, 64]) — out_real before rounding."""
+    lay = dct_layout(width, height, channels)
+    aa, pp = _u8(a), _u8(p)
+    assert aa.size >= lay["a_bytes"] and pp.size == lay["p_bytes"]
+    if aa.size == 0:
+        aa = np.zeros(1, np.uint8)
+    out = np.zeros(lay["p_bytes"], dtype=np.uint8)
+    orl = np.zeros((lay["records"], 64)) if real else None
+    k, v = _u8(key), _u8(iv)
+    rc = lib().oracle_dct_recover(width, height, channels, level, flags, block_offset, _p(k, _u8p), _p(v, _u8p),
+                                  _p(aa, _u8p), _p(pp, _u8p), _p(out, _u8p), _p(orl, _f64p) if real else None)
+    if rc:
+        raise ValueError(f"oracle_dct_recover failed rc={rc}")
+    return (out, orl) if real else out

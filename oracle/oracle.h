@@ -106,6 +106,26 @@ int oracle_recover(uint64_t n_bytes, uint32_t width, uint32_t levels,
 void oracle_stats(const uint8_t* x, const uint8_t* y, uint64_t n, uint32_t width, uint64_t* out,
                   uint64_t* joint);
 
+/* ---- Chapter 4 DCT 8x8 selective encryption (NEXT row f3, dct.c) --------
+ * Readings D1-D12 in dct.c and DESIGN.md §3.  Image W x H (multiples of 8)
+ * with `channels` interleaved layers; records of 66 bits. */
+#define ORACLE_DCT_KEYED 1u
+void oracle_dct_basis(double m[64]);                       /* Eq. 4.6, m[x*8+u] */
+void oracle_dct8_fwd(const double f[64], double c[64]);    /* Eq. 4.1 */
+void oracle_dct8_inv(const double c[64], double f[64]);    /* Eq. 4.2 */
+/* out[0]=records, out[1]=66, out[2]=Fragment-1 bytes, out[3]=Fragment-2 bytes */
+int oracle_dct_layout(uint32_t width, uint32_t height, uint32_t channels, uint64_t out[4]);
+/* the 6 selected real coefficients per record (DC from Eq. 4.4) */
+int oracle_dct_select(uint32_t width, uint32_t height, uint32_t channels, const uint8_t* in, double* coef6);
+/* p_real / out_real (optional, 64 doubles per record, block row-major):
+ * the real values before rounding to bytes (used by the tests to find ties). */
+int oracle_dct_protect(uint32_t width, uint32_t height, uint32_t channels, uint32_t level, uint32_t flags,
+                       uint64_t block_offset, const uint8_t key[16], const uint8_t iv[16], const uint8_t* in,
+                       uint8_t* a, uint8_t* p, double* p_real);
+int oracle_dct_recover(uint32_t width, uint32_t height, uint32_t channels, uint32_t level, uint32_t flags,
+                       uint64_t block_offset, const uint8_t key[16], const uint8_t iv[16], const uint8_t* a,
+                       const uint8_t* p, uint8_t* out, double* out_real);
+
 /* ---- exposed internals used by the pins --------------------------------- */
 /* Multi-level dyadic 2-D lifting in place on the top-left rows x cols region
  * of an int32 array with row stride `stride` (any magnitude; used by the
