@@ -19,7 +19,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libse.so")
 CSRC = os.path.join(_HERE, "csrc")
-SOURCES = ["se_api.cu", "k_block8.cu", "k_full.cu", "k_cipher.cu", "k_stats.cu", "se_host.cu"]
+SOURCES = ["se_api.cu", "k_block8.cu", "k_full.cu", "k_cipher.cu", "k_stats.cu", "se_host.cu",
+           "k_dct.cu", "se_dct_api.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
 
@@ -38,7 +39,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     another in-tree path, selectable at load time with SE_LIB_PATH."""
     target = out or LIB_PATH
     deps = sources() + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    deps.append(os.path.join(_ROOT, "include", "se.h"))
+    deps += [os.path.join(_ROOT, "include", h) for h in ("se.h", "se_dct.h")]
     if not force and os.path.exists(target):
         if os.path.getmtime(target) >= max(os.path.getmtime(p) for p in deps):
             return target
@@ -91,7 +92,19 @@ class Job(C.Structure):
 SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_batch_plan",
            "fragment_protect_batch", "fragment_recover_batch", "fragment_protect_host",
            "fragment_recover_host", "dwt_fwd", "dwt_inv", "cipher_encrypt", "cipher_decrypt",
-           "se_stats_accumulate", "se_strerror", "se_launch_count"]
+           "se_stats_accumulate", "se_strerror", "se_launch_count",
+           "dct_layout", "dct_protect", "dct_recover", "dct_select"]
+
+
+class DctGeom(C.Structure):
+    _fields_ = [("width", C.c_uint32), ("height", C.c_uint32), ("channels", C.c_uint32),
+                ("level", C.c_uint32), ("flags", C.c_uint32), ("reserved", C.c_uint32),
+                ("block_offset", C.c_uint64)]
+
+
+class DctLayout(C.Structure):
+    _fields_ = [("records", C.c_uint64), ("a_bytes", C.c_uint64), ("p_bytes", C.c_uint64),
+                ("a_bits", C.c_uint32), ("reserved", C.c_uint32)]
 
 _lib = None
 
@@ -120,6 +133,11 @@ def lib():
         L.cipher_encrypt.argtypes = [u8p, u8p, C.c_uint64, vp, vp, C.c_uint64, vp]
         L.cipher_decrypt.argtypes = [u8p, u8p, C.c_uint64, vp, vp, C.c_uint64, vp]
         L.se_stats_accumulate.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp, vp]
+        dg = C.POINTER(DctGeom)
+        L.dct_layout.argtypes = [dg, C.POINTER(DctLayout)]
+        L.dct_protect.argtypes = [dg, u8p, u8p, vp, vp, vp, vp]
+        L.dct_recover.argtypes = [dg, u8p, u8p, vp, vp, vp, vp]
+        L.dct_select.argtypes = [dg, vp, vp, vp]
         L.se_strerror.argtypes = [C.c_int]
         L.se_strerror.restype = C.c_char_p
         L.se_launch_count.argtypes = [C.c_int]
@@ -229,6 +247,55 @@ def cipher_decrypt(key, iv, x, ctr_block_offset: int = 0, out=None, stream=None)
     o = out if out is not None else _empty(x.numel(), x.device)
     _check(lib().cipher_decrypt(_bytes16(key, "key"), _bytes16(iv, "iv"), int(ctr_block_offset), _ptr(x),
                                 _ptr(o), x.numel(), _stream(stream)), "cipher_decrypt")
+    return o
+
+
+# ---------------------------------------------------------------- Chapter 4 DCT SE (row f3, se_dct.h)
+
+DCT_KEYED = 1
+
+
+def _dgeom(width, height, channels, level, flags=0, block_offset=0) -> DctGeom:
+    return DctGeom(int(width), int(height), int(channels), int(level), int(flags), 0, int(block_offset))
+
+
+def dct_layout(width: int, height: int, channels: int = 1, level: int = 1, flags: int = 0,
+               block_offset: int = 0) -> dict:
+    out = DctLayout()
+    _check(lib().dct_layout(C.byref(_dgeom(width, height, channels, level, flags, block_offset)), C.byref(out)),
+           "dct_layout")
+    return {k: int(getattr(out, k)) for k, _ in DctLayout._fields_ if k != "reserved"}
+
+
+def dct_protect(img, width: int, height: int, channels: int, level: int, key, iv, flags: int = 0,
+                block_offset: int = 0, out=None, stream=None):
+    """img: uint8 CUDA tensor of W*H*channels pixels.  Returns (A', P) device tensors."""
+    lay = dct_layout(width, height, channels, level, flags, block_offset)
+    a, p = out if out is not None else (_empty(lay["a_bytes"], img.device), _empty(lay["p_bytes"], img.device))
+    g = _dgeom(width, height, channels, level, flags, block_offset)
+    _check(lib().dct_protect(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(img), _ptr(a), _ptr(p),
+                             _stream(stream)), "dct_protect")
+    return a, p
+
+
+def dct_recover(a, p, width: int, height: int, channels: int, level: int, key, iv, flags: int = 0,
+                block_offset: int = 0, out=None, stream=None):
+    """Returns the rebuilt image (uint8 device tensor)."""
+    lay = dct_layout(width, height, channels, level, flags, block_offset)
+    o = out if out is not None else _empty(lay["p_bytes"], p.device)
+    g = _dgeom(width, height, channels, level, flags, block_offset)
+    _check(lib().dct_recover(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(a), _ptr(p), _ptr(o),
+                             _stream(stream)), "dct_recover")
+    return o
+
+
+def dct_select(img, width: int, height: int, channels: int = 1, out=None, stream=None):
+    """The 6 selected fp32 coefficients per record: (records, 6) device tensor."""
+    import torch
+    lay = dct_layout(width, height, channels)
+    o = out if out is not None else torch.empty((lay["records"], 6), dtype=torch.float32, device=img.device)
+    g = _dgeom(width, height, channels, 1)
+    _check(lib().dct_select(C.byref(g), _ptr(img), _ptr(o), _stream(stream)), "dct_select")
     return o
 
 

@@ -172,6 +172,7 @@ void launch_pdl(void (*kernel)(P), unsigned grid, unsigned block, cudaStream_t s
     cudaLaunchKernelEx(&cfg, kernel, p);
 }
 template void launch_pdl<FusedParams>(void (*)(FusedParams), unsigned, unsigned, cudaStream_t, const FusedParams&);
+template void launch_pdl<DctParams>(void (*)(DctParams), unsigned, unsigned, cudaStream_t, const DctParams&);
 
 static unsigned grid_for(uint64_t n_blocks) {
     return (unsigned)((n_blocks + kBlocksPerCta - 1) / kBlocksPerCta);

@@ -80,6 +80,19 @@ static void ctr_base(const uint8_t iv[16], uint64_t j, uint32_t out[4]) {
     out[2] = (uint32_t)(nlo >> 32); out[3] = (uint32_t)nlo;
 }
 
+void cipher_setup(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block, CipherParams& cp) {
+    ctr_base(iv, ctr_block, cp.ctr);
+    key_expansion(key, cp.rk);
+}
+
+void sha512_kiv(const uint8_t key[16], const uint8_t iv[16], uint32_t kiv[8], uint64_t mid[8], uint64_t h0[8]) {
+    for (int i = 0; i < 4; ++i) { kiv[i] = be32(key + 4 * i); kiv[4 + i] = be32(iv + 4 * i); }
+    uint64_t w[4];
+    for (int i = 0; i < 4; ++i) w[i] = (uint64_t)kiv[2 * i] << 32 | kiv[2 * i + 1];
+    sha512_mid(w, mid);
+    memcpy(h0, kH512, sizeof kH512);
+}
+
 static void record_bits(uint32_t L, uint32_t mode, uint32_t bits[3]) {
     // BLOCK8 (C21, C22) / FULL (C23): A, B, C bits per block
     if (L == 1) { bits[0] = 160; bits[1] = 0; bits[2] = 480; return; }
@@ -117,6 +130,21 @@ static void fill_fused(FusedParams& p, const se_geom* g, const se_layout& lay, c
     for (int i = 0; i < 4; ++i) w[i] = (uint64_t)p.kiv[2 * i] << 32 | p.kiv[2 * i + 1];
     sha512_mid(w, p.mid512);
     memcpy(p.h512, kH512, sizeof kH512);
+}
+
+// Keep the stream-ordered pool's memory across calls (default release
+// threshold 0 would hand it back to the OS at every synchronisation).
+void keep_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
 }
 
 }  // namespace se
@@ -179,20 +207,6 @@ static DwtParams dwt_params(const se_geom* g, const se_layout& lay) {
     return p;
 }
 
-// Keep the stream-ordered pool's memory across calls (default release
-// threshold 0 would hand it back to the OS at every synchronisation).
-static void keep_pool() {
-    static thread_local int done_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (done_dev == dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done_dev = dev;
-}
 
 // Row a6, keystream half: AES-128-CTR keystream of the whole A stream
 // (counter base p.ctr) written to `out`; the fused kernel that follows is

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "../../include/se.h"
+#include "../../include/se_dct.h"
 
 namespace se {
 
@@ -77,6 +78,31 @@ struct DwtParams {
     uint32_t one;             // = 1, opaque to ptxas (see FusedParams::one)
 };
 
+// Chapter 4 DCT 8x8 SE (row f3, k_dct.cu).  One thread per 8x8 block
+// position (all channels), 128 positions per CTA.
+struct DctParams {
+    const uint8_t* in;        // protect: image; recover: Fragment 2 (P')
+    uint8_t* out;             // protect: Fragment 2; recover: rebuilt image
+    uint8_t* a;               // Fragment 1 stream (protect: holds the keystream on entry)
+    const uint8_t* ks;        // recover: keystream of Fragment 1 (scratch)
+    float* coef;              // dct_select: records x 6
+    uint64_t n_pos;           // block positions (W/8)*(H/8)
+    uint64_t a_bytes;
+    uint64_t block_offset;    // global record index of record 0 (KEYED nonce)
+    uint32_t width;           // pixels per row
+    uint32_t bpr;             // block positions per block row = width / 8
+    uint32_t one;             // = 1, opaque to ptxas (sha2_device.cuh)
+    uint32_t pad_;
+    uint32_t kiv[8];          // K || IV words (KEYED)
+    uint64_t mid512[8];       // SHA-512 state after rounds 0..3 over K||IV (KEYED)
+    uint64_t h512[8];         // SHA-512 H(0)
+};
+
+// host helpers shared by the API translation units (se_api.cu)
+void cipher_setup(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block, CipherParams& cp);
+void sha512_kiv(const uint8_t key[16], const uint8_t iv[16], uint32_t kiv[8], uint64_t mid[8], uint64_t h0[8]);
+void keep_pool();
+
 // launchers (return cudaError_t as int)
 int launch_protect_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
 int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
@@ -91,6 +117,8 @@ int launch_protect_full(const FusedParams& p, uint32_t levels, bool mask, void* 
 int launch_recover_full(const FusedParams& p, uint32_t levels, bool mask, void* stream);
 int launch_dwt_inv_block8(const DwtParams& p, uint32_t levels, void* stream);
 int launch_cipher_ctr(const CipherParams& p, void* stream);
+
+int launch_dct(const DctParams& p, uint32_t channels, uint32_t level, bool keyed, int op, void* stream);  // op 0 protect, 1 recover, 2 select
 
 int launch_stats(const void* x, const void* y, uint64_t n, uint32_t width, se_stats* out, uint32_t* joint,
                  void* stream);

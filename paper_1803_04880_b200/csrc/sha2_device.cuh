@@ -378,15 +378,16 @@ __device__ __forceinline__ void sha512_sched8_rounds(W64 (&S)[8], W64 (&W)[16], 
     }
 }
 
-// SHA-512 of one block resuming after round 3 (W[0..3] = K||IV consumed by
-// the host midstate `st`).  Digest -> H.
-__device__ __forceinline__ void sha512_from_round4(const uint64_t (&st)[8], const uint64_t (&h0)[8],
-                                                   W64 (&W)[16], uint64_t (&H)[8], uint32_t one) {
-    // variable i at round 4 lives in S[(i - 4) & 7]
+// SHA-512 of one block resuming at round R0 from state `st` (R0 = 0: st =
+// H(0); R0 = 4: W[0..3] = K||IV consumed by the host midstate).  Digest -> H.
+template <int R0>
+__device__ __forceinline__ void sha512_from_round(const uint64_t (&st)[8], const uint64_t (&h0)[8],
+                                                  W64 (&W)[16], uint64_t (&H)[8], uint32_t one) {
+    // variable i at round R0 lives in S[(i - R0) & 7]
     W64 S[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) S[(i - 4) & 7] = w64(st[i]);
-    sha512_msg_rounds<4>(S, W, one);
+    for (int i = 0; i < 8; ++i) S[(i - R0) & 7] = w64(st[i]);
+    sha512_msg_rounds<R0>(S, W, one);
 #if SE_SHA_BODY == 8
 #pragma unroll 1
     for (int r = 16; r < 80; r += 8) {
@@ -402,6 +403,11 @@ __device__ __forceinline__ void sha512_from_round4(const uint64_t (&st)[8], cons
     // after round 79 (80 rounds) variable i lives in S[(i - 80) & 7] = S[i]
 #pragma unroll
     for (int i = 0; i < 8; ++i) H[i] = u64(fadd64(w64(h0[i]), S[i], one));
+}
+
+__device__ __forceinline__ void sha512_from_round4(const uint64_t (&st)[8], const uint64_t (&h0)[8],
+                                                   W64 (&W)[16], uint64_t (&H)[8], uint32_t one) {
+    sha512_from_round<4>(st, h0, W, H, one);
 }
 
 }  // namespace se

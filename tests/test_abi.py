@@ -22,7 +22,8 @@ def lib():
 
 
 def declared_functions():
-    src = open(os.path.join(ROOT, "include", "se.h")).read()
+    inc = os.path.join(ROOT, "include")
+    src = "".join(open(os.path.join(inc, h)).read() for h in sorted(os.listdir(inc)) if h.endswith(".h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\**\s+\**([A-Za-z_][A-Za-z0-9_]*)\s*\(",
                        src, flags=re.M)
@@ -33,7 +34,7 @@ def test_header_declares_the_boundary():
     names = declared_functions()
     for n in ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_protect_batch",
               "fragment_recover_batch", "dwt_fwd", "dwt_inv", "cipher_encrypt", "cipher_decrypt",
-              "se_strerror"]:
+              "se_strerror", "dct_layout", "dct_protect", "dct_recover", "dct_select"]:
         assert n in names, n
 
 
@@ -102,3 +103,20 @@ def test_validation_before_any_device_work(lib):
     assert lib.cipher_encrypt(key, key, 0, None, None, 0, None) == se.SE_OK
     assert lib.cipher_encrypt(None, key, 0, None, None, 16, None) == se.SE_EINVAL
     assert se.lib().se_strerror(se.SE_EALIGN).decode().startswith("device pointer")
+
+
+@pytest.mark.parametrize("W,H,C", [(4800, 4800, 1), (1600, 1200, 1), (64, 48, 3), (16, 8, 4)])
+def test_dct_layout_host(lib, orc, W, H, C):
+    lay = se.dct_layout(W, H, C, 2)
+    o = orc.dct_layout(W, H, C)
+    assert (lay["records"], lay["a_bits"], lay["a_bytes"], lay["p_bytes"]) == \
+        (o["records"], o["bits"], o["a_bytes"], o["p_bytes"])
+
+
+@pytest.mark.parametrize("W,H,C,level,flags,off", [(0, 8, 1, 1, 0, 0), (12, 8, 1, 1, 0, 0), (8, 12, 1, 1, 0, 0),
+                                                   (8, 8, 2, 1, 0, 0), (8, 8, 1, 3, 0, 0), (8, 8, 1, 2, 2, 0),
+                                                   (8, 8, 1, 1, 0, 3)])
+def test_dct_layout_rejects_bad_geometry(lib, W, H, C, level, flags, off):
+    with pytest.raises(se.SEError) as e:
+        se.dct_layout(W, H, C, level, flags, off)
+    assert e.value.status == se.SE_EINVAL
