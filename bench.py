@@ -514,6 +514,165 @@ def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=8 << 
                     f"{chunk_bytes >> 20} MiB chunks on {n_streams} streams), host wall clock"}
 
 
+# ---------------------------------------------------------------- NEXT row f3: Chapter 4 DCT SE
+
+# Table 4.1 / 4.9 image sizes (grey scale)
+DCT_SIZES = [(1024, 768), (1600, 1200), (3240, 2592), (4800, 4800)]
+# ALU-pipe ops per 8x8 block at level 2 (DESIGN.md §5 f3): SHA-512 of one
+# message block from round 0 (16 message rounds x 20 + 64 schedule rounds x
+# 36), pixel byte PRMTs (64 in, 48 pack), mask XOR 16, record pack ~30,
+# AES-CTR share 260 * 66/128.  The fp32 DCT work issues on the FMA pipe.
+DCT_ALU_OPS = {"sha512": 16 * 20 + 64 * 36, "bytes": 64 + 48, "xor": 16, "record": 30, "aes": 260 * 66 / 128}
+
+
+def run_dct(args):
+    import torch
+
+    import paper_1803_04880_b200 as se
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    se.lib()
+    level, flags = args.dct, (se.DCT_KEYED if args.dct_keyed else 0)
+    key, iv = synth.KEY, synth.iv_for(6)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+    per_size = []
+    clocks = ClockSampler(0)
+    clocks.start()
+    for (W, H) in DCT_SIZES:
+        x_np = synth.bitmap(H, W, 1, W + H).reshape(-1)
+        n = x_np.size
+        lay = se.dct_layout(W, H, 1, level, flags)
+        x = torch.from_numpy(x_np).to(dev)
+        a = torch.empty(lay["a_bytes"], dtype=torch.uint8, device=dev)
+        p = torch.empty(n, dtype=torch.uint8, device=dev)
+        out = torch.empty(n, dtype=torch.uint8, device=dev)
+        with torch.cuda.stream(stream):
+            se.dct_protect(x, W, H, 1, level, key, iv, flags=flags, out=(a, p), stream=stream)
+            se.dct_recover(a, p, W, H, 1, level, key, iv, flags=flags, out=out, stream=stream)
+        stream.synchronize()
+        d = (out.to(torch.int16) - x.to(torch.int16)).abs()
+        mse = float((d.float() ** 2).mean())
+        assert int(d.max()) <= 1, "DCT round trip off by more than 1"
+        t_end = time.time() + args.soak / len(DCT_SIZES)
+        i = 0
+        while i < args.warmup or time.time() < t_end:
+            se.dct_protect(x, W, H, 1, level, key, iv, flags=flags, out=(a, p), stream=stream)
+            se.dct_recover(a, p, W, H, 1, level, key, iv, flags=flags, out=out, stream=stream)
+            i += 1
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        se.launch_count(reset=True)
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                flush.fill_(k)                                  # evict L2 (images are < L2)
+                ev[k][0].record(stream)
+                se.dct_protect(x, W, H, 1, level, key, iv, flags=flags, out=(a, p), stream=stream)
+                ev[k][1].record(stream)
+                se.dct_recover(a, p, W, H, 1, level, key, iv, flags=flags, out=out, stream=stream)
+                ev[k][2].record(stream)
+        stream.synchronize()
+        launches = se.launch_count()
+        tp = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+        tr = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+        # AES-128-CTR of the whole image on the same GPU: the paper's comparator (Table 4.9)
+        y = torch.empty_like(x)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                se.cipher_encrypt(key, iv, x, out=y, stream=stream)
+            e0.record(stream)
+            for k in range(args.steps):
+                se.cipher_encrypt(key, iv, x, out=y, stream=stream)
+            e1.record(stream)
+        stream.synchronize()
+        t_aes = e0.elapsed_time(e1) / args.steps
+        per_size.append({"image": f"{W}x{H}", "n_bytes": n, "a_bytes": lay["a_bytes"],
+                         "protect_ms": round(tp, 5), "recover_ms": round(tr, 5),
+                         "protect_gbs": round(n / tp / 1e6, 2), "recover_gbs": round(n / tr / 1e6, 2),
+                         "aes128_ctr_ms": round(t_aes, 5),
+                         "psnr_db": round(10 * np.log10(255.0 ** 2 / mse), 3) if mse else None,
+                         "launches_per_step": launches / args.steps})
+        big = (x, a, p, out, W, H, n, lay, tp, tr, launches, x_np)
+    clocks.stop()
+    x, a, p, out, W, H, n, lay, tp, tr, launches, x_np = big
+    peaks, peak_src = load_peaks()
+    ms_step = tp + tr
+    dom_name, dom_ms = ("k_dct_protect", tp) if tp >= tr else ("k_dct_recover", tr)
+    kkey = f"{dom_name}<1, {level}, {1 if flags else 0}>"
+    traffic, traffic_src = load_traffic(kkey)
+    alg_bytes = 2 * n + lay["a_bytes"]
+    if level == 2:
+        ops_blk = sum(DCT_ALU_OPS.values())
+        ach = ops_blk * lay["records"] / (dom_ms / 1e3) / 1e9
+        peak_alu = NUM_SMS * ALU_LANES_PER_SM_CLK * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+        roofline = {"bound": "alu", "kernel": kkey, "achieved": round(ach, 1), "peak": round(peak_alu, 1),
+                    "unit": "Gop/s", "frac": round(ach / peak_alu, 4), "traffic": traffic,
+                    "traffic_source": traffic_src, "algorithmic_bytes": alg_bytes, "alu_ops_per_block": ops_blk,
+                    "peak_source": f"guide: {NUM_SMS} SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x "
+                                   f"{peaks.get('sm_max_mhz', 1965.0)} MHz ({peak_src} max clock)"}
+    else:
+        ach = alg_bytes / (dom_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": kkey, "achieved": round(ach, 1), "peak": peaks.get("hbm_gbs"),
+                    "unit": "GB/s", "frac": round(ach / peaks.get("hbm_gbs", 6551.7), 4), "traffic": traffic,
+                    "traffic_source": traffic_src, "algorithmic_bytes": alg_bytes,
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+    # e2e: pinned host image -> device -> protect -> fragments to host -> back -> recover -> image to host
+    hx = torch.from_numpy(x_np).pin_memory()
+    ha = torch.empty(lay["a_bytes"], dtype=torch.uint8).pin_memory()
+    hp, ho = torch.empty(n, dtype=torch.uint8).pin_memory(), torch.empty(n, dtype=torch.uint8).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(3, args.steps // 4)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(reps):
+            x.copy_(hx, non_blocking=True)
+            se.dct_protect(x, W, H, 1, level, key, iv, flags=flags, out=(a, p), stream=stream)
+            ha.copy_(a, non_blocking=True)
+            hp.copy_(p, non_blocking=True)
+            a.copy_(ha, non_blocking=True)
+            p.copy_(hp, non_blocking=True)
+            se.dct_recover(a, p, W, H, 1, level, key, iv, flags=flags, out=out, stream=stream)
+            ho.copy_(out, non_blocking=True)
+        e1.record(stream)
+    stream.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / reps
+    line = {
+        "metric": "DCT 8x8 SE (Ch. 4) protect+recover GB/s per GPU",
+        "value": round(n / (ms_step / 1e3) / 1e9, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"Table 4.1 image {W}x{H} grey, level {level}" + (" keyed" if flags else ""),
+                   "row": "f3", "l2": "flushed between steps"},
+        "roofline": roofline,
+        "per_image": per_size,
+        "paper_context": "Table 4.9 (GTX 780): SE level 2 5.41 ms, AES-128 5.46 ms for 4800x4800",
+        "e2e": {"value": round(n / (e2e_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+                "h2d_bytes_per_step": n + lay["a_bytes"] + n, "d2h_bytes_per_step": lay["a_bytes"] + n + n,
+                "path": "pinned host image, H2D, dct_protect, D2H fragments, H2D fragments, dct_recover, D2H"},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if not args.no_cpu_baseline:
+        import oracle
+        rows = 64
+        xs = x_np[: rows * W]
+        t0 = time.perf_counter()
+        reps_c = 0
+        while True:
+            a_o, p_o = oracle.dct_protect(xs, W, rows, 1, level, key, iv, flags=flags)
+            oracle.dct_recover(a_o, p_o, W, rows, 1, level, key, iv, flags=flags)
+            reps_c += 1
+            if time.perf_counter() - t0 > args.cpu_seconds / 3:
+                break
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": round(xs.size * reps_c / dt / 1e9, 6), "unit": "GB/s", "cores": 1,
+                                "kind": "oracle",
+                                "sample": f"{reps_c} pass(es) over the first {rows} rows ({xs.size} bytes) of the "
+                                          f"{W}x{H} image (protect+recover), 1 host thread, {dt:.1f} s",
+                                "host_cpu": cpu_model()}
+    return line
+
+
 # ---------------------------------------------------------------- CPU oracle baseline
 
 def oracle_time(x_np, W, L, key, iv, flags, n_blocks_sample, threads, reps=1):
@@ -620,11 +779,16 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparator", action="store_true")
+    ap.add_argument("--dct", type=int, default=0, choices=[0, 1, 2],
+                    help="NEXT row f3: bench the Chapter 4 DCT SE at this protection level instead")
+    ap.add_argument("--dct-keyed", action="store_true", help="level 2 with the keyed hash framing (D9)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         line = run_reference(args)
+    elif args.dct:
+        line = run_dct(args)
     elif args.config == 5 or (args.config == 4 and args.stripes):
         line = run_multi(args)
     else:

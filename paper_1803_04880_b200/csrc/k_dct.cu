@@ -33,13 +33,15 @@ namespace {
 constexpr float kA0 = (float)SE_DCT_A0;   // alpha(0) = sqrt(1/8), Eq. 4.3
 
 // D[u][x] = alpha(u) cos(pi (2x+1) u / 16) for u = 1, 2 and x = 0..7
+// (D[1][7-x] = -D[1][x], D[2][7-x] = D[2][x]); x is a compile-time constant
+// at every use, so these fold to immediates.
 __device__ __forceinline__ constexpr float d1(int x) {
-    return x == 0 ? (float)SE_DCT_H1 : x == 1 ? (float)SE_DCT_H3 : x == 2 ? (float)SE_DCT_H5
-         : x == 3 ? (float)SE_DCT_H7 : -d1(7 - x);
+    constexpr float h1 = (float)SE_DCT_H1, h3 = (float)SE_DCT_H3, h5 = (float)SE_DCT_H5, h7 = (float)SE_DCT_H7;
+    return x == 0 ? h1 : x == 1 ? h3 : x == 2 ? h5 : x == 3 ? h7 : x == 4 ? -h7 : x == 5 ? -h5 : x == 6 ? -h3 : -h1;
 }
 __device__ __forceinline__ constexpr float d2(int x) {
-    return x == 0 ? (float)SE_DCT_H2 : x == 1 ? (float)SE_DCT_H6 : x == 2 ? -(float)SE_DCT_H6
-         : x == 3 ? -(float)SE_DCT_H2 : d2(7 - x);
+    constexpr float h2 = (float)SE_DCT_H2, h6 = (float)SE_DCT_H6;
+    return (x == 0 || x == 7) ? h2 : (x == 1 || x == 6) ? h6 : (x == 2 || x == 5) ? -h6 : -h2;
 }
 
 // byte `k` of word w, minus 128, as an exact float: PRMT the byte under the
