@@ -20,11 +20,12 @@ _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libse.so")
 CSRC = os.path.join(_HERE, "csrc")
 SOURCES = ["se_api.cu", "k_block8.cu", "k_full.cu", "k_cipher.cu", "k_stats.cu", "se_host.cu",
-           "k_dct.cu", "se_dct_api.cu"]
+           "k_dct.cu", "se_dct_api.cu", "se_container.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
 
 SE_OK, SE_EINVAL, SE_EALIGN, SE_ECUDA, SE_ENOTSUP = 0, -1, -2, -3, -4
+SE_EFORMAT, SE_EINTEGRITY = -5, -6
 MODE_BLOCK8, MODE_FULL = 0, 1
 FLAG_PUBLIC_PLAIN = 1
 
@@ -39,7 +40,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     another in-tree path, selectable at load time with SE_LIB_PATH."""
     target = out or LIB_PATH
     deps = sources() + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    deps += [os.path.join(_ROOT, "include", h) for h in ("se.h", "se_dct.h")]
+    deps += [os.path.join(_ROOT, "include", h) for h in ("se.h", "se_dct.h", "se_container.h")]
     if not force and os.path.exists(target):
         if os.path.getmtime(target) >= max(os.path.getmtime(p) for p in deps):
             return target
@@ -93,7 +94,15 @@ SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_
            "fragment_protect_batch", "fragment_recover_batch", "fragment_protect_host",
            "fragment_recover_host", "dwt_fwd", "dwt_inv", "cipher_encrypt", "cipher_decrypt",
            "se_stats_accumulate", "se_strerror", "se_launch_count",
-           "dct_layout", "dct_protect", "dct_recover", "dct_select"]
+           "dct_layout", "dct_protect", "dct_recover", "dct_select",
+           "se_container_streams", "se_container_size", "se_container_pack", "se_container_open",
+           "se_disperse_plan", "se_storage_footprint", "se_sha256"]
+
+
+class ContainerInfo(C.Structure):
+    _fields_ = [("scheme", C.c_uint32), ("flags", C.c_uint32), ("levels", C.c_uint32), ("width", C.c_uint32),
+                ("height", C.c_uint32), ("channels", C.c_uint32), ("n_bytes", C.c_uint64),
+                ("block_offset", C.c_uint64), ("iv", C.c_uint8 * 16)]
 
 
 class DctGeom(C.Structure):
@@ -138,6 +147,17 @@ def lib():
         L.dct_protect.argtypes = [dg, u8p, u8p, vp, vp, vp, vp]
         L.dct_recover.argtypes = [dg, u8p, u8p, vp, vp, vp, vp]
         L.dct_select.argtypes = [dg, vp, vp, vp]
+        cip = C.POINTER(ContainerInfo)
+        L.se_container_streams.argtypes = [cip, C.POINTER(C.c_uint64)]
+        L.se_container_size.argtypes = [cip, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.se_container_pack.argtypes = [cip, C.c_uint32, C.POINTER(C.c_void_p), vp, C.c_uint64,
+                                        C.POINTER(C.c_uint64)]
+        L.se_container_open.argtypes = [vp, C.c_uint64, C.c_int, cip, C.POINTER(C.c_uint32),
+                                        C.POINTER(C.c_void_p), C.POINTER(C.c_uint32)]
+        L.se_disperse_plan.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        L.se_storage_footprint.argtypes = [cip, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.se_sha256.argtypes = [vp, C.c_uint64, vp]
+        L.se_sha256.restype = None
         L.se_strerror.argtypes = [C.c_int]
         L.se_strerror.restype = C.c_char_p
         L.se_launch_count.argtypes = [C.c_int]
@@ -297,6 +317,111 @@ def dct_select(img, width: int, height: int, channels: int = 1, out=None, stream
     g = _dgeom(width, height, channels, 1)
     _check(lib().dct_select(C.byref(g), _ptr(img), _ptr(o), _stream(stream)), "dct_select")
     return o
+
+
+# ---------------------------------------------------------------- containers / dispersion (row f4, se_container.h)
+
+SCHEME_DWT_BLOCK8, SCHEME_DWT_FULL, SCHEME_DCT = 1, 2, 3
+STREAM_A, STREAM_B, STREAM_C, STREAM_P = 0, 1, 2, 3
+LAYOUT_A_LOCAL, LAYOUT_AB_LOCAL = 0, 1
+
+
+def container_info(scheme: int, n_bytes: int, width: int, levels: int, iv, flags: int = 0, block_offset: int = 0,
+                   height: int = 0, channels: int = 1) -> ContainerInfo:
+    info = ContainerInfo(int(scheme), int(flags), int(levels), int(width), int(height), int(channels),
+                         int(n_bytes), int(block_offset))
+    info.iv[:] = list(_bytes16(iv, "iv"))
+    return info
+
+
+def _host_bytes(x):
+    import numpy as np
+    if hasattr(x, "cpu"):
+        x = x.cpu().numpy()
+    return np.ascontiguousarray(np.frombuffer(bytes(x), np.uint8) if isinstance(x, (bytes, bytearray)) else x,
+                                dtype=np.uint8)
+
+
+def container_streams(info: ContainerInfo) -> list:
+    lens = (C.c_uint64 * 4)()
+    _check(lib().se_container_streams(C.byref(info), lens), "se_container_streams")
+    return [int(v) for v in lens]
+
+
+def container_pack(info: ContainerInfo, streams: dict):
+    """streams: {stream id: host bytes / numpy / tensor}.  Returns the container (numpy uint8)."""
+    import numpy as np
+    mask = 0
+    keep = {}
+    ptrs = (C.c_void_p * 4)()
+    for sid, data in streams.items():
+        mask |= 1 << sid
+        keep[sid] = _host_bytes(data)
+        ptrs[sid] = keep[sid].ctypes.data if keep[sid].size else None
+    size = C.c_uint64()
+    _check(lib().se_container_size(C.byref(info), mask, C.byref(size)), "se_container_size")
+    lens = container_streams(info)
+    for sid, a in keep.items():
+        if a.size != lens[sid]:
+            raise ValueError(f"stream {sid}: {a.size} bytes, layout says {lens[sid]}")
+    out = np.zeros(size.value, np.uint8)
+    written = C.c_uint64()
+    _check(lib().se_container_pack(C.byref(info), mask, ptrs, out.ctypes.data, out.size, C.byref(written)),
+           "se_container_pack")
+    return out
+
+
+def container_open(buf, verify: bool = True):
+    """Returns (info, {stream id: numpy view into buf}).  Raises SEError
+    (status SE_EFORMAT / SE_EINTEGRITY; .bad_mask = failing stream ids)."""
+    import numpy as np
+    b = _host_bytes(buf)
+    info = ContainerInfo()
+    mask = C.c_uint32()
+    bad = C.c_uint32()
+    ptrs = (C.c_void_p * 4)()
+    rc = lib().se_container_open(b.ctypes.data if b.size else None, b.size, 1 if verify else 0, C.byref(info),
+                                 C.byref(mask), ptrs, C.byref(bad))
+    if rc != SE_OK:
+        err = SEError(rc, "se_container_open")
+        err.bad_mask = int(bad.value)
+        raise err
+    lens = container_streams(info)
+    base = b.ctypes.data
+    streams = {sid: b[ptrs[sid] - base: ptrs[sid] - base + lens[sid]] if lens[sid] else np.zeros(0, np.uint8)
+               for sid in range(4) if (mask.value >> sid) & 1}
+    return info, streams
+
+
+def disperse_plan(layout: int, scheme: int):
+    """(local stream mask, [remote mask 0, remote mask 1]) of a placement layout."""
+    lm = C.c_uint32()
+    rm = (C.c_uint32 * 2)()
+    _check(lib().se_disperse_plan(int(layout), int(scheme), C.byref(lm), rm), "se_disperse_plan")
+    return int(lm.value), [int(rm[0]), int(rm[1])]
+
+
+def disperse(info: ContainerInfo, streams: dict, layout: int) -> dict:
+    """Pack the fragments into the layout's containers: {"local": c, "remote": [c, ...]}."""
+    lm, rms = disperse_plan(layout, info.scheme)
+
+    def pick(mask):
+        return {sid: streams[sid] for sid in range(4) if (mask >> sid) & 1}
+    return {"local": container_pack(info, pick(lm)), "remote": [container_pack(info, pick(m)) for m in rms if m]}
+
+
+def storage_footprint(info: ContainerInfo, layout: int):
+    """(local bytes / n, total bytes / n) for a layout, headers included."""
+    lo, to = C.c_double(), C.c_double()
+    _check(lib().se_storage_footprint(C.byref(info), int(layout), C.byref(lo), C.byref(to)), "se_storage_footprint")
+    return lo.value, to.value
+
+
+def sha256(data) -> bytes:
+    b = _host_bytes(data)
+    out = (C.c_uint8 * 32)()
+    lib().se_sha256(b.ctypes.data if b.size else None, b.size, out)
+    return bytes(out)
 
 
 def launch_count(reset: bool = False) -> int:

@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include "se_internal.h"
+#include "../../include/se_container.h"
 #include "tables.h"
 
 namespace se {
@@ -160,6 +161,8 @@ const char* se_strerror(int s) {
         case SE_EALIGN: return "device pointer not 16-byte aligned";
         case SE_ECUDA: return "CUDA error";
         case SE_ENOTSUP: return "not supported";
+        case SE_EFORMAT: return "bad container format";
+        case SE_EINTEGRITY: return "container stream digest mismatch";
         default: return "unknown status";
     }
 }
