@@ -1,8 +1,9 @@
 // k_cipher.cu — AES-128-CTR over an arbitrary byte range (cipher_encrypt /
 // cipher_decrypt, row a6 as a standalone op and the paper's full-encryption
-// comparator).  T-tables in shared memory; one 16-byte
+// comparator).  Lane-replicated T-table in 64 KB of
+// dynamic shared memory (conflict-free lookups, se_device.cuh); one 16-byte
 // counter block per thread per iteration, 128-bit coalesced loads/stores,
-// grid sized to whole waves of the 148 SMs.
+// grid sized to whole waves of the 148 SMs (3 CTAs of 256 threads per SM).
 #include <cuda_runtime.h>
 
 #include "se_device.cuh"
@@ -13,19 +14,26 @@ constexpr int kCipherThreads = 256;
 
 // p.in == nullptr: write the keystream itself (used by the fused kernels,
 // which then XOR it into the private fragment, see fused_cta.cuh).
+// LANE: the 64 KB lane-replicated table (standalone cipher), else the 5 KB
+// tables (keystream next to a running fused kernel).
+template <bool LANE>
 __global__ void __launch_bounds__(kCipherThreads) k_cipher_ctr(const __grid_constant__ CipherParams p) {
     // a dependent kernel launched with programmatic stream serialization may
     // start now; it waits (griddepcontrol.wait) before reading our output
     asm volatile("griddepcontrol.launch_dependents;");
-    __shared__ AesSmem aes;
-    aes_load_tables(aes, threadIdx.x, kCipherThreads);
+    extern __shared__ __align__(16) uint32_t lut[];
+    __shared__ AesSmem small;
+    if constexpr (LANE) aes_load_lut(lut, threadIdx.x, kCipherThreads);
+    else aes_load_tables(small, threadIdx.x, kCipherThreads);
     __syncthreads();
+    const AesLane lane = aes_lane(lut);
     const uint64_t nblk = (p.n + 15) / 16;
     const uint64_t stride = (uint64_t)gridDim.x * kCipherThreads;
     for (uint64_t j = (uint64_t)blockIdx.x * kCipherThreads + threadIdx.x; j < nblk; j += stride) {
         uint32_t x[4];
         ctr_add(p.ctr, j, x);
-        aes128_block(aes, p.rk, x);
+        if constexpr (LANE) aes128_block(lane, p.rk, x);
+        else aes128_block(small, p.rk, x);
         const uint64_t off = j * 16;
         if (off + 16 <= p.n) {
             const uint4 q = p.in ? __ldg(reinterpret_cast<const uint4*>(p.in + off)) : make_uint4(0, 0, 0, 0);
@@ -84,13 +92,30 @@ __global__ void __launch_bounds__(kCipherThreads) k_batch_keystream(const __grid
     }
 }
 
+// 64 KB of dynamic shared memory needs an opt-in, once per kernel and device
+template <auto Kernel>
+static void allow_lut() {
+    static thread_local int done = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (done == dev) return;
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAesLutBytes);
+    done = dev;
+}
+
+// Standalone cipher: 3 CTAs x 64 KB lane tables per SM.  Keystream for a
+// fused kernel that runs concurrently (programmatic launch): 5 KB tables.
+constexpr int kCipherCtasPerSm = 3;
+constexpr int kKeystreamCtasPerSm = 8;
+
 int launch_batch_keystream(const BatchParams& bp, uint32_t a_bits, void* stream) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t total = bp.total_ctas * (uint64_t)a_bits;
     const uint64_t want = (total + kCipherThreads - 1) / kCipherThreads;
-    const unsigned grid = (unsigned)(want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8);
+    const uint64_t cap = (uint64_t)sms * kKeystreamCtasPerSm;
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
     cudaStream_t s = (cudaStream_t)stream;
     if (grid == 0) return 0;
     if (a_bits == 40) k_batch_keystream<40><<<grid, kCipherThreads, 0, s>>>(bp);
@@ -106,9 +131,15 @@ int launch_cipher_ctr(const CipherParams& p, void* stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t nblk = (p.n + 15) / 16;
     const uint64_t want = (nblk + kCipherThreads - 1) / kCipherThreads;
-    const uint64_t cap = (uint64_t)sms * 8;          // 8 resident CTAs per SM
+    const uint64_t cap = (uint64_t)sms * (p.in ? kCipherCtasPerSm : kKeystreamCtasPerSm);
     const unsigned grid = (unsigned)(want < cap ? want : cap);
-    k_cipher_ctr<<<grid, kCipherThreads, 0, (cudaStream_t)stream>>>(p);
+    if (grid == 0) return 0;
+    if (p.in) {
+        allow_lut<k_cipher_ctr<true>>();
+        k_cipher_ctr<true><<<grid, kCipherThreads, kAesLutBytes, (cudaStream_t)stream>>>(p);
+    } else {
+        k_cipher_ctr<false><<<grid, kCipherThreads, 0, (cudaStream_t)stream>>>(p);
+    }
     note_launch();
     return (int)cudaGetLastError();
 }

@@ -195,7 +195,7 @@ int se_container_open(const uint8_t* buf, uint64_t len, int verify, se_container
     *stream_mask = mask;
     for (int id = 0; id < 4; ++id) streams[id] = ptr[id];
     if (bad_mask) *bad_mask = bad;
-    return bad ? SE_EINTEGRITY : SE_OK;
+    return bad ? (int)SE_EINTEGRITY : (int)SE_OK;
 }
 
 int se_disperse_plan(uint32_t layout, uint32_t scheme, uint32_t* local_mask, uint32_t remote_masks[2]) {

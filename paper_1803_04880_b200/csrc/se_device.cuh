@@ -242,9 +242,81 @@ __device__ __forceinline__ void for_each_field(F&& f) {
 
 // ------------------------------------------------------------------ AES
 static __device__ const uint32_t g_aes_te0[256] = SE_AES_TE0_INIT;
+
+// Lane-replicated T-table in shared memory (64 KB, dynamic): row x is 256
+// bytes — words 0..31 hold Te0[x] once per lane, words 32..63 Te2[x] =
+// ror16(Te0[x]).  Lane l reads word l (or 32 + l) of whatever row its byte
+// selects, so the 32 lanes of a warp always hit 32 distinct banks: one
+// shared-memory wavefront per lookup instead of ~3.5 for random indices into
+// a single table.  The row address (byte << 8 | lane column) is one PRMT.
+// Te1 = ror8(Te0) and Te3 = ror8(Te2), and rotation distributes over XOR, so
+// each output column needs a single rotation.  The S-box of the last round
+// is byte 2 of Te0[x] = (2s, s, s, 3s).
+constexpr int kAesLutBytes = 256 * 256;
+
+__device__ __forceinline__ void aes_load_lut(uint32_t* lut, int tid, int nthreads) {
+    uint4* l4 = reinterpret_cast<uint4*>(lut);
+    for (int i = tid; i < 256 * 16; i += nthreads) {              // 16 x 16 B per row
+        const uint32_t t = g_aes_te0[i >> 4];
+        const uint32_t v = (i & 15) < 8 ? t : __funnelshift_r(t, t, 16);
+        l4[i] = make_uint4(v, v, v, v);
+    }
+}
+
+struct AesLane {
+    const uint8_t* lut;   // shared-memory base of the table
+    uint32_t c0, c2;      // this lane's byte column in the Te0 / Te2 halves
+};
+
+__device__ __forceinline__ AesLane aes_lane(const uint32_t* lut) {
+    const uint32_t lane = threadIdx.x & 31;
+    return AesLane{reinterpret_cast<const uint8_t*>(lut), lane * 4, 128 + lane * 4};
+}
+
+// table word for byte K of s (K = 3: most significant), column c
+template <int K>
+__device__ __forceinline__ uint32_t aes_lu(const AesLane& a, uint32_t s, uint32_t c) {
+    const uint32_t addr = __byte_perm(s, c, 0x5504 | (K << 4));     // (byte K << 8) | c
+    return *reinterpret_cast<const uint32_t*>(a.lut + addr);
+}
+
+// one output column of a middle round:
+// Te0[sa.b3] ^ Te1[sb.b2] ^ Te2[sc.b1] ^ Te3[sd.b0] ^ k = Te0 ^ Te2 ^ ror8(Te0 ^ Te2) ^ k
+__device__ __forceinline__ uint32_t aes_col(const AesLane& a, uint32_t sa, uint32_t sb, uint32_t sc, uint32_t sd,
+                                            uint32_t k) {
+    const uint32_t v = aes_lu<2>(a, sb, a.c0) ^ aes_lu<0>(a, sd, a.c2);
+    return aes_lu<3>(a, sa, a.c0) ^ aes_lu<1>(a, sc, a.c2) ^ k ^ __funnelshift_r(v, v, 8);
+}
+
+// One AES-128 block (FIPS-197 §5.1), big-endian column words in/out; rk = 44
+// round-key words.
+__device__ __forceinline__ void aes128_block(const AesLane& a, const uint32_t* __restrict__ rk, uint32_t (&x)[4]) {
+    uint32_t s0 = x[0] ^ rk[0], s1 = x[1] ^ rk[1], s2 = x[2] ^ rk[2], s3 = x[3] ^ rk[3];
+#pragma unroll
+    for (int r = 1; r < 10; ++r) {
+        const uint32_t t0 = aes_col(a, s0, s1, s2, s3, rk[4 * r + 0]);
+        const uint32_t t1 = aes_col(a, s1, s2, s3, s0, rk[4 * r + 1]);
+        const uint32_t t2 = aes_col(a, s2, s3, s0, s1, rk[4 * r + 2]);
+        const uint32_t t3 = aes_col(a, s3, s0, s1, s2, rk[4 * r + 3]);
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    // last round: SubBytes + ShiftRows + AddRoundKey; S[x] = byte 2 of Te0[x]
+    const uint32_t s[4] = {s0, s1, s2, s3};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t hi = __byte_perm(aes_lu<3>(a, s[j], a.c0), aes_lu<2>(a, s[(j + 1) & 3], a.c0), 0x2600);
+        const uint32_t lo = __byte_perm(aes_lu<1>(a, s[(j + 2) & 3], a.c0), aes_lu<0>(a, s[(j + 3) & 3], a.c0), 0x0026);
+        x[j] = __byte_perm(lo, hi, 0x7610) ^ rk[40 + j];
+    }
+}
+
+// Small T-tables (5 KB): te[0..3][256] (Te1..3 = byte rotations of Te0) + the
+// S-box.  Random indices conflict in the shared-memory banks (~3.5 wavefronts
+// per lookup), but the footprint is small: used for the keystream kernels
+// that run concurrently with a fused kernel (programmatic launch), where the
+// 64 KB lane table below measured 2.6 % slower on C2 protect.
 static __device__ const uint8_t g_aes_sbox[256] = SE_AES_SBOX_INIT;
 
-// Shared-memory T-tables: te[0..3][256] (Te1..3 = byte rotations of Te0) + S-box.
 struct AesSmem {
     uint32_t te[4][256];
     uint32_t sb[256];
@@ -261,9 +333,7 @@ __device__ __forceinline__ void aes_load_tables(AesSmem& s, int tid, int nthread
     }
 }
 
-// One AES-128 block, big-endian column words in/out; rk = 44 round-key words.
-__device__ __forceinline__ void aes128_block(const AesSmem& s, const uint32_t* __restrict__ rk,
-                                             uint32_t (&x)[4]) {
+__device__ __forceinline__ void aes128_block(const AesSmem& s, const uint32_t* __restrict__ rk, uint32_t (&x)[4]) {
     uint32_t s0 = x[0] ^ rk[0], s1 = x[1] ^ rk[1], s2 = x[2] ^ rk[2], s3 = x[3] ^ rk[3];
 #pragma unroll
     for (int r = 1; r < 10; ++r) {
