@@ -246,7 +246,8 @@ def run_se(args):
         ms_step = total_ms / args.steps
 
     # ---- e2e: same metric with host buffers, H2D/D2H inside the timed region
-    e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, args.e2e_steps) if args.e2e_steps > 0 else \
+    e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, args.e2e_steps, chunk_bytes=args.e2e_chunk_kib << 10,
+                  n_streams=args.e2e_streams) if args.e2e_steps > 0 else \
         {"value": None, "unit": "GB/s", "note": "skipped (--e2e-steps 0, profiling runs only)"}
 
     # ---- comparator: full-file AES-128-CTR on the same GPU (paper methodology)
@@ -511,7 +512,7 @@ def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=8 << 
     return {"value": round(n / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n + frag_bytes,
             "d2h_bytes_per_step": frag_bytes + n, "ms_per_step": round(ms, 4),
             "path": f"fragment_protect_host + fragment_recover_host (C ABI, pinned host buffers, "
-                    f"{chunk_bytes >> 20} MiB chunks on {n_streams} streams), host wall clock"}
+                    f"{chunk_bytes >> 10} KiB chunks on {n_streams} streams), host wall clock"}
 
 
 # ---------------------------------------------------------------- NEXT row f3: Chapter 4 DCT SE
@@ -776,6 +777,8 @@ def main():
     ap.add_argument("--plain", action="store_true", help="PUBLIC_PLAIN measurement mode (C26)")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of sustained warm-up load")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-chunk-kib", type=int, default=4096, help="host-API chunk size (input KiB)")
+    ap.add_argument("--e2e-streams", type=int, default=3, help="host-API CUDA streams")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparator", action="store_true")

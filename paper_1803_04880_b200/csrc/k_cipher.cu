@@ -131,10 +131,11 @@ int launch_cipher_ctr(const CipherParams& p, void* stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t nblk = (p.n + 15) / 16;
     const uint64_t want = (nblk + kCipherThreads - 1) / kCipherThreads;
-    const uint64_t cap = (uint64_t)sms * (p.in ? kCipherCtasPerSm : kKeystreamCtasPerSm);
+    const bool lane = p.in != nullptr || p.lane_lut;
+    const uint64_t cap = (uint64_t)sms * (lane ? kCipherCtasPerSm : kKeystreamCtasPerSm);
     const unsigned grid = (unsigned)(want < cap ? want : cap);
     if (grid == 0) return 0;
-    if (p.in) {
+    if (lane) {
         allow_lut<k_cipher_ctr<true>>();
         k_cipher_ctr<true><<<grid, kCipherThreads, kAesLutBytes, (cudaStream_t)stream>>>(p);
     } else {

@@ -265,13 +265,20 @@ int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     return e ? SE_ECUDA : SE_OK;
 }
 
-int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
-                     const void* d_b, const void* d_c, void* d_out, se_report* d_report, void* stream) {
+}  // extern "C"
+
+namespace se {
+
+// fragment_recover with an optional caller-provided keystream scratch
+// (>= a_bytes + 16 device bytes; the host-streaming path passes its slot
+// buffer) and an optional already-initialised report (report_ready).
+int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a, const void* d_b,
+                 const void* d_c, void* d_out, se_report* d_report, void* d_ks, bool report_ready, void* stream) {
     se_layout lay;
     int rc = fused_checks(g, key, iv, lay);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    if (d_report) {   // first_bad_block = -1 (all ones), bad_blocks = 0
+    if (d_report && !report_ready) {   // first_bad_block = -1 (all ones), bad_blocks = 0
         if (cudaMemsetAsync(&d_report->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
             cudaMemsetAsync(&d_report->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
             return SE_ECUDA;
@@ -285,20 +292,23 @@ int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     p.report = d_report;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
-    keep_pool();
-    // keystream scratch (a_bytes, 7.8% of n at L = 2) from the stream-ordered pool
-    void* ks = nullptr;
-    if (cudaMallocAsync(&ks, lay.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
+    // keystream scratch (a_bytes, 7.8% of n at L = 2): the caller's, else the stream-ordered pool
+    void* ks = d_ks;
+    if (!ks) {
+        keep_pool();
+        if (cudaMallocAsync(&ks, lay.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
+    }
     p.ks = (const uint8_t*)ks;
     int e = launch_keystream(p, (uint8_t*)ks, lay.a_bytes, stream);
     if (g->mode == SE_MODE_BLOCK8) {
         if (!e) e = launch_recover_block8(p, g->levels, mask, stream);
-        cudaFreeAsync(ks, s);
+        if (!d_ks) cudaFreeAsync(ks, s);
         return e ? SE_ECUDA : SE_OK;
     }
+    keep_pool();
     int16_t* ws = e ? nullptr : ws_alloc(lay, g->width, s);
     if (!ws) {
-        cudaFreeAsync(ks, s);
+        if (!d_ks) cudaFreeAsync(ks, s);
         return SE_ECUDA;
     }
     p.ws = ws; p.rows = lay.rows;
@@ -307,8 +317,17 @@ int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     e = launch_recover_full(p, g->levels, mask, stream);                      // unmask + scatter
     if (!e) e = launch_dwt_full_inv(dp, g->levels, d_report, stream);         // inverse + report
     cudaFreeAsync(ws, s);
-    cudaFreeAsync(ks, s);
+    if (!d_ks) cudaFreeAsync(ks, s);
     return e ? SE_ECUDA : SE_OK;
+}
+
+}  // namespace se
+
+extern "C" {
+
+int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
+                     const void* d_b, const void* d_c, void* d_out, se_report* d_report, void* stream) {
+    return recover_impl(g, key, iv, d_a, d_b, d_c, d_out, d_report, nullptr, false, stream);
 }
 
 int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream) {

@@ -8,6 +8,10 @@
 
 using namespace se;
 
+#ifndef SE_DCT_LANE_KS
+#define SE_DCT_LANE_KS 0
+#endif
+
 static int check_dct(const se_dct_geom* g, bool need_level) {
     if (!g) return SE_EINVAL;
     if (g->width == 0 || g->height == 0 || g->width % 8 || g->height % 8) return SE_EINVAL;   // D11
@@ -40,6 +44,7 @@ static int launch_ks(const uint8_t key[16], const uint8_t iv[16], const se_dct_g
     cp.in = nullptr;
     cp.out = out;
     cp.n = n;
+    cp.lane_lut = SE_DCT_LANE_KS;
     return launch_cipher_ctr(cp, stream);
 }
 

@@ -10,6 +10,7 @@
 // stream-ordered pool.  Host buffers should be pinned for the copies to be
 // asynchronous (pageable buffers still work, with driver staging).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -68,15 +69,43 @@ static std::vector<Chunk> make_chunks(const se_geom* g, const se_layout& lay, ui
 // buffers for one chunk's input / output and its three fragment slices, grown
 // on demand).  Chunk k uses slot k mod S on stream k mod S, so stream order
 // alone makes slot reuse safe; steady-state calls allocate nothing.
+//
+// The per-chunk work is ~8 API calls (copies, keystream and fused kernels),
+// which at 1-4 MiB chunks costs as much host time as the PCIe transfer it
+// pipelines.  So each call's whole chunk sequence (on all streams, fork/join
+// by events) is captured once into a CUDA graph, cached per (operation,
+// geometry, key, IV, host pointers, chunking) and replayed by one
+// cudaGraphLaunch on later calls with the same arguments (host data is read
+// at replay time, so new contents in the same buffers are fine).  Any
+// staging-buffer reallocation drops the cache.  SE_HOST_GRAPHS=0 in the
+// environment disables it.
 struct Slot {
-    void* buf[4] = {nullptr, nullptr, nullptr, nullptr};   // bytes, A, B, C
-    size_t cap[4] = {0, 0, 0, 0};
+    void* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // bytes, A, B, C, keystream scratch
+    size_t cap[5] = {0, 0, 0, 0, 0};
+};
+
+struct GraphKey {
+    int op;                   // 0 protect, 1 recover
+    uint32_t n_streams;
+    uint64_t chunk_bytes;
+    se_geom g;
+    uint8_t key[16], iv[16];
+    const void* ptr[4];       // host buffers: bytes (in or out), A, B, C
+};
+
+struct GraphEntry {
+    GraphKey k;
+    cudaGraphExec_t exec;
 };
 
 struct HostCtx {
     std::vector<cudaStream_t> streams;
+    std::vector<cudaEvent_t> events;      // fork / join events for graph capture
+    std::vector<GraphEntry> graphs;       // small cache, most recent last
     std::vector<Slot> slots;
-    se_report* reps = nullptr;
+    se_report* reps = nullptr;            // device: one report per chunk
+    se_report* hreps = nullptr;           // pinned host mirror (async D2H, no per-chunk sync)
+    se_report* hinit = nullptr;           // pinned {-1, 0} per chunk: one H2D initialises a report
     size_t reps_cap = 0;
     std::mutex mu;
 };
@@ -93,15 +122,105 @@ static HostCtx& host_ctx(int dev) {
 static int ensure(HostCtx& c, uint32_t n_streams) {
     while (c.streams.size() < n_streams) {
         cudaStream_t s;
+        cudaEvent_t e;
         if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return SE_ECUDA;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SE_ECUDA;
         c.streams.push_back(s);
+        c.events.push_back(e);
         c.slots.emplace_back();
     }
     return SE_OK;
 }
 
-static int grow(void*& p, size_t& cap, size_t need) {
+static void drop_graphs(HostCtx& c) {
+    for (auto& g : c.graphs) cudaGraphExecDestroy(g.exec);
+    c.graphs.clear();
+}
+
+static bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SE_HOST_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+static GraphKey make_key(int op, const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* p0,
+                         const void* p1, const void* p2, const void* p3, uint64_t chunk_bytes, uint32_t n_streams) {
+    GraphKey k;
+    memset(&k, 0, sizeof k);
+    k.op = op; k.n_streams = n_streams; k.chunk_bytes = chunk_bytes; k.g = *g;
+    memcpy(k.key, key, 16); memcpy(k.iv, iv, 16);
+    k.ptr[0] = p0; k.ptr[1] = p1; k.ptr[2] = p2; k.ptr[3] = p3;
+    return k;
+}
+
+static cudaGraphExec_t find_graph(HostCtx& c, const GraphKey& k) {
+    for (auto& g : c.graphs)
+        if (memcmp(&g.k, &k, sizeof k) == 0) return g.exec;
+    return nullptr;
+}
+
+// Run issue(streams) either captured into a (cached) graph or directly.
+// issue() enqueues every chunk op on c.streams[k % S] and returns a status.
+static bool g_graph_broken = false;       // capture unsupported here: issue directly from then on
+
+template <typename F>
+static int run_direct(HostCtx& c, uint32_t n_streams, F& issue) {
+    int status = issue();
+    for (uint32_t i = 0; i < n_streams; ++i)
+        if (cudaStreamSynchronize(c.streams[i]) != cudaSuccess) status = SE_ECUDA;
+    return status;
+}
+
+// Run issue() — which enqueues every chunk op on c.streams[k % S] — either
+// captured into a (cached) graph and replayed, or directly.
+template <typename F>
+static int run_chunks(HostCtx& c, const GraphKey& key, uint32_t n_streams, F issue) {
+    if (!graphs_enabled() || g_graph_broken) return run_direct(c, n_streams, issue);
+    cudaStream_t s0 = c.streams[0];
+    cudaGraphExec_t exec = find_graph(c, key);
+    if (!exec) {
+        cudaGraph_t graph = nullptr;
+        if (cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            cudaGetLastError();
+            g_graph_broken = true;
+            return run_direct(c, n_streams, issue);
+        }
+        cudaEventRecord(c.events[0], s0);                                 // fork
+        for (uint32_t i = 1; i < n_streams; ++i) cudaStreamWaitEvent(c.streams[i], c.events[0], 0);
+        const int status = issue();
+        for (uint32_t i = 1; i < n_streams; ++i) {                        // join
+            cudaEventRecord(c.events[i], c.streams[i]);
+            cudaStreamWaitEvent(s0, c.events[i], 0);
+        }
+        const cudaError_t ce = cudaStreamEndCapture(s0, &graph);
+        if (status != SE_OK && status != SE_ECUDA) {                      // argument error: report it
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            return status;
+        }
+        if (ce != cudaSuccess || status != SE_OK || !graph ||
+            cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            g_graph_broken = true;
+            return run_direct(c, n_streams, issue);
+        }
+        cudaGraphDestroy(graph);
+        if (c.graphs.size() >= 8) {
+            cudaGraphExecDestroy(c.graphs.front().exec);
+            c.graphs.erase(c.graphs.begin());
+        }
+        c.graphs.push_back(GraphEntry{key, exec});
+    }
+    if (cudaGraphLaunch(exec, s0) != cudaSuccess) return SE_ECUDA;
+    return cudaStreamSynchronize(s0) == cudaSuccess ? SE_OK : SE_ECUDA;
+}
+
+static int grow(void*& p, size_t& cap, size_t need, HostCtx& c) {
     if (need <= cap) return SE_OK;
+    drop_graphs(c);                       // cached graphs hold the old pointer
     if (p) cudaFree(p);                   // synchronous, only while the slot grows
     p = nullptr;
     cap = 0;
@@ -136,36 +255,45 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
     if (ensure(ctx, n_streams)) return SE_ECUDA;
     const uint32_t bits[3] = {lay.a_bits, lay.b_bits, lay.c_bits};
     uint8_t* hout[3] = {(uint8_t*)h_a, (uint8_t*)h_b, (uint8_t*)h_c};
-    int status = SE_OK;
-    for (size_t k = 0; k < chunks.size() && status == SE_OK; ++k) {
+    std::vector<se_geom> cgs(chunks.size());
+    std::vector<se_layout> cls(chunks.size());
+    // pass 1: per-chunk geometry and staging capacity (may synchronise and reallocate)
+    for (size_t k = 0; k < chunks.size(); ++k) {
         const Chunk& c = chunks[k];
-        cudaStream_t s = ctx.streams[k % n_streams];
         Slot& sl = ctx.slots[k % n_streams];
-        se_geom cg = *g;
-        cg.n_bytes = c.byte1 - c.byte0;
-        cg.block_offset = g->block_offset + c.blk0;
-        se_layout cl;
-        fragment_layout(&cg, &cl);
-        const uint64_t sizes[4] = {cg.n_bytes, cl.a_bytes, cl.b_bytes, cl.c_bytes};
-        for (int i = 0; i < 4 && status == SE_OK; ++i) {
-            if (sizes[i] > sl.cap[i]) cudaStreamSynchronize(s);          // slot busy until its stream drains
-            status = grow(sl.buf[i], sl.cap[i], sizes[i] + 16);
+        cgs[k] = *g;
+        cgs[k].n_bytes = c.byte1 - c.byte0;
+        cgs[k].block_offset = g->block_offset + c.blk0;
+        fragment_layout(&cgs[k], &cls[k]);
+        const uint64_t sizes[4] = {cgs[k].n_bytes, cls[k].a_bytes, cls[k].b_bytes, cls[k].c_bytes};
+        for (int i = 0; i < 4; ++i) {
+            if (sizes[i] + 16 > sl.cap[i]) cudaStreamSynchronize(ctx.streams[k % n_streams]);
+            if (grow(sl.buf[i], sl.cap[i], sizes[i] + 16, ctx)) return SE_ECUDA;
         }
-        if (status == SE_OK &&
-            cudaMemcpyAsync(sl.buf[0], (const uint8_t*)h_in + c.byte0, cg.n_bytes, cudaMemcpyHostToDevice, s) !=
-                cudaSuccess)
-            status = SE_ECUDA;
-        if (status == SE_OK)
-            status = fragment_protect(&cg, key, iv, sl.buf[0], sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr,
-                                      sl.buf[3], s);
-        for (int i = 0; i < 3 && status == SE_OK; ++i)
-            if (sizes[i + 1] && cudaMemcpyAsync(hout[i] + c.blk0 * bits[i] / 8, sl.buf[i + 1], sizes[i + 1],
-                                                cudaMemcpyDeviceToHost, s) != cudaSuccess)
-                status = SE_ECUDA;
     }
-    for (uint32_t i = 0; i < n_streams; ++i)
-        if (cudaStreamSynchronize(ctx.streams[i]) != cudaSuccess) status = SE_ECUDA;
-    return status;
+    // pass 2: H2D -> keystream + fused kernel -> D2H per chunk, chunk k on stream k mod S
+    auto issue = [&]() -> int {
+        for (size_t k = 0; k < chunks.size(); ++k) {
+            const Chunk& c = chunks[k];
+            cudaStream_t s = ctx.streams[k % n_streams];
+            Slot& sl = ctx.slots[k % n_streams];
+            const se_layout& cl = cls[k];
+            const uint64_t sizes[4] = {cgs[k].n_bytes, cl.a_bytes, cl.b_bytes, cl.c_bytes};
+            if (cudaMemcpyAsync(sl.buf[0], (const uint8_t*)h_in + c.byte0, sizes[0], cudaMemcpyHostToDevice, s) !=
+                cudaSuccess)
+                return SE_ECUDA;
+            int st = fragment_protect(&cgs[k], key, iv, sl.buf[0], sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr,
+                                      sl.buf[3], s);
+            if (st) return st;
+            for (int i = 0; i < 3; ++i)
+                if (sizes[i + 1] && cudaMemcpyAsync(hout[i] + c.blk0 * bits[i] / 8, sl.buf[i + 1], sizes[i + 1],
+                                                    cudaMemcpyDeviceToHost, s) != cudaSuccess)
+                    return SE_ECUDA;
+        }
+        return SE_OK;
+    };
+    const GraphKey gk = make_key(0, g, key, iv, h_in, h_a, h_b, h_c, chunk_bytes, n_streams);
+    return run_chunks(ctx, gk, n_streams, issue);
 }
 
 int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_a,
@@ -189,47 +317,62 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
     if (ensure(ctx, n_streams)) return SE_ECUDA;
     if (chunks.size() > ctx.reps_cap) {
         for (auto s : ctx.streams) cudaStreamSynchronize(s);
+        drop_graphs(ctx);
         if (ctx.reps) cudaFree(ctx.reps);
-        ctx.reps = nullptr;
+        if (ctx.hreps) cudaFreeHost(ctx.hreps);
+        if (ctx.hinit) cudaFreeHost(ctx.hinit);
+        ctx.reps = ctx.hreps = ctx.hinit = nullptr;
         ctx.reps_cap = 0;
         if (cudaMalloc((void**)&ctx.reps, sizeof(se_report) * chunks.size()) != cudaSuccess) return SE_ECUDA;
+        if (cudaMallocHost((void**)&ctx.hreps, sizeof(se_report) * chunks.size()) != cudaSuccess) return SE_ECUDA;
+        if (cudaMallocHost((void**)&ctx.hinit, sizeof(se_report) * chunks.size()) != cudaSuccess) return SE_ECUDA;
+        for (size_t k = 0; k < chunks.size(); ++k) { ctx.hinit[k].first_bad_block = -1; ctx.hinit[k].bad_blocks = 0; }
         ctx.reps_cap = chunks.size();
     }
     const uint32_t bits[3] = {lay.a_bits, lay.b_bits, lay.c_bits};
     const uint8_t* hin[3] = {(const uint8_t*)h_a, (const uint8_t*)h_b, (const uint8_t*)h_c};
-    std::vector<se_report> reps(chunks.size());
-    int status = SE_OK;
-    for (size_t k = 0; k < chunks.size() && status == SE_OK; ++k) {
+    std::vector<se_geom> cgs(chunks.size());
+    std::vector<se_layout> cls(chunks.size());
+    for (size_t k = 0; k < chunks.size(); ++k) {
         const Chunk& c = chunks[k];
-        cudaStream_t s = ctx.streams[k % n_streams];
         Slot& sl = ctx.slots[k % n_streams];
-        se_geom cg = *g;
-        cg.n_bytes = c.byte1 - c.byte0;
-        cg.block_offset = g->block_offset + c.blk0;
-        se_layout cl;
-        fragment_layout(&cg, &cl);
-        const uint64_t sizes[4] = {cg.n_bytes, cl.a_bytes, cl.b_bytes, cl.c_bytes};
-        for (int i = 0; i < 4 && status == SE_OK; ++i) {
-            if (sizes[i] > sl.cap[i]) cudaStreamSynchronize(s);
-            status = grow(sl.buf[i], sl.cap[i], sizes[i] + 16);
+        cgs[k] = *g;
+        cgs[k].n_bytes = c.byte1 - c.byte0;
+        cgs[k].block_offset = g->block_offset + c.blk0;
+        fragment_layout(&cgs[k], &cls[k]);
+        const uint64_t sizes[5] = {cgs[k].n_bytes, cls[k].a_bytes, cls[k].b_bytes, cls[k].c_bytes, cls[k].a_bytes};
+        for (int i = 0; i < 5; ++i) {
+            if (sizes[i] + 16 > sl.cap[i]) cudaStreamSynchronize(ctx.streams[k % n_streams]);
+            if (grow(sl.buf[i], sl.cap[i], sizes[i] + 16, ctx)) return SE_ECUDA;
         }
-        for (int i = 0; i < 3 && status == SE_OK; ++i)
-            if (sizes[i + 1] && cudaMemcpyAsync(sl.buf[i + 1], hin[i] + c.blk0 * bits[i] / 8, sizes[i + 1],
-                                                cudaMemcpyHostToDevice, s) != cudaSuccess)
-                status = SE_ECUDA;
-        if (status == SE_OK)
-            status = fragment_recover(&cg, key, iv, sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr, sl.buf[3],
-                                      sl.buf[0], ctx.reps + k, s);
-        if (status == SE_OK &&
-            cudaMemcpyAsync((uint8_t*)h_out + c.byte0, sl.buf[0], cg.n_bytes, cudaMemcpyDeviceToHost, s) !=
-                cudaSuccess)
-            status = SE_ECUDA;
-        if (status == SE_OK &&
-            cudaMemcpyAsync(&reps[k], ctx.reps + k, sizeof(se_report), cudaMemcpyDeviceToHost, s) != cudaSuccess)
-            status = SE_ECUDA;
     }
-    for (uint32_t i = 0; i < n_streams; ++i)
-        if (cudaStreamSynchronize(ctx.streams[i]) != cudaSuccess) status = SE_ECUDA;
+    se_report* reps = ctx.hreps;          // pinned: the per-chunk copies stay asynchronous
+    auto issue = [&]() -> int {
+        for (size_t k = 0; k < chunks.size(); ++k) {
+            const Chunk& c = chunks[k];
+            cudaStream_t s = ctx.streams[k % n_streams];
+            Slot& sl = ctx.slots[k % n_streams];
+            const se_layout& cl = cls[k];
+            const uint64_t sizes[4] = {cgs[k].n_bytes, cl.a_bytes, cl.b_bytes, cl.c_bytes};
+            if (cudaMemcpyAsync(ctx.reps + k, ctx.hinit + k, sizeof(se_report), cudaMemcpyHostToDevice, s) !=
+                cudaSuccess)
+                return SE_ECUDA;
+            for (int i = 0; i < 3; ++i)
+                if (sizes[i + 1] && cudaMemcpyAsync(sl.buf[i + 1], hin[i] + c.blk0 * bits[i] / 8, sizes[i + 1],
+                                                    cudaMemcpyHostToDevice, s) != cudaSuccess)
+                    return SE_ECUDA;
+            int st = recover_impl(&cgs[k], key, iv, sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr, sl.buf[3],
+                                  sl.buf[0], ctx.reps + k, sl.buf[4], true, s);
+            if (st) return st;
+            if (cudaMemcpyAsync((uint8_t*)h_out + c.byte0, sl.buf[0], sizes[0], cudaMemcpyDeviceToHost, s) !=
+                    cudaSuccess ||
+                cudaMemcpyAsync(&reps[k], ctx.reps + k, sizeof(se_report), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+                return SE_ECUDA;
+        }
+        return SE_OK;
+    };
+    const GraphKey gk = make_key(1, g, key, iv, h_out, h_a, h_b, h_c, chunk_bytes, n_streams);
+    int status = run_chunks(ctx, gk, n_streams, issue);
     if (status == SE_OK && h_report) {
         for (size_t k = 0; k < chunks.size(); ++k) {
             if (reps[k].bad_blocks) {

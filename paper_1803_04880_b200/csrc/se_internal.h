@@ -64,6 +64,8 @@ struct CipherParams {
     uint64_t n;
     uint32_t ctr[4];          // IV + ctr_block_offset
     uint32_t rk[44];
+    uint32_t lane_lut;        // keystream (in == nullptr) with the 64 KB lane table
+    uint32_t pad_;
 };
 
 struct DwtParams {
@@ -102,6 +104,8 @@ struct DctParams {
 void cipher_setup(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block, CipherParams& cp);
 void sha512_kiv(const uint8_t key[16], const uint8_t iv[16], uint32_t kiv[8], uint64_t mid[8], uint64_t h0[8]);
 void keep_pool();
+int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a, const void* d_b,
+                 const void* d_c, void* d_out, se_report* d_report, void* d_ks, bool report_ready, void* stream);
 
 // launchers (return cudaError_t as int)
 int launch_protect_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);

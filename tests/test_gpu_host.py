@@ -73,3 +73,27 @@ def test_host_pageable_buffers(dev, orc):
     a, b, c = se.fragment_protect_host(xt, W, 2, KEY, IV, chunk_bytes=32 * 1024)
     oa, ob, oc = orc.protect(x, W, 2, KEY, IV)
     assert np.array_equal(c.numpy(), oc) and np.array_equal(a.numpy(), oa)
+
+
+def test_graph_replay_reads_new_contents(dev, orc):
+    """Repeated calls with the same buffers and arguments replay a cached CUDA
+    graph (se_host.cu): new contents of the same host buffers must be read,
+    and a different key or chunking must not reuse the graph."""
+    n, W, L = 1024 * 8 * 24, 1024, 2
+    hx = host(np.zeros(n, np.uint8))
+    lay = se.fragment_layout(n, W, L)
+    frag = tuple(se._host_empty(lay[k]) for k in ("a_bytes", "b_bytes", "c_bytes"))
+    out = se._host_empty(n)
+    for i, (key, chunk) in enumerate([(KEY, 64 * 1024), (KEY, 64 * 1024), (KEY, 64 * 1024),
+                                      (bytes(16), 64 * 1024), (KEY, 96 * 1024)]):
+        x = synth.random_bytes(n, 100 + i)
+        hx.copy_(torch.from_numpy(x))
+        se.fragment_protect_host(hx, W, L, key, IV, out=frag, chunk_bytes=chunk, n_streams=3)
+        oa, ob, oc = orc.protect(x, W, L, key, IV)
+        assert np.array_equal(frag[0].numpy(), oa) and np.array_equal(frag[2].numpy(), oc), i
+        _, rep = se.fragment_recover_host(*frag, n, W, L, key, IV, out=out, chunk_bytes=chunk, n_streams=3)
+        assert np.array_equal(out.numpy(), x) and rep == (-1, 0), i
+    # a corrupted replay still reports (the report copies are part of the graph)
+    frag[2][60 * 7] ^= 0xFF
+    _, rep = se.fragment_recover_host(*frag, n, W, L, KEY, IV, out=out, chunk_bytes=96 * 1024, n_streams=3)
+    assert rep == orc.recover(frag[0].numpy(), frag[1].numpy(), frag[2].numpy(), n, W, L, KEY, IV)[1]
