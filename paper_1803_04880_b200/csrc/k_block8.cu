@@ -19,19 +19,30 @@
 #ifndef SE_MIN_CTAS
 #define SE_MIN_CTAS 5      // resident 128-thread CTAs per SM the register budget must allow (96 regs)
 #endif
+// PUBLIC_PLAIN kernels (no SHA) are latency-bound: more resident warps pay
+// (protect fits 72 registers without spills; recover holds more records)
+#ifndef SE_MIN_CTAS_PLAIN_P
+#define SE_MIN_CTAS_PLAIN_P 7
+#endif
+#ifndef SE_MIN_CTAS_PLAIN_R
+#define SE_MIN_CTAS_PLAIN_R 6
+#endif
+#ifndef SE_MIN_CTAS_BATCH
+#define SE_MIN_CTAS_BATCH 5
+#endif
 
 namespace se {
 
 // ---------------------------------------------------------------- kernels
 
 template <int L, bool MASK>
-__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
+__global__ void __launch_bounds__(kBlocksPerCta, MASK ? SE_MIN_CTAS : SE_MIN_CTAS_PLAIN_P)
 k_protect_block8(const __grid_constant__ FusedParams p) {
     protect_cta<L, MASK, 0>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
-__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
+__global__ void __launch_bounds__(kBlocksPerCta, MASK ? SE_MIN_CTAS : SE_MIN_CTAS_PLAIN_R)
 k_recover_block8(const __grid_constant__ FusedParams p) {
     recover_cta<L, MASK, 0>(p, blockIdx.x);
 }
@@ -41,7 +52,7 @@ k_recover_block8(const __grid_constant__ FusedParams p) {
 // parameters in shared memory (the per-job counter base and SHA midstates were
 // derived on the host by fragment_batch_plan) and runs the same CTA body.
 template <int L, bool MASK, bool RECOVER>
-__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS)
+__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS_BATCH)
 k_batch_block8(const __grid_constant__ BatchParams bp) {
     __shared__ FusedParams sp;
     __shared__ uint32_t s_job;

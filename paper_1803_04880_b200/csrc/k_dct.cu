@@ -73,13 +73,18 @@ __device__ __forceinline__ float load11(uint32_t f) {
 // the 6 selected coefficients of one centered block (t = pixel sum: DC = t/8)
 struct Sel6 { float t, c01, c10, c20, c11, c02; };
 
-__device__ __forceinline__ Sel6 select6(const float (&f)[8][8]) {
+
+// Row-streaming: each row's 8 bytes become floats, then their row
+// frequencies 0, 1, 2; the 64 floats are never live together.
+__device__ __forceinline__ Sel6 select6(const uint32_t (&pw)[16]) {
     float T0[8], T1[8], T2[8];
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
-        float s[4], d[4];
+        float f[8], s[4], d[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { s[k] = f[x][k] + f[x][7 - k]; d[k] = f[x][k] - f[x][7 - k]; }
+        for (int y = 0; y < 8; ++y) f[y] = px(pw[2 * x + (y >> 2)], y & 3);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { s[k] = f[k] + f[7 - k]; d[k] = f[k] - f[7 - k]; }
         T0[x] = (s[0] + s[3]) + (s[1] + s[2]);
         T1[x] = fmaf(d1(3), d[3], fmaf(d1(2), d[2], fmaf(d1(1), d[1], d1(0) * d[0])));
         T2[x] = fmaf(d2(1), s[1] - s[2], d2(0) * (s[0] - s[3]));
@@ -102,14 +107,21 @@ __device__ __forceinline__ Sel6 select6(const float (&f)[8][8]) {
 }
 
 // bytes of f + bias + sum_k w_k D[u_k][x] D[v_k][y] over the 5 selected AC,
-// rounded to [0, 255]; row x -> words out[2x] (pixels 0-3), out[2x+1] (4-7)
-__device__ __forceinline__ void rebuild(const float (&f)[8][8], float bias, float w10, float w20, float w01,
-                                        float w11, float w02, uint32_t (&out)[16]) {
+// rounded to [0, 255], where f = the centered pixels held in pw (row x in
+// words 2x, 2x+1); the result replaces pw row by row.  The pixels are
+// converted again here (PRMT + FADD) rather than kept live as 64 floats.
+__device__ __forceinline__ void rebuild(uint32_t (&pw)[16], float bias, float w10, float w20, float w01,
+                                        float w11, float w02) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) asm volatile("" : "+r"(pw[k]));    // no reuse of select6's floats
     const float hA = kA0 * w02 * d2(0), hB = kA0 * w02 * d2(1);    // v = 2 terms, h(y) = hA, hB, -hB, -hA
     const float a01 = kA0 * w01;
     const float a10 = kA0 * w10, a20 = kA0 * w20;
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
+        float f[8];
+#pragma unroll
+        for (int y = 0; y < 8; ++y) f[y] = px(pw[2 * x + (y >> 2)], y & 3);
         const float R = fmaf(a20, d2(x), fmaf(a10, d1(x), bias));       // v = 0 terms + bias
         const float g1 = fmaf(w11, d1(x), a01);                          // v = 1 coefficient of row x
         uint32_t b[8];
@@ -117,11 +129,11 @@ __device__ __forceinline__ void rebuild(const float (&f)[8][8], float bias, floa
         for (int y = 0; y < 4; ++y) {
             const float h = y == 0 ? hA : y == 1 ? hB : y == 2 ? -hB : -hA;
             const float base = R + h;
-            b[y] = rnd_u8(f[x][y] + fmaf(g1, d1(y), base));
-            b[7 - y] = rnd_u8(f[x][7 - y] + fmaf(-g1, d1(y), base));
+            b[y] = rnd_u8(f[y] + fmaf(g1, d1(y), base));
+            b[7 - y] = rnd_u8(f[7 - y] + fmaf(-g1, d1(y), base));
         }
-        out[2 * x] = pack4(b[0], b[1], b[2], b[3]);
-        out[2 * x + 1] = pack4(b[4], b[5], b[6], b[7]);
+        pw[2 * x] = pack4(b[0], b[1], b[2], b[3]);
+        pw[2 * x + 1] = pack4(b[4], b[5], b[6], b[7]);
     }
 }
 
@@ -166,13 +178,6 @@ __device__ __forceinline__ void gather(const uint32_t (&w)[8][2 * C], uint32_t (
             pw[2 * x + 1] = pack4(b[4], b[5], b[6], b[7]);
         }
     }
-}
-
-__device__ __forceinline__ void to_float(const uint32_t (&pw)[16], float (&f)[8][8]) {
-#pragma unroll
-    for (int x = 0; x < 8; ++x)
-#pragma unroll
-        for (int y = 0; y < 8; ++y) f[x][y] = px(pw[2 * x + (y >> 2)], y & 3);
 }
 
 template <int C, int CH>
@@ -249,9 +254,7 @@ __device__ __forceinline__ void protect_layer(const DctParams& p, const uint32_t
                                               uint64_t br, uint64_t bc, uint32_t* sa, int tid) {
     uint32_t pw[16];
     gather<C, CH>(w, pw);
-    float f[8][8];
-    to_float(pw, f);
-    const Sel6 s = select6(f);
+    const Sel6 s = select6(pw);
     uint32_t q[6], r[3];
     q[0] = store11(s.t * 0.125f);                                         // Eq. 4.4, exact
     q[1] = store11(s.c01); q[2] = store11(s.c10); q[3] = store11(s.c20);
@@ -259,7 +262,7 @@ __device__ __forceinline__ void protect_layer(const DctParams& p, const uint32_t
     pack_record(q, r);
     smem_put_record<3, 66>(sa, (uint32_t)(tid * C + CH) * 66u, r);
     // Fragment 2 = x - t/64 - sum of the 5 AC terms (P:1487 pad-and-invert)
-    rebuild(f, 128.0f - s.t * 0.015625f, -s.c10, -s.c20, -s.c01, -s.c11, -s.c02, pw);
+    rebuild(pw, 128.0f - s.t * 0.015625f, -s.c10, -s.c20, -s.c01, -s.c11, -s.c02);
     if constexpr (LEVEL == 2) mask_level2<KEYED>(p, p.block_offset + pos * C + CH, r, pw);
     store_rows<C, CH>(p.out, p.width, br, bc, pw);
 }
@@ -272,13 +275,11 @@ __device__ __forceinline__ void recover_layer(const DctParams& p, const uint32_t
     unpack_record(r, q);
     gather<C, CH>(w, pw);
     if constexpr (LEVEL == 2) mask_level2<KEYED>(p, p.block_offset + pos * C + CH, r, pw);
-    float f[8][8];
-    to_float(pw, f);
-    const Sel6 s = select6(f);
+    const Sel6 s = select6(pw);
     // image = P + (iDCT of stored - computed over the 6 positions), + 128
     const float bias = fmaf(load11(q[0]), 0.125f, 128.0f) - s.t * 0.015625f;
-    rebuild(f, bias, load11(q[2]) - s.c10, load11(q[3]) - s.c20, load11(q[1]) - s.c01,
-            load11(q[4]) - s.c11, load11(q[5]) - s.c02, pw);
+    rebuild(pw, bias, load11(q[2]) - s.c10, load11(q[3]) - s.c20, load11(q[1]) - s.c01,
+            load11(q[4]) - s.c11, load11(q[5]) - s.c02);
     store_rows<C, CH>(p.out, p.width, br, bc, pw);
 }
 
@@ -333,9 +334,7 @@ template <int C, int CH>
 __device__ __forceinline__ void select_layer(const DctParams& p, const uint32_t (&w)[8][2 * C], uint64_t pos) {
     uint32_t pw[16];
     gather<C, CH>(w, pw);
-    float f[8][8];
-    to_float(pw, f);
-    const Sel6 s = select6(f);
+    const Sel6 s = select6(pw);
     float* o = p.coef + (pos * C + CH) * 6;
     o[0] = s.t * 0.125f; o[1] = s.c01; o[2] = s.c10; o[3] = s.c20; o[4] = s.c11; o[5] = s.c02;
 }
