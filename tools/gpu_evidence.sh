@@ -9,6 +9,8 @@ timeout 600 python bench.py > gpurun_out/ev/bench.json 2> gpurun_out/ev/bench.er
 timeout 600 python bench.py --plain --no-cpu-baseline > gpurun_out/ev/bench_plain.json 2>> gpurun_out/ev/bench.err
 timeout 900 python bench.py --config 4 --steps 10 --no-cpu-baseline > gpurun_out/ev/bench_c4.json 2>> gpurun_out/ev/bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/ev/bench_ref.json 2>> gpurun_out/ev/bench.err
+timeout 600 python bench.py --dct 1 --steps 100 > gpurun_out/ev/bench_dct_level1.json 2>> gpurun_out/ev/bench.err
+timeout 600 python bench.py --dct 2 --steps 100 --no-cpu-baseline > gpurun_out/ev/bench_dct_level2.json 2>> gpurun_out/ev/bench.err
 CMD="python bench.py --steps 3 --warmup 3 --soak 0 --no-cpu-baseline --no-comparator --e2e-steps 0"
 $CMD > gpurun_out/ev/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/ev/launches.csv $CMD > gpurun_out/ev/ncu_launches.log 2>&1 && \
@@ -17,5 +19,12 @@ ncu --set full --clock-control none --import-source on -k regex:k_recover_block8
 CMD2="python tools/prof_cipher.py"
 $CMD2 > gpurun_out/ev/plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_cipher_ctr -s 2 -c 1 -o gpurun_out/ev/cipher $CMD2 > gpurun_out/ev/ncu_c.log 2>&1
+CMD3="python tools/prof_dct.py 1"
+$CMD3 > gpurun_out/ev/plain3.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_dct_protect -s 1 -c 1 -o gpurun_out/ev/dct1_protect $CMD3 > gpurun_out/ev/ncu_d1p.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_dct_recover -s 1 -c 1 -o gpurun_out/ev/dct1_recover $CMD3 > gpurun_out/ev/ncu_d1r.log 2>&1
+CMD4="python tools/prof_dct.py 2"
+$CMD4 > gpurun_out/ev/plain4.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_dct_protect -s 1 -c 1 -o gpurun_out/ev/dct2_protect $CMD4 > gpurun_out/ev/ncu_d2p.log 2>&1
 echo evidence done
 ls gpurun_out/ev

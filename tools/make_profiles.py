@@ -129,6 +129,7 @@ def main(src, dst, tag):
             text, name, tb = kernel_summary(os.path.join(src, f))
             open(os.path.join(dst, f"{tag}_{f[:-8]}_ncu.txt"), "w").write(text)
             short = re.sub(r"\(.*", "", name).replace("void ", "").replace("se::", "")
+            short = re.sub(r"^(unnamed>::|\(anonymous namespace\)::)", "", short)
             traffic[short] = tb
     for f in sorted(os.listdir(src)):
         if f.endswith(".json") or f.endswith(".txt"):
