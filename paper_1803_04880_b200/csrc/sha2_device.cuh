@@ -64,6 +64,20 @@ __device__ __forceinline__ W64 fadd64(W64 a, W64 b, uint32_t one) {
 #endif
 }
 
+#ifndef SE_SHA512_SCHED_ADD
+#define SE_SHA512_SCHED_ADD SE_SHA512_ADD
+#endif
+// the message-schedule adds, selectable separately (pipe balance tuning)
+__device__ __forceinline__ W64 fadd64s(W64 a, W64 b, uint32_t one) {
+#if SE_SHA512_SCHED_ADD == 1
+    uint64_t t;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(t) : "r"(a.lo), "r"(one), "l"(u64(b)));
+    return W64{(uint32_t)t, fadd(a.hi, (uint32_t)(t >> 32), one)};
+#else
+    return fadd64(a, b, one);
+#endif
+}
+
 __device__ __forceinline__ W64 xor3(W64 a, W64 b, W64 c) { return W64{a.lo ^ b.lo ^ c.lo, a.hi ^ b.hi ^ c.hi}; }
 
 template <int N>
@@ -372,7 +386,7 @@ __device__ __forceinline__ void sha512_sched8_rounds(W64 (&S)[8], W64 (&W)[16], 
         const W64 w2 = win<J - 2>(W, N), w15 = win<J - 15>(W, N);
         const W64 s1 = sig2s_512<19, 61, 6, (SE_ROT_WIDE & 1) != 0>(w2, one);
         const W64 s0 = sig2s_512<1, 8, 7, (SE_ROT_WIDE & 1) != 0>(w15, one);
-        N[J] = fadd64(fadd64(fadd64(s1, win<J - 7>(W, N), one), s0, one), win<J - 16>(W, N), one);
+        N[J] = fadd64s(fadd64s(fadd64s(s1, win<J - 7>(W, N), one), s0, one), win<J - 16>(W, N), one);
         sha512_round<J>(S, fadd64(N[J], w64(k[J]), one), one);
         sha512_sched8_rounds<J + 1>(S, W, N, k, one);
     }
