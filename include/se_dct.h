@@ -89,6 +89,16 @@ int dct_recover(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
  * before rounding.  g->level and key material are not used. */
 int dct_select(const se_dct_geom* g, const void* d_in, float* d_coef, void* stream);
 
+/* The DCT 8x8 itself (Eq. 4.1 / 4.2; the operation of Table 4.1),
+ * fp32, for every 8x8 block of every layer.  dct8_forward: coefficients of
+ * (pixel - 128) into d_coef (W*H*channels floats, pixel layout:
+ * coefficient (u, v) of block (br, bc), layer ch at ((8br+u)*W + 8bc+v)*ch_n
+ * + ch).  dct8_inverse: Eq. 4.2 + 128, rounded half-to-even and clamped to
+ * [0, 255] (D3) into d_out.  g->level / flags / block_offset unused.
+ * d_coef 16-byte aligned. */
+int dct8_forward(const se_dct_geom* g, const void* d_in, float* d_coef, void* stream);
+int dct8_inverse(const se_dct_geom* g, const float* d_coef, void* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,6 +77,8 @@ def lib():
         L.oracle_dct8_inv.argtypes = [_f64p, _f64p]
         L.oracle_dct_layout.argtypes = [u32, u32, u32, _u64p]
         L.oracle_dct_select.argtypes = [u32, u32, u32, _u8p, _f64p]
+        L.oracle_dct_image_fwd.argtypes = [u32, u32, u32, _u8p, _f64p]
+        L.oracle_dct_image_inv.argtypes = [u32, u32, u32, _f64p, _u8p]
         L.oracle_dct_protect.argtypes = [u32, u32, u32, u32, u32, u64, _u8p, _u8p, _u8p, _u8p, _u8p, _f64p]
         L.oracle_dct_recover.argtypes = [u32, u32, u32, u32, u32, u64, _u8p, _u8p, _u8p, _u8p, _u8p, _f64p]
         L.oracle_record_fields.argtypes = [u32, u32, C.c_int, _i32p, _i32p, _i32p, _i32p, _i32p]
@@ -326,3 +328,22 @@ def dct_recover(a, p, width: int, height: int, channels: int, level: int, key: b
     if rc:
         raise ValueError(f"oracle_dct_recover failed rc={rc}")
     return (out, orl) if real else out
+
+
+def dct_image_fwd(img, width: int, height: int, channels: int = 1) -> np.ndarray:
+    """Full DCT 8x8 of (img - 128), coefficients in pixel layout (float64, img's shape)."""
+    lay = dct_layout(width, height, channels)
+    x = _u8(img)
+    assert x.size == lay["p_bytes"]
+    out = np.zeros(lay["p_bytes"])
+    assert lib().oracle_dct_image_fwd(width, height, channels, _p(x, _u8p), _p(out, _f64p)) == 0
+    return out
+
+
+def dct_image_inv(coef, width: int, height: int, channels: int = 1) -> np.ndarray:
+    lay = dct_layout(width, height, channels)
+    c = np.ascontiguousarray(coef, dtype=np.float64).reshape(-1)
+    assert c.size == lay["p_bytes"]
+    out = np.zeros(lay["p_bytes"], np.uint8)
+    assert lib().oracle_dct_image_inv(width, height, channels, _p(c, _f64p), _p(out, _u8p)) == 0
+    return out

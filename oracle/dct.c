@@ -168,6 +168,43 @@ static void select6(const double f[64], double c[64], double sel[6]) {
     for (int k = 0; k < 6; ++k) sel[k] = c[kSel[k][0] * 8 + kSel[k][1]];
 }
 
+/* The full DCT 8x8 of an image (Table 4.1's operation): every block of
+ * every layer, minus 128, by Eq. 4.1; coefficient (u, v) of block
+ * (br, bc) of layer ch at ((8br + u) * W + 8bc + v) * channels + ch. */
+int oracle_dct_image_fwd(uint32_t width, uint32_t height, uint32_t channels, const uint8_t* in, double* coef) {
+    uint64_t lay[4];
+    if (oracle_dct_layout(width, height, channels, lay)) return -1;
+    for (uint64_t br = 0; br < height / 8; ++br)
+        for (uint64_t bc = 0; bc < width / 8; ++bc)
+            for (uint32_t ch = 0; ch < channels; ++ch) {
+                double f[64], c[64];
+                block_get(in, width, ch, channels, br, bc, f);
+                for (int k = 0; k < 64; ++k) f[k] -= 128.0;
+                oracle_dct8_fwd(f, c);
+                for (int u = 0; u < 8; ++u)
+                    for (int v = 0; v < 8; ++v) coef[((8 * br + u) * width + 8 * bc + v) * channels + ch] = c[u * 8 + v];
+            }
+    return 0;
+}
+
+/* Its inverse by Eq. 4.2, + 128, rounded to bytes in [0, 255] (D3). */
+int oracle_dct_image_inv(uint32_t width, uint32_t height, uint32_t channels, const double* coef, uint8_t* out) {
+    uint64_t lay[4];
+    if (oracle_dct_layout(width, height, channels, lay)) return -1;
+    for (uint64_t br = 0; br < height / 8; ++br)
+        for (uint64_t bc = 0; bc < width / 8; ++bc)
+            for (uint32_t ch = 0; ch < channels; ++ch) {
+                double c[64], f[64];
+                uint8_t b[64];
+                for (int u = 0; u < 8; ++u)
+                    for (int v = 0; v < 8; ++v) c[u * 8 + v] = coef[((8 * br + u) * width + 8 * bc + v) * channels + ch];
+                oracle_dct8_inv(c, f);
+                for (int k = 0; k < 64; ++k) b[k] = to_u8(f[k] + 128.0);
+                block_put(out, width, ch, channels, br, bc, b);
+            }
+    return 0;
+}
+
 int oracle_dct_select(uint32_t width, uint32_t height, uint32_t channels, const uint8_t* in, double* coef6) {
     uint64_t lay[4];
     if (oracle_dct_layout(width, height, channels, lay)) return -1;

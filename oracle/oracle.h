@@ -115,6 +115,10 @@ void oracle_dct8_fwd(const double f[64], double c[64]);    /* Eq. 4.1 */
 void oracle_dct8_inv(const double c[64], double f[64]);    /* Eq. 4.2 */
 /* out[0]=records, out[1]=66, out[2]=Fragment-1 bytes, out[3]=Fragment-2 bytes */
 int oracle_dct_layout(uint32_t width, uint32_t height, uint32_t channels, uint64_t out[4]);
+/* full DCT 8x8 of an image minus 128 (Eq. 4.1), coefficients in pixel layout;
+ * and its inverse (Eq. 4.2) + 128 rounded to bytes (Table 4.1's operation) */
+int oracle_dct_image_fwd(uint32_t width, uint32_t height, uint32_t channels, const uint8_t* in, double* coef);
+int oracle_dct_image_inv(uint32_t width, uint32_t height, uint32_t channels, const double* coef, uint8_t* out);
 /* the 6 selected real coefficients per record (DC from Eq. 4.4) */
 int oracle_dct_select(uint32_t width, uint32_t height, uint32_t channels, const uint8_t* in, double* coef6);
 /* p_real / out_real (optional, 64 doubles per record, block row-major):

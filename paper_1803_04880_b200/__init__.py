@@ -94,7 +94,7 @@ SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_
            "fragment_protect_batch", "fragment_recover_batch", "fragment_protect_host",
            "fragment_recover_host", "dwt_fwd", "dwt_inv", "cipher_encrypt", "cipher_decrypt",
            "se_stats_accumulate", "se_strerror", "se_launch_count",
-           "dct_layout", "dct_protect", "dct_recover", "dct_select",
+           "dct_layout", "dct_protect", "dct_recover", "dct_select", "dct8_forward", "dct8_inverse",
            "se_container_streams", "se_container_size", "se_container_pack", "se_container_open",
            "se_disperse_plan", "se_storage_footprint", "se_sha256"]
 
@@ -147,6 +147,8 @@ def lib():
         L.dct_protect.argtypes = [dg, u8p, u8p, vp, vp, vp, vp]
         L.dct_recover.argtypes = [dg, u8p, u8p, vp, vp, vp, vp]
         L.dct_select.argtypes = [dg, vp, vp, vp]
+        L.dct8_forward.argtypes = [dg, vp, vp, vp]
+        L.dct8_inverse.argtypes = [dg, vp, vp, vp]
         cip = C.POINTER(ContainerInfo)
         L.se_container_streams.argtypes = [cip, C.POINTER(C.c_uint64)]
         L.se_container_size.argtypes = [cip, C.c_uint32, C.POINTER(C.c_uint64)]
@@ -422,6 +424,25 @@ def sha256(data) -> bytes:
     out = (C.c_uint8 * 32)()
     lib().se_sha256(b.ctypes.data if b.size else None, b.size, out)
     return bytes(out)
+
+
+def dct8_forward(img, width: int, height: int, channels: int = 1, out=None, stream=None):
+    """DCT 8x8 (Eq. 4.1) of (img - 128), fp32 coefficients in pixel layout (device tensor)."""
+    import torch
+    lay = dct_layout(width, height, channels)
+    o = out if out is not None else torch.empty(lay["p_bytes"], dtype=torch.float32, device=img.device)
+    _check(lib().dct8_forward(C.byref(_dgeom(width, height, channels, 1)), _ptr(img), _ptr(o), _stream(stream)),
+           "dct8_forward")
+    return o
+
+
+def dct8_inverse(coef, width: int, height: int, channels: int = 1, out=None, stream=None):
+    """iDCT 8x8 (Eq. 4.2) + 128, rounded to bytes in [0, 255] (device tensor)."""
+    lay = dct_layout(width, height, channels)
+    o = out if out is not None else _empty(lay["p_bytes"], coef.device)
+    _check(lib().dct8_inverse(C.byref(_dgeom(width, height, channels, 1)), _ptr(coef), _ptr(o), _stream(stream)),
+           "dct8_inverse")
+    return o
 
 
 def launch_count(reset: bool = False) -> int:

@@ -352,6 +352,143 @@ __global__ void __launch_bounds__(kBlocksPerCta) k_dct_select(const DctParams p)
     if constexpr (C > 3) select_layer<C, 3>(p, w, pos);
 }
 
+// ---------------------------------------------------------------- full DCT 8x8 (Table 4.1)
+
+// D[u][x] = alpha(u) cos(pi (2x+1) u / 16) for any u, x (Eq. 4.1, 4.3):
+// reduce (2x+1)u mod 32 onto [0, 8] with the cosine's symmetries.
+__device__ __forceinline__ constexpr float hcos(int k) {      // cos(k pi / 16) / 2, k = 0..8
+    return k == 0 ? 0.5f : k == 1 ? (float)SE_DCT_H1 : k == 2 ? (float)SE_DCT_H2 : k == 3 ? (float)SE_DCT_H3
+         : k == 4 ? (float)SE_DCT_H4 : k == 5 ? (float)SE_DCT_H5 : k == 6 ? (float)SE_DCT_H6
+         : k == 7 ? (float)SE_DCT_H7 : 0.0f;
+}
+__device__ __forceinline__ constexpr float dm(int u, int x) {
+    return u == 0 ? kA0
+         : (((2 * x + 1) * u) % 32 > 16 ? 32 - ((2 * x + 1) * u) % 32 : ((2 * x + 1) * u) % 32) > 8
+               ? -hcos(16 - (((2 * x + 1) * u) % 32 > 16 ? 32 - ((2 * x + 1) * u) % 32 : ((2 * x + 1) * u) % 32))
+               : hcos(((2 * x + 1) * u) % 32 > 16 ? 32 - ((2 * x + 1) * u) % 32 : ((2 * x + 1) * u) % 32);
+}
+
+// 8-point orthonormal DCT-II (Eq. 4.1 in one dimension), even/odd split:
+// even u use s = f(x) + f(7-x), odd u use d = f(x) - f(7-x).
+__device__ __forceinline__ void dct8_1d(const float (&f)[8], float (&X)[8]) {
+    float s[4], d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { s[k] = f[k] + f[7 - k]; d[k] = f[k] - f[7 - k]; }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const float (&v)[4] = (u & 1) ? d : s;
+        X[u] = fmaf(dm(u, 3), v[3], fmaf(dm(u, 2), v[2], fmaf(dm(u, 1), v[1], dm(u, 0) * v[0])));
+    }
+}
+
+// its inverse (Eq. 4.2): f(x) = e(x) + o(x), f(7-x) = e(x) - o(x)
+__device__ __forceinline__ void idct8_1d(const float (&X)[8], float (&f)[8]) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+        const float e = fmaf(dm(6, x), X[6], fmaf(dm(4, x), X[4], fmaf(dm(2, x), X[2], dm(0, x) * X[0])));
+        const float o = fmaf(dm(7, x), X[7], fmaf(dm(5, x), X[5], fmaf(dm(3, x), X[3], dm(1, x) * X[1])));
+        f[x] = e + o;
+        f[7 - x] = e - o;
+    }
+}
+
+template <int C, int CH>
+__device__ __forceinline__ void dct8_layer(const DctParams& p, const uint32_t (&w)[8][2 * C], uint64_t br,
+                                           uint64_t bc) {
+    uint32_t pw[16];
+    gather<C, CH>(w, pw);
+    float T[8][8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {                                       // rows
+        float f[8];
+#pragma unroll
+        for (int y = 0; y < 8; ++y) f[y] = px(pw[2 * x + (y >> 2)], y & 3);
+        dct8_1d(f, T[x]);
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {                                       // columns
+        float col[8], Y[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) col[x] = T[x][v];
+        dct8_1d(col, Y);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) T[u][v] = Y[u];                     // (u, v) in place
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        float* row = p.coef + ((8 * br + u) * (uint64_t)p.width + 8 * bc) * C;
+        if constexpr (C == 1) {
+            reinterpret_cast<float4*>(row)[0] = make_float4(T[u][0], T[u][1], T[u][2], T[u][3]);
+            reinterpret_cast<float4*>(row)[1] = make_float4(T[u][4], T[u][5], T[u][6], T[u][7]);
+        } else {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) row[v * C + CH] = T[u][v];
+        }
+    }
+}
+
+template <int C>
+__global__ void __launch_bounds__(kBlocksPerCta) k_dct8_fwd(const DctParams p) {
+    const uint64_t pos = (uint64_t)blockIdx.x * kBlocksPerCta + threadIdx.x;
+    if (pos >= p.n_pos) return;
+    const uint64_t br = pos / p.bpr, bc = pos - br * p.bpr;
+    uint32_t w[8][2 * C];
+    load_rows<C>(p.in, p.width, br, bc, w);
+    dct8_layer<C, 0>(p, w, br, bc);
+    if constexpr (C > 1) dct8_layer<C, 1>(p, w, br, bc);
+    if constexpr (C > 2) dct8_layer<C, 2>(p, w, br, bc);
+    if constexpr (C > 3) dct8_layer<C, 3>(p, w, br, bc);
+}
+
+template <int C, int CH>
+__device__ __forceinline__ void idct8_layer(const DctParams& p, uint64_t br, uint64_t bc) {
+    float T[8][8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const float* row = p.coef + ((8 * br + u) * (uint64_t)p.width + 8 * bc) * C;
+        if constexpr (C == 1) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(row)), b = __ldg(reinterpret_cast<const float4*>(row) + 1);
+            T[u][0] = a.x; T[u][1] = a.y; T[u][2] = a.z; T[u][3] = a.w;
+            T[u][4] = b.x; T[u][5] = b.y; T[u][6] = b.z; T[u][7] = b.w;
+        } else {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) T[u][v] = __ldg(row + v * C + CH);
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {                                       // columns
+        float col[8], f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) col[u] = T[u][v];
+        idct8_1d(col, f);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) T[x][v] = f[x];
+    }
+    uint32_t pw[16];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {                                       // rows, + 128, bytes
+        float f[8];
+        idct8_1d(T[x], f);
+        uint32_t b[8];
+#pragma unroll
+        for (int y = 0; y < 8; ++y) b[y] = rnd_u8(f[y] + 128.0f);
+        pw[2 * x] = pack4(b[0], b[1], b[2], b[3]);
+        pw[2 * x + 1] = pack4(b[4], b[5], b[6], b[7]);
+    }
+    store_rows<C, CH>(p.out, p.width, br, bc, pw);
+}
+
+template <int C>
+__global__ void __launch_bounds__(kBlocksPerCta) k_dct8_inv(const DctParams p) {
+    const uint64_t pos = (uint64_t)blockIdx.x * kBlocksPerCta + threadIdx.x;
+    if (pos >= p.n_pos) return;
+    const uint64_t br = pos / p.bpr, bc = pos - br * p.bpr;
+    idct8_layer<C, 0>(p, br, bc);
+    if constexpr (C > 1) idct8_layer<C, 1>(p, br, bc);
+    if constexpr (C > 2) idct8_layer<C, 2>(p, br, bc);
+    if constexpr (C > 3) idct8_layer<C, 3>(p, br, bc);
+}
+
 template <int C, int LEVEL, bool KEYED>
 void launch_c(const DctParams& p, int op, unsigned grid, cudaStream_t s) {
     if (op == 0) launch_pdl(k_dct_protect<C, LEVEL, KEYED>, grid, kBlocksPerCta, s, p);
@@ -361,6 +498,8 @@ void launch_c(const DctParams& p, int op, unsigned grid, cudaStream_t s) {
 template <int C>
 void launch_level(const DctParams& p, uint32_t level, bool keyed, int op, unsigned grid, cudaStream_t s) {
     if (op == 2) k_dct_select<C><<<grid, kBlocksPerCta, 0, s>>>(p);
+    else if (op == 3) k_dct8_fwd<C><<<grid, kBlocksPerCta, 0, s>>>(p);
+    else if (op == 4) k_dct8_inv<C><<<grid, kBlocksPerCta, 0, s>>>(p);
     else if (level == 1) launch_c<C, 1, false>(p, op, grid, s);
     else if (keyed) launch_c<C, 2, true>(p, op, grid, s);
     else launch_c<C, 2, false>(p, op, grid, s);

@@ -117,4 +117,38 @@ int dct_select(const se_dct_geom* g, const void* d_in, float* d_coef, void* stre
     return launch_dct(p, g->channels, 1, false, 2, stream) ? SE_ECUDA : SE_OK;
 }
 
+static int dct8_common(const se_dct_geom* g, se_dct_layout& lay) {
+    int rc = check_dct(g, false);
+    if (rc) return rc;
+    se_dct_geom g2 = *g;
+    g2.level = 1;
+    g2.flags = 0;
+    g2.block_offset = 0;
+    return dct_layout(&g2, &lay);
+}
+
+int dct8_forward(const se_dct_geom* g, const void* d_in, float* d_coef, void* stream) {
+    se_dct_layout lay;
+    int rc = dct8_common(g, lay);
+    if (rc) return rc;
+    if (!d_in || !d_coef) return SE_EINVAL;
+    if (!aligned16(d_in) || !aligned16(d_coef)) return SE_EALIGN;
+    DctParams p = dct_params(g, lay);
+    p.in = (const uint8_t*)d_in;
+    p.coef = d_coef;
+    return launch_dct(p, g->channels, 1, false, 3, stream) ? SE_ECUDA : SE_OK;
+}
+
+int dct8_inverse(const se_dct_geom* g, const float* d_coef, void* d_out, void* stream) {
+    se_dct_layout lay;
+    int rc = dct8_common(g, lay);
+    if (rc) return rc;
+    if (!d_coef || !d_out) return SE_EINVAL;
+    if (!aligned16(d_out) || !aligned16(d_coef)) return SE_EALIGN;
+    DctParams p = dct_params(g, lay);
+    p.coef = const_cast<float*>(d_coef);
+    p.out = (uint8_t*)d_out;
+    return launch_dct(p, g->channels, 1, false, 4, stream) ? SE_ECUDA : SE_OK;
+}
+
 }  // extern "C"

@@ -87,7 +87,7 @@ struct DctParams {
     uint8_t* out;             // protect: Fragment 2; recover: rebuilt image
     uint8_t* a;               // Fragment 1 stream (protect: holds the keystream on entry)
     const uint8_t* ks;        // recover: keystream of Fragment 1 (scratch)
-    float* coef;              // dct_select: records x 6
+    float* coef;              // dct_select: records x 6; dct8_forward/inverse: coefficient image
     uint64_t n_pos;           // block positions (W/8)*(H/8)
     uint64_t a_bytes;
     uint64_t block_offset;    // global record index of record 0 (KEYED nonce)
@@ -122,7 +122,7 @@ int launch_recover_full(const FusedParams& p, uint32_t levels, bool mask, void* 
 int launch_dwt_inv_block8(const DwtParams& p, uint32_t levels, void* stream);
 int launch_cipher_ctr(const CipherParams& p, void* stream);
 
-int launch_dct(const DctParams& p, uint32_t channels, uint32_t level, bool keyed, int op, void* stream);  // op 0 protect, 1 recover, 2 select
+int launch_dct(const DctParams& p, uint32_t channels, uint32_t level, bool keyed, int op, void* stream);  // op 0 protect, 1 recover, 2 select, 3 dct8 fwd, 4 dct8 inv
 
 int launch_stats(const void* x, const void* y, uint64_t n, uint32_t width, se_stats* out, uint32_t* joint,
                  void* stream);

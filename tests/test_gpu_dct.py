@@ -184,3 +184,28 @@ def test_full_size_sampled(dev, orc):
         check_protect(orc, xs, W, 64, 1, 2, 0, off, a_np[a0:a0 + band_bytes], p_np[rows])
     y = se.dct_recover(a, p, W, H, 1, 2, KEY, IV)
     assert psnr(x, y.cpu().numpy()) > 59.5
+
+
+@pytest.mark.parametrize("W,H,C", [(8, 8, 1), (72, 40, 1), (1024, 128, 1), (64, 48, 3), (48, 40, 4)])
+def test_dct8_transform_parity(dev, orc, W, H, C):
+    """The DCT 8x8 alone (Table 4.1's operation): fp32 coefficients within
+    TAU_C of the oracle's Eq. 4.1; the inverse of the oracle's coefficients
+    equals the oracle's inverse on every decided byte (and x itself)."""
+    x = image(W, H, C, 7 * W + H + C)
+    got = se.dct8_forward(to_dev(x, dev), W, H, C).cpu().numpy().astype(np.float64)
+    ref = orc.dct_image_fwd(x, W, H, C)
+    assert np.max(np.abs(got - ref)) <= TAU_C
+    back = se.dct8_inverse(to_dev(ref.astype(np.float32), dev), W, H, C).cpu().numpy()
+    assert np.array_equal(back, orc.dct_image_inv(ref, W, H, C))
+    assert np.array_equal(back, x)                                      # lossless before rounding loss
+    import scipy.fft
+    c = np.random.default_rng(W).normal(0, 40, x.size)                 # arbitrary coefficients: ties, clamps
+    real = unblocks(scipy.fft.idctn(blocks_f(c, W, H, C), type=2, norm="ortho", axes=(1, 2)), W, H, C) + 128
+    g = se.dct8_inverse(to_dev(c.astype(np.float32), dev), W, H, C).cpu().numpy()
+    r = orc.dct_image_inv(c.astype(np.float32).astype(np.float64), W, H, C)
+    tie = near_half(real, TAU_P)
+    assert np.array_equal(g[~tie], r[~tie]) and np.abs(g.astype(int) - r).max() <= 1
+
+
+def blocks_f(v, W, H, C):
+    return np.asarray(v, np.float64).reshape(H // 8, 8, W // 8, 8, C).transpose(0, 2, 4, 1, 3).reshape(-1, 8, 8)

@@ -48,6 +48,18 @@ def test_dct8_equals_scipy_orthonormal_dct2(orc, seed):
     assert np.isclose((f ** 2).sum(), (c ** 2).sum())                          # Parseval
 
 
+@pytest.mark.parametrize("W,H,C", [(16, 8, 1), (24, 16, 3)])
+def test_image_transform_equals_scipy(orc, W, H, C):
+    """The whole-image DCT (Table 4.1's operation) = scipy per block of
+    (x - 128), coefficients in pixel layout; the inverse rebuilds x exactly."""
+    img = synth.bitmap(H, W, C, 31).reshape(-1)
+    got = orc.dct_image_fwd(img, W, H, C)
+    blk = blocks(img, W, H, C).astype(float) - 128
+    ref = unblocks(scipy.fft.dctn(blk, type=2, norm="ortho", axes=(1, 2)), W, H, C)
+    assert np.allclose(got, ref, atol=1e-9)
+    assert np.array_equal(orc.dct_image_inv(got, W, H, C), img)
+
+
 def test_dc_is_eight_times_the_mean(orc):
     """Eq. 4.4: C(0,0) = alpha(0)^2 sum f = 8 * mean; all AC of a flat block vanish."""
     f = np.full((8, 8), 37.0)
