@@ -175,9 +175,23 @@ static int run_direct(HostCtx& c, uint32_t n_streams, F& issue) {
 
 // Run issue() — which enqueues every chunk op on c.streams[k % S] — either
 // captured into a (cached) graph and replayed, or directly.
+// Page-locked (or registered) host memory?  Copies from pageable memory are
+// staged synchronously by the driver and cannot be captured into a graph.
+static bool pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 template <typename F>
 static int run_chunks(HostCtx& c, const GraphKey& key, uint32_t n_streams, F issue) {
     if (!graphs_enabled() || g_graph_broken) return run_direct(c, n_streams, issue);
+    for (const void* p : key.ptr)
+        if (!pinned(p)) return run_direct(c, n_streams, issue);
     cudaStream_t s0 = c.streams[0];
     cudaGraphExec_t exec = find_graph(c, key);
     if (!exec) {
