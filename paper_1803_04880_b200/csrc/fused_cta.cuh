@@ -95,48 +95,52 @@ __device__ __forceinline__ void smem_get_record(const uint32_t* s, uint32_t nwor
     r[NW - 1] &= head_mask(BITS % 32);
 }
 
+template <int NT = kBlocksPerCta>
 __device__ __forceinline__ void copy_g2s(uint32_t* s, const uint8_t* __restrict__ g, uint64_t len,
                                          uint32_t cap_bytes, int tid) {
     // zero-filled copy of `len` bytes (<= cap) from 16-byte aligned global memory
     const uint32_t nv = (uint32_t)(len / 16);
-    for (uint32_t i = tid; i < nv; i += kBlocksPerCta)
+    for (uint32_t i = tid; i < nv; i += NT)
         reinterpret_cast<uint4*>(s)[i] = __ldg(reinterpret_cast<const uint4*>(g) + i);
     uint8_t* sb = reinterpret_cast<uint8_t*>(s);
-    for (uint32_t i = nv * 16 + tid; i < cap_bytes; i += kBlocksPerCta) sb[i] = (i < len) ? g[i] : 0;
+    for (uint32_t i = nv * 16 + tid; i < cap_bytes; i += NT) sb[i] = (i < len) ? g[i] : 0;
 }
 
+template <int NT = kBlocksPerCta>
 __device__ __forceinline__ void copy_s2g(uint8_t* __restrict__ g, const uint32_t* s, uint64_t len, int tid) {
     const uint32_t nv = (uint32_t)(len / 16);
-    for (uint32_t i = tid; i < nv; i += kBlocksPerCta)
+    for (uint32_t i = tid; i < nv; i += NT)
         reinterpret_cast<uint4*>(g)[i] = reinterpret_cast<const uint4*>(s)[i];
     const uint8_t* sb = reinterpret_cast<const uint8_t*>(s);
-    for (uint32_t i = nv * 16 + tid; i < len; i += kBlocksPerCta) g[i] = sb[i];
+    for (uint32_t i = nv * 16 + tid; i < len; i += NT) g[i] = sb[i];
 }
 
 // A' = A ^ KS where the keystream already sits at the destination in global
 // memory (written there by k_cipher_ctr); each CTA reads and rewrites only its
 // own slice.
+template <int NT = kBlocksPerCta>
 __device__ __forceinline__ void copy_s2g_xor_global(uint8_t* __restrict__ g, const uint32_t* s, uint64_t len,
                                                     int tid) {
     const uint32_t nv = (uint32_t)(len / 16);
-    for (uint32_t i = tid; i < nv; i += kBlocksPerCta) {
+    for (uint32_t i = tid; i < nv; i += NT) {
         const uint4 a = reinterpret_cast<const uint4*>(s)[i], k = reinterpret_cast<const uint4*>(g)[i];
         reinterpret_cast<uint4*>(g)[i] = make_uint4(a.x ^ k.x, a.y ^ k.y, a.z ^ k.z, a.w ^ k.w);
     }
     const uint8_t* sb = reinterpret_cast<const uint8_t*>(s);
-    for (uint32_t i = nv * 16 + tid; i < len; i += kBlocksPerCta) g[i] = sb[i] ^ g[i];
+    for (uint32_t i = nv * 16 + tid; i < len; i += NT) g[i] = sb[i] ^ g[i];
 }
 
 // A = A' ^ KS in shared memory, keystream read from global memory.
+template <int NT = kBlocksPerCta>
 __device__ __forceinline__ void xor_g2s(uint32_t* s, const uint8_t* __restrict__ ks, uint64_t len, int tid) {
     const uint32_t nv = (uint32_t)(len / 16);
-    for (uint32_t i = tid; i < nv; i += kBlocksPerCta) {
+    for (uint32_t i = tid; i < nv; i += NT) {
         const uint4 k = reinterpret_cast<const uint4*>(ks)[i];
         uint4& a = reinterpret_cast<uint4*>(s)[i];
         a.x ^= k.x; a.y ^= k.y; a.z ^= k.z; a.w ^= k.w;
     }
     uint8_t* sb = reinterpret_cast<uint8_t*>(s);
-    for (uint32_t i = nv * 16 + tid; i < len; i += kBlocksPerCta) sb[i] ^= ks[i];
+    for (uint32_t i = nv * 16 + tid; i < len; i += NT) sb[i] ^= ks[i];
 }
 
 // SHA-256 mask of B from the plain A record (framing C15: K||IV||be64(b)||A).
@@ -267,20 +271,24 @@ __device__ __forceinline__ void footprint_full(const FusedParams& p, uint64_t br
 // kernel with programmatic stream serialization; the CTA waits for it
 // (griddepcontrol.wait) only at the copy-out, so the keystream kernel overlaps
 // the lifting and hashing and the fused kernel carries no AES tables.
-template <int L, bool MASK, int MODE = 0>
+// BPC = blocks (threads) per CTA: 128 everywhere but the single-file BLOCK8
+// kernels at L = 1, 2, where 32 or 64 give finer work units (k_block8.cu).
+template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta>
 __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
-    constexpr int SA_W = 4 * R::ABITS;             // 16*ABITS bytes per CTA
-    constexpr int SB_W = R::BBITS ? 4 * R::BBITS : 4;
-    constexpr int SC_W = 4 * R::CBITS;
+    static_assert((BPC * R::ABITS) % 128 == 0 && (BPC * R::BBITS) % 128 == 0 && (BPC * R::CBITS) % 128 == 0,
+                  "CTA stream slices must be whole 16-byte units (and A whole AES blocks)");
+    constexpr int SA_W = BPC * R::ABITS / 32;      // BPC*ABITS/8 bytes per CTA
+    constexpr int SB_W = R::BBITS ? BPC * R::BBITS / 32 : 4;
+    constexpr int SC_W = BPC * R::CBITS / 32;
     __shared__ __align__(16) uint32_t sa[SA_W];
     __shared__ __align__(16) uint32_t sb[SB_W];
     __shared__ __align__(16) uint32_t sc[SC_W];
 
     const int tid = threadIdx.x;
-    const uint64_t blk = cta * kBlocksPerCta + tid;
-    for (int i = tid; i < SA_W; i += kBlocksPerCta) sa[i] = 0;
-    for (int i = tid; i < SB_W; i += kBlocksPerCta) sb[i] = 0;
+    const uint64_t blk = cta * BPC + tid;
+    for (int i = tid; i < SA_W; i += BPC) sa[i] = 0;
+    for (int i = tid; i < SB_W; i += BPC) sb[i] = 0;
     __syncthreads();
 
     if (blk < p.n_blocks) {
@@ -324,14 +332,14 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
 
     // row a9: 128-bit coalesced stores of the CTA's slice of each stream;
     // A' = A ^ keystream on the way out (row a6, XOR half)
-    const uint64_t a0 = cta * 16ull * R::ABITS, c0 = cta * 16ull * R::CBITS;
+    const uint64_t a0 = cta * (BPC / 8ull) * R::ABITS, c0 = cta * (BPC / 8ull) * R::CBITS;
     asm volatile("griddepcontrol.wait;" ::: "memory");              // keystream kernel complete
-    copy_s2g_xor_global(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
+    copy_s2g_xor_global<BPC>(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
     if (R::BBITS) {
-        const uint64_t b0 = cta * 16ull * R::BBITS;
-        copy_s2g(p.b + b0, sb, min((uint64_t)SB_W * 4, p.b_bytes - b0), tid);
+        const uint64_t b0 = cta * (BPC / 8ull) * R::BBITS;
+        copy_s2g<BPC>(p.b + b0, sb, min((uint64_t)SB_W * 4, p.b_bytes - b0), tid);
     }
-    copy_s2g(p.c + c0, sc, min((uint64_t)SC_W * 4, p.c_bytes - c0), tid);
+    copy_s2g<BPC>(p.c + c0, sc, min((uint64_t)SC_W * 4, p.c_bytes - c0), tid);
 }
 
 // ---------------------------------------------------------------- recover
@@ -342,12 +350,14 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
 // The keystream of the whole A stream sits in p.ks (k_cipher_ctr, launched
 // before with programmatic stream serialization); it is waited for and
 // applied after the SHA-512 unmask of C, which does not need A.
-template <int L, bool MASK, int MODE = 0>
+template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta>
 __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
-    constexpr int SA_W = 4 * R::ABITS;
-    constexpr int SB_W = R::BBITS ? 4 * R::BBITS : 4;
-    constexpr int SC_W = 4 * R::CBITS;
+    static_assert((BPC * R::ABITS) % 128 == 0 && (BPC * R::BBITS) % 128 == 0 && (BPC * R::CBITS) % 128 == 0,
+                  "CTA stream slices must be whole 16-byte units (and A whole AES blocks)");
+    constexpr int SA_W = BPC * R::ABITS / 32;
+    constexpr int SB_W = R::BBITS ? BPC * R::BBITS / 32 : 4;
+    constexpr int SC_W = BPC * R::CBITS / 32;
     __shared__ __align__(16) uint32_t sa[SA_W];
     __shared__ __align__(16) uint32_t sb[SB_W];
     __shared__ __align__(16) uint32_t sc[SC_W];
@@ -355,16 +365,16 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
     __shared__ unsigned int s_bad;
 
     const int tid = threadIdx.x;
-    const uint64_t blk = cta * kBlocksPerCta + tid;
-    const uint64_t a0 = cta * 16ull * R::ABITS, c0 = cta * 16ull * R::CBITS;
+    const uint64_t blk = cta * BPC + tid;
+    const uint64_t a0 = cta * (BPC / 8ull) * R::ABITS, c0 = cta * (BPC / 8ull) * R::CBITS;
     const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
     if (tid == 0) { s_first = ~0ull; s_bad = 0; }
-    copy_g2s(sa, p.a + a0, alen, SA_W * 4, tid);
+    copy_g2s<BPC>(sa, p.a + a0, alen, SA_W * 4, tid);
     if (R::BBITS) {
-        const uint64_t b0 = cta * 16ull * R::BBITS;
-        copy_g2s(sb, p.b + b0, min((uint64_t)SB_W * 4, p.b_bytes - b0), SB_W * 4, tid);
+        const uint64_t b0 = cta * (BPC / 8ull) * R::BBITS;
+        copy_g2s<BPC>(sb, p.b + b0, min((uint64_t)SB_W * 4, p.b_bytes - b0), SB_W * 4, tid);
     }
-    copy_g2s(sc, p.c + c0, min((uint64_t)SC_W * 4, p.c_bytes - c0), SC_W * 4, tid);
+    copy_g2s<BPC>(sc, p.c + c0, min((uint64_t)SC_W * 4, p.c_bytes - c0), SC_W * 4, tid);
     __syncthreads();
 
     // C needs only B' (C19): its SHA-512 unmask runs before the keystream is needed
@@ -378,7 +388,7 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         if (MASK && R::BBITS) mask_c<R::BW, R::BBYTES>(p, gb, B, C);          // C from B'
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");                      // keystream kernel complete
-    xor_g2s(sa, p.ks + a0, alen, tid);                                       // A' -> A
+    xor_g2s<BPC>(sa, p.ks + a0, alen, tid);                                       // A' -> A
     __syncthreads();                                                         // plain A ready
 
     bool bad = false;

@@ -35,16 +35,27 @@ namespace se {
 
 // ---------------------------------------------------------------- kernels
 
+// Blocks (threads) per CTA of the single-file kernels.  Finer CTAs spread
+// a file more evenly over the SMs (C2: 1536 CTAs of 128 leave each SM 10 or 11
+// of them, ~10 % idle at the end; 64-block CTAs halve that).  The CTA's
+// stream slices must stay whole 16-byte units: L = 3 (155-bit B records)
+// keeps 128.
+#ifndef SE_BPC
+#define SE_BPC 128
+#endif
+template <int L>
+__host__ __device__ constexpr int bpc_for() { return L == 3 ? kBlocksPerCta : SE_BPC; }
+
 template <int L, bool MASK>
-__global__ void __launch_bounds__(kBlocksPerCta, MASK ? SE_MIN_CTAS : SE_MIN_CTAS_PLAIN_P)
+__global__ void __launch_bounds__(bpc_for<L>(), (MASK ? SE_MIN_CTAS : SE_MIN_CTAS_PLAIN_P) * kBlocksPerCta / bpc_for<L>())
 k_protect_block8(const __grid_constant__ FusedParams p) {
-    protect_cta<L, MASK, 0>(p, blockIdx.x);
+    protect_cta<L, MASK, 0, bpc_for<L>()>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
-__global__ void __launch_bounds__(kBlocksPerCta, MASK ? SE_MIN_CTAS : SE_MIN_CTAS_PLAIN_R)
+__global__ void __launch_bounds__(bpc_for<L>(), (MASK ? SE_MIN_CTAS : SE_MIN_CTAS_PLAIN_R) * kBlocksPerCta / bpc_for<L>())
 k_recover_block8(const __grid_constant__ FusedParams p) {
-    recover_cta<L, MASK, 0>(p, blockIdx.x);
+    recover_cta<L, MASK, 0, bpc_for<L>()>(p, blockIdx.x);
 }
 
 // Many independent files in one launch (C5; SURVEY §8.6 "sharded by file").
@@ -185,19 +196,21 @@ void launch_pdl(void (*kernel)(P), unsigned grid, unsigned block, cudaStream_t s
 template void launch_pdl<FusedParams>(void (*)(FusedParams), unsigned, unsigned, cudaStream_t, const FusedParams&);
 template void launch_pdl<DctParams>(void (*)(DctParams), unsigned, unsigned, cudaStream_t, const DctParams&);
 
-static unsigned grid_for(uint64_t n_blocks) {
-    return (unsigned)((n_blocks + kBlocksPerCta - 1) / kBlocksPerCta);
+static unsigned grid_for(uint64_t n_blocks, int bpc = kBlocksPerCta) {
+    return (unsigned)((n_blocks + bpc - 1) / bpc);
 }
 
 template <int L>
 static void protect_l(const FusedParams& p, bool mask, cudaStream_t s) {
-    if (mask) launch_pdl(k_protect_block8<L, true>, grid_for(p.n_blocks), kBlocksPerCta, s, p);
-    else launch_pdl(k_protect_block8<L, false>, grid_for(p.n_blocks), kBlocksPerCta, s, p);
+    constexpr int B = bpc_for<L>();
+    if (mask) launch_pdl(k_protect_block8<L, true>, grid_for(p.n_blocks, B), B, s, p);
+    else launch_pdl(k_protect_block8<L, false>, grid_for(p.n_blocks, B), B, s, p);
 }
 template <int L>
 static void recover_l(const FusedParams& p, bool mask, cudaStream_t s) {
-    if (mask) launch_pdl(k_recover_block8<L, true>, grid_for(p.n_blocks), kBlocksPerCta, s, p);
-    else launch_pdl(k_recover_block8<L, false>, grid_for(p.n_blocks), kBlocksPerCta, s, p);
+    constexpr int B = bpc_for<L>();
+    if (mask) launch_pdl(k_recover_block8<L, true>, grid_for(p.n_blocks, B), B, s, p);
+    else launch_pdl(k_recover_block8<L, false>, grid_for(p.n_blocks, B), B, s, p);
 }
 
 int launch_protect_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream) {
