@@ -374,7 +374,46 @@ def run_multi(args):
     torch.cuda.set_device(dev)
     se.lib()
     key, L = synth.KEY, 2
-    if args.config == 4:
+    if args.config == 4 and args.full:
+        # C4-FULL (row a11 with row e): whole-matrix DWT, W = 32768, stripes of
+        # block rows protected from their rows + 2(2^L-1) halo rows and recovered
+        # from their fragments + one halo block row per side
+        c = synth.CONFIGS[4]
+        n, W = c["n_bytes"], 32768
+        plan = shard.plan_full_stripes(n, W, L, world)[rank]
+        full = synth.config_input(4)
+        iv = synth.iv_for(4)
+        src = torch.from_numpy(np.ascontiguousarray(full[plan["src_byte_begin"]: plan["src_byte_end"]])).to(dev)
+        rec_src0 = max(0, plan["rec_row0"] - 2 * ((1 << L) - 1))
+        rec_src1 = min(n, (plan["rec_row0"] + plan["rec_rows"] + 2 * ((1 << L) - 1)) * W)
+        ext_in = torch.from_numpy(np.ascontiguousarray(full[rec_src0 * W: rec_src1])).to(dev)
+        x = torch.from_numpy(np.ascontiguousarray(full[plan["byte_begin"]: plan["byte_end"]])).to(dev)
+        del full
+        # the fragments of the recover window (untimed setup: in a deployment they are read from storage)
+        ext = se.fragment_protect_stripe(ext_in, n, W, L, key, iv, plan["rec_row0"],
+                                         plan["rec_row0"] + plan["rec_rows"], rec_src0)
+        del ext_in
+        nb = plan["n_blocks"]
+        lay = se.fragment_layout(n, W, L, se.MODE_FULL)
+        frag = tuple(se._empty(-(-nb * lay[k] // 8), dev) for k in ("a_bits", "b_bits", "c_bits"))
+        out = se._empty(x.numel(), dev)
+        rep = torch.empty(2, dtype=torch.int64, device=dev)
+
+        def protect():
+            se.fragment_protect_stripe(src, n, W, L, key, iv, plan["row_begin"], plan["row_end"], plan["src_row0"],
+                                       out=frag)
+
+        def recover():
+            se.fragment_recover_stripe(*ext, n, W, L, key, iv, plan["row_begin"], plan["row_end"], plan["rec_row0"],
+                                       plan["rec_rows"], out=out, report=rep)
+
+        def check():
+            return torch.equal(out, x) and rep.cpu().tolist() == [-1, 0]
+        total_bytes, n_blocks_local = n, nb
+        workload = (f"C4-FULL 1 GiB W=32768 whole-matrix DWT L=2: {world} row stripes with "
+                    f"{2 * ((1 << L) - 1)} halo rows per side (protect) / 1 halo block row (recover)")
+        extra = {"stripe_rows": plan["row_end"] - plan["row_begin"], "mode_detail": "FULL"}
+    elif args.config == 4:
         c = synth.CONFIGS[4]
         n, W = c["n_bytes"], c["width"]
         plan = shard.plan_stripes(n, W, L, world)[rank]
@@ -468,7 +507,8 @@ def run_multi(args):
         "value": round(total_bytes / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": dict({"workload": workload, "n_bytes_total": total_bytes, "levels": L, "mode": "BLOCK8",
+        "config": dict({"workload": workload, "n_bytes_total": total_bytes, "levels": L,
+                        "mode": "FULL" if getattr(args, "full", False) else "BLOCK8",
                         "parallelism": f"dp{world} ({'row stripes' if args.config == 4 else 'by file'})",
                         "l2": "flushed between steps"}, **extra),
         "roofline": {"bound": "alu", "kernel": "k_protect/k_recover (rank 0 slowest)", "achieved": round(achieved, 1),
@@ -794,6 +834,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--stripes", action="store_true", help="C4: split the one file into per-rank row stripes")
+    ap.add_argument("--full", action="store_true", help="C4 stripes in FULL mode (whole-matrix DWT, halo rows)")
     ap.add_argument("--impl", default="se", choices=["se", "reference"])
     ap.add_argument("--plain", action="store_true", help="PUBLIC_PLAIN measurement mode (C26)")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of sustained warm-up load")

@@ -154,6 +154,37 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
                           const void* h_a, const void* h_b, const void* h_c, void* h_out,
                           se_report* h_report, uint64_t chunk_bytes, uint32_t n_streams);
 
+/* ---- FULL-mode row stripes with halo rows (row e for a11) ---------------
+ * A FULL-mode file (whole-matrix DWT) split into stripes of block rows for
+ * several GPUs.  Lifting reaches 2(2^L - 1) input rows beyond a stripe
+ * (layout.halo_rows: 6 at L = 2), so each stripe is protected from its rows
+ * plus that many halo rows per side, and recovered from the fragments of its
+ * block rows plus ceil(halo_rows / 8) halo block rows per side.  Concatenated
+ * in row order, the stripes' streams and bytes equal the whole-file ones.
+ *   g          the WHOLE file (mode SE_MODE_FULL; block_offset of its block 0)
+ *   row_begin, row_end   the stripe's rows, multiples of 8 (row_end may be R);
+ *              row_begin * W/8 * bits must be a multiple of 8 for every
+ *              stream and of 128 for A (any multiple of 128 blocks is)
+ *   src_row0, src_rows   the rows present at the source pointer:
+ *              protect: input bytes of rows [src_row0, src_row0 + src_rows),
+ *              covering [row_begin - halo, row_end + halo] clipped to [0, R);
+ *              recover: fragments of block rows [src_row0/8, (src_row0 +
+ *              src_rows)/8) (multiples of 8, src_row0 aligned like row_begin),
+ *              covering the halo block rows.
+ * Outputs: protect writes the stripe's blocks' records (stream slices at
+ * byte offset first_block * bits / 8 of the whole-file streams); recover
+ * writes the stripe's bytes (row_begin * W onwards, clipped at n_bytes) and
+ * reports bad blocks with stripe-local indices.  SE_EINVAL on a bad window. */
+typedef struct {
+    uint64_t row_begin, row_end, src_row0, src_rows;
+} se_stripe;
+
+int fragment_protect_stripe(const se_geom* g, const se_stripe* s, const uint8_t key[16], const uint8_t iv[16],
+                            const void* d_in, void* d_a, void* d_b, void* d_c, void* stream);
+int fragment_recover_stripe(const se_geom* g, const se_stripe* s, const uint8_t key[16], const uint8_t iv[16],
+                            const void* d_a, const void* d_b, const void* d_c, void* d_out,
+                            se_report* d_report, void* stream);
+
 /* ---- transform only: rows a1-a4 / a11 ------------------------------------
  * d_coef: R x W int16 (R = layout.rows).  BLOCK8: block (br, bc) coefficient
  * (i, j) at [(8br+i)*W + 8bc+j], dyadic quadrants inside each block (LL top-

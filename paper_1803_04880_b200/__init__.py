@@ -96,7 +96,13 @@ SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_
            "se_stats_accumulate", "se_strerror", "se_launch_count",
            "dct_layout", "dct_protect", "dct_recover", "dct_select", "dct8_forward", "dct8_inverse",
            "se_container_streams", "se_container_size", "se_container_pack", "se_container_open",
-           "se_disperse_plan", "se_storage_footprint", "se_sha256"]
+           "se_disperse_plan", "se_storage_footprint", "se_sha256",
+           "fragment_protect_stripe", "fragment_recover_stripe"]
+
+
+class Stripe(C.Structure):
+    _fields_ = [("row_begin", C.c_uint64), ("row_end", C.c_uint64), ("src_row0", C.c_uint64),
+                ("src_rows", C.c_uint64)]
 
 
 class ContainerInfo(C.Structure):
@@ -160,6 +166,9 @@ def lib():
         L.se_storage_footprint.argtypes = [cip, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.se_sha256.argtypes = [vp, C.c_uint64, vp]
         L.se_sha256.restype = None
+        sp = C.POINTER(Stripe)
+        L.fragment_protect_stripe.argtypes = [gp, sp, u8p, u8p, vp, vp, vp, vp, vp]
+        L.fragment_recover_stripe.argtypes = [gp, sp, u8p, u8p, vp, vp, vp, vp, vp, vp]
         L.se_strerror.argtypes = [C.c_int]
         L.se_strerror.restype = C.c_char_p
         L.se_launch_count.argtypes = [C.c_int]
@@ -238,6 +247,43 @@ def fragment_recover(a, b, c, n_bytes: int, width: int, levels: int, key, iv, mo
     _check(lib().fragment_recover(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(a),
                                   _ptr(b) if b is not None and b.numel() else None, _ptr(c), _ptr(o),
                                   _ptr(rep), _stream(stream)), "fragment_recover")
+    return o, rep
+
+
+def fragment_protect_stripe(src, n_bytes: int, width: int, levels: int, key, iv, row_begin: int, row_end: int,
+                            src_row0: int, flags: int = 0, block_offset: int = 0, out=None, stream=None):
+    """FULL-mode stripe: `src` = input bytes of rows [src_row0, ...) (the stripe
+    plus halo rows).  Returns the stripe's (A', B', C') slices (device)."""
+    lay = fragment_layout(n_bytes, width, levels, MODE_FULL, flags, block_offset)
+    nb = (row_end - row_begin) // 8 * (width // 8)
+    sizes = [-(-nb * lay[k] // 8) for k in ("a_bits", "b_bits", "c_bits")]
+    a, b, c = out if out is not None else tuple(_empty(n, src.device) for n in sizes)
+    src_rows = -(-src.numel() // width)
+    st = Stripe(int(row_begin), int(row_end), int(src_row0), int(min(src_rows, lay["rows"] - src_row0)))
+    g = _geom(n_bytes, width, levels, MODE_FULL, flags, block_offset)
+    _check(lib().fragment_protect_stripe(C.byref(g), C.byref(st), _bytes16(key, "key"), _bytes16(iv, "iv"),
+                                         _ptr(src), _ptr(a), _ptr(b) if b.numel() else None, _ptr(c),
+                                         _stream(stream)),
+           "fragment_protect_stripe")
+    return a, b, c
+
+
+def fragment_recover_stripe(a, b, c, n_bytes: int, width: int, levels: int, key, iv, row_begin: int, row_end: int,
+                            src_row0: int, src_rows: int, flags: int = 0, block_offset: int = 0, out=None,
+                            report=None, stream=None):
+    """FULL-mode stripe recovery from the fragments of block rows [src_row0/8,
+    (src_row0+src_rows)/8).  Returns (stripe bytes, report[2])."""
+    import torch
+    dev = a.device
+    nbytes = max(0, min(n_bytes, row_end * width) - row_begin * width)
+    o = out if out is not None else _empty(nbytes, dev)
+    rep = report if report is not None else torch.empty(2, dtype=torch.int64, device=dev)
+    st = Stripe(int(row_begin), int(row_end), int(src_row0), int(src_rows))
+    g = _geom(n_bytes, width, levels, MODE_FULL, flags, block_offset)
+    _check(lib().fragment_recover_stripe(C.byref(g), C.byref(st), _bytes16(key, "key"), _bytes16(iv, "iv"),
+                                         _ptr(a), _ptr(b) if b is not None and b.numel() else None, _ptr(c),
+                                         _ptr(o), _ptr(rep), _stream(stream)),
+           "fragment_recover_stripe")
     return o, rep
 
 

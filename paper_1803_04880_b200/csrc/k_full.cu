@@ -38,8 +38,8 @@ struct FullTile {
 //   DIR 0: rows (neighbours at j +- s), DIR 1: columns (i +- s)
 //   STEP 0: predict (odd level positions), 1: update (even positions),
 //   INV: the inverse step (undo update = STEP 1, undo predict = STEP 0)
-template <int L, int DIR, int STEP, bool INV>
-__device__ __forceinline__ void lift_sweep(int* g, int s, int64_t R0, int64_t C0, int64_t R, int64_t W) {
+template <int L, int DIR, int STEP, bool INV, int s>
+__device__ __forceinline__ void lift_sweep(int* g, int64_t R0, int64_t C0, int64_t R, int64_t W) {
     using T = FullTile<L>;
     // positions: along DIR, index ≡ (STEP == 0 ? s : 0) mod 2s; across DIR, ≡ 0 mod s
     const int nA = DIR == 0 ? T::SR / s : T::SC / s;             // across
@@ -49,8 +49,10 @@ __device__ __forceinline__ void lift_sweep(int* g, int s, int64_t R0, int64_t C0
     const int64_t Oa = DIR == 0 ? R0 : C0, Na = DIR == 0 ? R : W;
     const int span = DIR == 0 ? T::SC : T::SR;
     for (int idx = threadIdx.x; idx < nA * nL; idx += blockDim.x) {
-        const int a = (idx / nL) * s;                 // across coordinate
-        const int k = (idx % nL) * 2 * s + (STEP == 0 ? s : 0);   // along coordinate
+        // consecutive threads: along a row (DIR 0) or across columns (DIR 1),
+        // so a warp's shared-memory accesses fall in distinct banks
+        const int a = (DIR == 0 ? idx / nL : idx % nA) * s;                        // across coordinate
+        const int k = (DIR == 0 ? idx % nL : idx / nA) * 2 * s + (STEP == 0 ? s : 0);   // along coordinate
         const int64_t ga = Oa + a, gk = O + k;
         if (ga < 0 || ga >= Na || gk < 0 || gk >= N) continue;    // outside the matrix
         int lo = k - s, hi = k + s;
@@ -65,6 +67,31 @@ __device__ __forceinline__ void lift_sweep(int* g, int s, int64_t R0, int64_t C0
         const int nb = at(lo) + at(hi);
         if (STEP == 0) x = INV ? x + (nb >> 1) : x - (nb >> 1);            // Eq. 5.1
         else x = INV ? x - ((nb + 2) >> 2) : x + ((nb + 2) >> 2);          // Eq. 5.2 (+)
+    }
+}
+
+// All levels, forward (l = 1..L) / inverse (l = L..1); the sample spacing
+// s = 2^(l-1) is a compile-time constant so the sweep index arithmetic folds.
+template <int L, int l>
+__device__ __forceinline__ void fwd_levels(int* g, int64_t R0, int64_t C0, int64_t R, int64_t W) {
+    if constexpr (l <= L) {
+        constexpr int s = 1 << (l - 1);
+        lift_sweep<L, 0, 0, false, s>(g, R0, C0, R, W); __syncthreads();
+        lift_sweep<L, 0, 1, false, s>(g, R0, C0, R, W); __syncthreads();
+        lift_sweep<L, 1, 0, false, s>(g, R0, C0, R, W); __syncthreads();
+        lift_sweep<L, 1, 1, false, s>(g, R0, C0, R, W); __syncthreads();
+        fwd_levels<L, l + 1>(g, R0, C0, R, W);
+    }
+}
+template <int L, int l>
+__device__ __forceinline__ void inv_levels(int* g, int64_t R0, int64_t C0, int64_t R, int64_t W) {
+    if constexpr (l >= 1) {
+        constexpr int s = 1 << (l - 1);
+        lift_sweep<L, 1, 1, true, s>(g, R0, C0, R, W); __syncthreads();
+        lift_sweep<L, 1, 0, true, s>(g, R0, C0, R, W); __syncthreads();
+        lift_sweep<L, 0, 1, true, s>(g, R0, C0, R, W); __syncthreads();
+        lift_sweep<L, 0, 0, true, s>(g, R0, C0, R, W); __syncthreads();
+        inv_levels<L, l - 1>(g, R0, C0, R, W);
     }
 }
 
@@ -84,36 +111,36 @@ __global__ void __launch_bounds__(kFullThreads) k_dwt_full_fwd(const __grid_cons
     using T = FullTile<L>;
     extern __shared__ int g[];
     const int64_t W = p.width, R = p.rows;
-    const int64_t tr0 = (int64_t)blockIdx.y * kTileR, tc0 = (int64_t)blockIdx.x * kTileC;
+    const int64_t row0 = (int64_t)p.row0, row_end = min((int64_t)(p.row0 + p.rows_out), R);
+    const int64_t s0 = (int64_t)p.src_row0, s1 = (int64_t)(p.src_row0 + p.src_rows);
+    const int64_t tr0 = row0 + (int64_t)blockIdx.y * kTileR, tc0 = (int64_t)blockIdx.x * kTileC;
     const int64_t R0 = tr0 - T::H, C0 = tc0 - T::H;
-    // load tile + halo, centered (C8), zero fill past n (C18)
+    // load tile + halo, centered (C8), zero fill past n (C18); rows the caller
+    // did not provide (beyond a stripe's halo) only feed outputs not written
     for (int idx = threadIdx.x; idx < T::SR * T::SC; idx += blockDim.x) {
         const int i = idx / T::SC, j = idx % T::SC;
         const int64_t gr = R0 + i, gc = C0 + j;
         int v = 0;
         if (gr >= 0 && gr < R && gc >= 0 && gc < W) {
             const uint64_t o = (uint64_t)gr * W + gc;
-            v = (o < p.n_bytes ? (int)p.in[o] : 0) - 128;
+            if (o >= p.n_bytes) v = -128;                                   // zero fill (C18)
+            else if (gr >= s0 && gr < s1) v = (int)p.in[(uint64_t)(gr - s0) * W + gc] - 128;
         }
         g[idx] = v;
     }
     __syncthreads();
-    for (int l = 1, s = 1; l <= L; ++l, s *= 2) {
-        lift_sweep<L, 0, 0, false>(g, s, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 0, 1, false>(g, s, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 1, 0, false>(g, s, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 1, 1, false>(g, s, R0, C0, R, W); __syncthreads();
-    }
+    fwd_levels<L, 1>(g, R0, C0, R, W);
     // write the tile interior band by band in Mallat layout
     for_each_band<L>([&](int l, int band) {
         const int hr = band >= 2, hc = band & 1, half = 1 << (l - 1);
         const int br = kTileR >> l, bc = kTileC >> l;        // band rectangle of this tile
-        const int64_t mr0 = (hr ? (R >> l) : 0) + (tr0 >> l), mc0 = (hc ? (W >> l) : 0) + (tc0 >> l);
+        const int64_t mr0 = (hr ? ((int64_t)p.rows_out >> l) : 0) + ((tr0 - row0) >> l);   // local Mallat rows
+        const int64_t mc0 = (hc ? (W >> l) : 0) + (tc0 >> l);
         for (int idx = threadIdx.x; idx < br * bc; idx += blockDim.x) {
             const int bi = idx / bc, bj = idx % bc;
             const int64_t gr = tr0 + ((int64_t)bi << l) + (hr ? half : 0);
             const int64_t gc = tc0 + ((int64_t)bj << l) + (hc ? half : 0);
-            if (gr >= R || gc >= W) continue;
+            if (gr >= row_end || gc >= W) continue;
             const int v = g[(gr - R0) * T::SC + (gc - C0)];
             p.coef[(uint64_t)(mr0 + bi) * W + (mc0 + bj)] = (int16_t)v;
         }
@@ -127,7 +154,8 @@ __global__ void __launch_bounds__(kFullThreads) k_dwt_full_inv(const __grid_cons
     extern __shared__ int g[];
     __shared__ unsigned int s_badmask[(kTileR / 8) * (kTileC / 8) / 32];
     const int64_t W = p.width, R = p.rows;
-    const int64_t tr0 = (int64_t)blockIdx.y * kTileR, tc0 = (int64_t)blockIdx.x * kTileC;
+    const int64_t row0 = (int64_t)p.row0, row_end = min((int64_t)(p.row0 + p.rows_out), R);
+    const int64_t tr0 = row0 + (int64_t)blockIdx.y * kTileR, tc0 = (int64_t)blockIdx.x * kTileC;
     const int64_t R0 = tr0 - T::H, C0 = tc0 - T::H;
     for (int i = threadIdx.x; i < (kTileR / 8) * (kTileC / 8) / 32; i += blockDim.x) s_badmask[i] = 0;
     // gather tile + halo from the Mallat layout into the interleaved grid, band by band
@@ -137,34 +165,32 @@ __global__ void __launch_bounds__(kFullThreads) k_dwt_full_inv(const __grid_cons
         const int64_t b_r0 = (R0 - (hr ? half : 0) + ((1 << l) - 1)) >> l;   // ceil, R0 may be negative
         const int64_t b_c0 = (C0 - (hc ? half : 0) + ((1 << l) - 1)) >> l;
         const int nbr = (T::SR >> l) + 1, nbc = (T::SC >> l) + 1;
+        // the source window holds band rows [src_row0 >> l, (src_row0 + src_rows) >> l)
+        const int64_t sb0 = (int64_t)p.src_row0 >> l, sbn = (int64_t)p.src_rows >> l;
         for (int idx = threadIdx.x; idx < nbr * nbc; idx += blockDim.x) {
             const int64_t bi = b_r0 + idx / nbc, bj = b_c0 + idx % nbc;
             if (bi < 0 || bj < 0 || bi >= (R >> l) || bj >= (W >> l)) continue;
+            if (bi < sb0 || bi >= sb0 + sbn) continue;            // beyond a stripe's halo: unused
             const int64_t gr = (bi << l) + (hr ? half : 0), gc = (bj << l) + (hc ? half : 0);
             if (gr < R0 || gr >= R0 + T::SR || gc < C0 || gc >= C0 + T::SC) continue;
-            const int64_t mr = (hr ? (R >> l) : 0) + bi, mc = (hc ? (W >> l) : 0) + bj;
+            const int64_t mr = (hr ? sbn : 0) + (bi - sb0), mc = (hc ? (W >> l) : 0) + bj;
             g[(gr - R0) * T::SC + (gc - C0)] = p.coef[(uint64_t)mr * W + mc];
         }
     });
     __syncthreads();
-    for (int l = L, s = 1 << (L - 1); l >= 1; --l, s /= 2) {
-        lift_sweep<L, 1, 1, true>(g, s, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 1, 0, true>(g, s, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 0, 1, true>(g, s, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 0, 0, true>(g, s, R0, C0, R, W); __syncthreads();
-    }
+    inv_levels<L, L>(g, R0, C0, R, W);
     // write bytes (+128), flag footprints with samples outside [0, 255]
     for (int idx = threadIdx.x; idx < kTileR * kTileC; idx += blockDim.x) {
         const int i = idx / kTileC, j = idx % kTileC;
         const int64_t gr = tr0 + i, gc = tc0 + j;
-        if (gr >= R || gc >= W) continue;
+        if (gr >= row_end || gc >= W) continue;
         const int v = g[(i + T::H) * T::SC + (j + T::H)] + 128;
         if (v & ~0xff) {
             const int fp = (i / 8) * (kTileC / 8) + (j / 8);
             atomicOr(&s_badmask[fp / 32], 1u << (fp % 32));
         }
         const uint64_t o = (uint64_t)gr * W + gc;
-        if (o < p.n_bytes) p.out[o] = (uint8_t)v;
+        if (o < p.n_bytes) p.out[(uint64_t)(gr - row0) * W + gc] = (uint8_t)v;
     }
     if (report) {
         __syncthreads();
@@ -172,8 +198,8 @@ __global__ void __launch_bounds__(kFullThreads) k_dwt_full_inv(const __grid_cons
         for (int fp = threadIdx.x; fp < nfp; fp += blockDim.x) {
             if (s_badmask[fp / 32] & (1u << (fp % 32))) {
                 const int64_t fbr = tr0 / 8 + fp / (kTileC / 8), fbc = tc0 / 8 + fp % (kTileC / 8);
-                if (fbr < R / 8 && fbc < W / 8) {
-                    const unsigned long long b = (unsigned long long)(fbr * (W / 8) + fbc);
+                if (fbr < row_end / 8 && fbc < W / 8) {                   // block index local to row0
+                    const unsigned long long b = (unsigned long long)((fbr - row0 / 8) * (W / 8) + fbc);
                     atomicMin(reinterpret_cast<unsigned long long*>(&report->first_bad_block), b);
                     atomicAdd(reinterpret_cast<unsigned long long*>(&report->bad_blocks), 1ull);
                 }
@@ -198,7 +224,7 @@ template <int L>
 static int full_fwd_l(const DwtParams& p, cudaStream_t s) {
     using T = FullTile<L>;
     cudaFuncSetAttribute(k_dwt_full_fwd<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
-    const dim3 grid((unsigned)((p.width + kTileC - 1) / kTileC), (unsigned)((p.rows + kTileR - 1) / kTileR));
+    const dim3 grid((unsigned)((p.width + kTileC - 1) / kTileC), (unsigned)((p.rows_out + kTileR - 1) / kTileR));
     k_dwt_full_fwd<L><<<grid, kFullThreads, T::smem, s>>>(p);
     return (int)cudaGetLastError();
 }
@@ -207,7 +233,7 @@ template <int L>
 static int full_inv_l(const DwtParams& p, se_report* rep, cudaStream_t s) {
     using T = FullTile<L>;
     cudaFuncSetAttribute(k_dwt_full_inv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
-    const dim3 grid((unsigned)((p.width + kTileC - 1) / kTileC), (unsigned)((p.rows + kTileR - 1) / kTileR));
+    const dim3 grid((unsigned)((p.width + kTileC - 1) / kTileC), (unsigned)((p.rows_out + kTileR - 1) / kTileR));
     k_dwt_full_inv<L><<<grid, kFullThreads, T::smem, s>>>(p, rep);
     return (int)cudaGetLastError();
 }

@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "se_internal.h"
 #include "../../include/se_container.h"
 #include "tables.h"
@@ -207,6 +209,7 @@ static DwtParams dwt_params(const se_geom* g, const se_layout& lay) {
     memset(&p, 0, sizeof p);
     p.n_bytes = g->n_bytes; p.n_blocks = lay.n_blocks;
     p.width = g->width; p.bpr = g->width / 8; p.rows = (uint32_t)lay.rows; p.one = 1;
+    p.row0 = 0; p.rows_out = lay.rows; p.src_row0 = 0; p.src_rows = lay.rows;   // whole matrix
     return p;
 }
 
@@ -328,6 +331,125 @@ extern "C" {
 int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
                      const void* d_b, const void* d_c, void* d_out, se_report* d_report, void* stream) {
     return recover_impl(g, key, iv, d_a, d_b, d_c, d_out, d_report, nullptr, false, stream);
+}
+
+// ---------------------------------------------------------------- FULL-mode stripes (row e for a11)
+
+static bool stripe_aligned(const se_layout& lay, uint64_t blocks_before) {
+    const uint64_t bits[3] = {lay.a_bits, lay.b_bits, lay.c_bits};
+    for (uint64_t b : bits)
+        if ((blocks_before * b) % 8) return false;
+    return (blocks_before * lay.a_bits) % 128 == 0;                         // CTR start whole AES blocks
+}
+
+static int stripe_checks(const se_geom* g, const se_stripe* st, const uint8_t* key, const uint8_t* iv,
+                         se_layout& lay, bool recover) {
+    int rc = fragment_layout(g, &lay);
+    if (rc) return rc;
+    if (!st || !key || !iv || g->mode != SE_MODE_FULL || g->n_bytes == 0) return SE_EINVAL;
+    if ((g->block_offset * lay.a_bits) % 128) return SE_EINVAL;
+    const uint64_t R = lay.rows, bpr = g->width / 8;
+    if (st->row_begin % 8 || st->row_end % 8 || st->row_begin >= st->row_end || st->row_end > R) return SE_EINVAL;
+    const uint64_t s0 = st->src_row0, s1 = st->src_row0 + st->src_rows;
+    if (s1 > R || s0 >= s1) return SE_EINVAL;
+    // (protect windows may end before need1 only where the file has no bytes)
+    // halo: input rows (protect) or whole halo block rows of fragments (recover)
+    const uint64_t halo = recover ? (lay.halo_rows + 7) / 8 * 8 : lay.halo_rows;
+    const uint64_t need0 = st->row_begin >= halo ? st->row_begin - halo : 0;
+    // protect: rows past the file's last byte read as zero (C18) and need not be present
+    const uint64_t data_rows = recover ? R : (g->n_bytes + g->width - 1) / g->width;
+    const uint64_t need1 = std::min<uint64_t>(std::min<uint64_t>(R, data_rows), st->row_end + halo);
+    if (s0 > need0 || s1 < need1) return SE_EINVAL;
+    if (!stripe_aligned(lay, st->row_begin / 8 * bpr)) return SE_EINVAL;
+    if (recover && (s0 % 8 || s1 % 8 || !stripe_aligned(lay, s0 / 8 * bpr))) return SE_EINVAL;
+    return SE_OK;
+}
+
+// FusedParams for the blocks of rows [r0, r1) of a FULL file (local Mallat of those rows)
+static void stripe_fused(FusedParams& p, const se_geom* g, const se_layout& lay, const uint8_t key[16],
+                         const uint8_t iv[16], uint64_t r0, uint64_t r1) {
+    fill_fused(p, g, lay, key, iv);
+    const uint64_t bpr = g->width / 8, nb = (r1 - r0) / 8 * bpr;
+    p.n_blocks = nb;
+    p.block_offset = g->block_offset + r0 / 8 * bpr;
+    p.a_bytes = (nb * lay.a_bits + 7) / 8;
+    p.b_bytes = (nb * lay.b_bits + 7) / 8;
+    p.c_bytes = (nb * lay.c_bits + 7) / 8;
+    p.rows = r1 - r0;
+    ctr_base(iv, p.block_offset * lay.a_bits / 128, p.ctr);
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int fragment_protect_stripe(const se_geom* g, const se_stripe* st, const uint8_t key[16], const uint8_t iv[16],
+                            const void* d_in, void* d_a, void* d_b, void* d_c, void* stream) {
+    se_layout lay;
+    int rc = stripe_checks(g, st, key, iv, lay, false);
+    if (rc) return rc;
+    if (!d_in || !d_a || !d_c || (lay.b_bits && !d_b)) return SE_EINVAL;
+    if (!aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
+    FusedParams p;
+    stripe_fused(p, g, lay, key, iv, st->row_begin, st->row_end);
+    p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
+    keep_pool();
+    cudaStream_t s = (cudaStream_t)stream;
+    void* ws = nullptr;
+    if (cudaMallocAsync(&ws, (st->row_end - st->row_begin) * g->width * sizeof(int16_t), s) != cudaSuccess)
+        return SE_ECUDA;
+    DwtParams dp = dwt_params(g, lay);
+    dp.in = (const uint8_t*)d_in; dp.coef = (int16_t*)ws;
+    dp.row0 = st->row_begin; dp.rows_out = st->row_end - st->row_begin;
+    dp.src_row0 = st->src_row0; dp.src_rows = st->src_rows;
+    p.ws = (int16_t*)ws;
+    const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
+    int e = launch_dwt_full_fwd(dp, g->levels, stream);
+    if (!e) e = launch_keystream(p, p.a, p.a_bytes, stream);
+    if (!e) e = launch_protect_full(p, g->levels, mask, stream);
+    cudaFreeAsync(ws, s);
+    return e ? SE_ECUDA : SE_OK;
+}
+
+int fragment_recover_stripe(const se_geom* g, const se_stripe* st, const uint8_t key[16], const uint8_t iv[16],
+                            const void* d_a, const void* d_b, const void* d_c, void* d_out, se_report* d_report,
+                            void* stream) {
+    se_layout lay;
+    int rc = stripe_checks(g, st, key, iv, lay, true);
+    if (rc) return rc;
+    if (!d_a || !d_c || !d_out || (lay.b_bits && !d_b)) return SE_EINVAL;
+    if (!aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (d_report) {
+        if (cudaMemsetAsync(&d_report->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
+            cudaMemsetAsync(&d_report->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
+            return SE_ECUDA;
+    }
+    const uint64_t e0 = st->src_row0, e1 = st->src_row0 + st->src_rows;
+    FusedParams p;
+    stripe_fused(p, g, lay, key, iv, e0, e1);                              // the halo-extended block rows
+    p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
+    keep_pool();
+    void* ks = nullptr;
+    void* ws = nullptr;
+    if (cudaMallocAsync(&ks, p.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
+    if (cudaMallocAsync(&ws, (e1 - e0) * g->width * sizeof(int16_t), s) != cudaSuccess) {
+        cudaFreeAsync(ks, s);
+        return SE_ECUDA;
+    }
+    p.ks = (const uint8_t*)ks;
+    p.ws = (int16_t*)ws;
+    const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
+    DwtParams dp = dwt_params(g, lay);
+    dp.out = (uint8_t*)d_out; dp.coef = (int16_t*)ws;
+    dp.row0 = st->row_begin; dp.rows_out = st->row_end - st->row_begin;
+    dp.src_row0 = e0; dp.src_rows = e1 - e0;
+    int e = launch_keystream(p, (uint8_t*)ks, p.a_bytes, stream);
+    if (!e) e = launch_recover_full(p, g->levels, mask, stream);             // unmask + scatter (halo too)
+    if (!e) e = launch_dwt_full_inv(dp, g->levels, d_report, stream);        // the stripe's rows
+    cudaFreeAsync(ws, s);
+    cudaFreeAsync(ks, s);
+    return e ? SE_ECUDA : SE_OK;
 }
 
 int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream) {

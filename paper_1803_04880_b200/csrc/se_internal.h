@@ -72,12 +72,18 @@ struct DwtParams {
     const uint8_t* in;
     uint8_t* out;
     int16_t* coef;
-    uint64_t n_bytes;
+    uint64_t n_bytes;         // of the whole file
     uint64_t n_blocks;
     uint32_t width;
     uint32_t bpr;
-    uint32_t rows;
+    uint32_t rows;            // R of the whole matrix (border reflection)
     uint32_t one;             // = 1, opaque to ptxas (see FusedParams::one)
+    // FULL-mode row window (whole file: 0, R, 0, R).  Output rows
+    // [row0, row0 + rows_out): Mallat bands of these rows only (forward) or
+    // these bytes (inverse), at local offsets.  Source rows [src_row0,
+    // src_row0 + src_rows): input bytes at in[(r - src_row0) * W] (forward) or
+    // the local Mallat layout of their coefficients in coef (inverse).
+    uint64_t row0, rows_out, src_row0, src_rows;
 };
 
 // Chapter 4 DCT 8x8 SE (row f3, k_dct.cu).  One thread per 8x8 block

@@ -94,3 +94,63 @@ def test_full_c4_shape_sampled(dev, orc):
     assert np.array_equal(c.cpu().numpy(), oc)
     back, rep = se.fragment_recover(a, b, c, x.size, W, L, KEY, IV, mode=FULL)
     assert torch.equal(back, xt) and rep.cpu().tolist() == [-1, 0]
+
+
+# FULL-mode row stripes with halo rows (row e for a11): (n, W) with several
+# stripes per file, stripe edges inside 64-row tiles, ragged last stripe
+STRIPE_CASES = [(256 * 200 + 77, 256), (128 * 520, 128), (1024 * 96, 1024), (64 * 1000 + 3, 64)]
+
+
+@pytest.mark.parametrize("L", [1, 2, 3])
+@pytest.mark.parametrize("n,W", STRIPE_CASES)
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_full_stripes_equal_whole_file(dev, orc, n, W, L, world):
+    """Each stripe protected from its rows + halo rows only, and recovered from
+    its fragments + halo block rows only: the concatenated streams equal the
+    whole-file FULL streams (and the oracle's), the bytes equal the input."""
+    from paper_1803_04880_b200 import shard
+    x = data(n, n + W + L + world)
+    oa, ob, oc = orc.protect(x, W, L, KEY, IV, mode=orc.MODE_FULL)
+    plan = [s for s in shard.plan_full_stripes(n, W, L, world) if s is not None]
+    assert len(plan) >= 2
+    got = {k: [] for k in "abc"}
+    for st in plan:
+        src = to_dev(x[st["src_byte_begin"]: st["src_byte_end"]], dev)
+        a, b, c = se.fragment_protect_stripe(src, n, W, L, KEY, IV, st["row_begin"], st["row_end"], st["src_row0"])
+        for k, t in zip("abc", (a, b, c)):
+            got[k].append(t.cpu().numpy())
+    for k, ref in zip("abc", (oa, ob, oc)):
+        assert np.array_equal(np.concatenate(got[k]), ref), k
+    back = []
+    for st in plan:
+        ins = [to_dev(s[slice(*st["rec_in"][k])], dev) for k, s in zip("abc", (oa, ob, oc))]
+        out, rep = se.fragment_recover_stripe(*ins, n, W, L, KEY, IV, st["row_begin"], st["row_end"],
+                                              st["rec_row0"], st["rec_rows"])
+        assert rep.cpu().tolist() == [-1, 0]
+        back.append(out.cpu().numpy())
+    assert np.array_equal(np.concatenate(back), x)
+
+
+def test_full_stripe_corruption_report(dev, orc):
+    """A flipped C' bit in stripe 1: its bytes equal the oracle's whole-file
+    recovery of the damaged streams; the report uses stripe-local indices."""
+    from paper_1803_04880_b200 import shard
+    n, W, L = 256 * 256, 256, 2
+    x = data(n, 11)
+    oa, ob, oc = orc.protect(x, W, L, KEY, IV, mode=orc.MODE_FULL)
+    plan = [s for s in shard.plan_full_stripes(n, W, L, 3) if s is not None]
+    st = plan[1]
+    blk = st["block_offset"] + 5
+    oc2 = oc.copy()
+    oc2[blk * 60 + 7] ^= 0xFF
+    oback, orep = orc.recover(oa, ob, oc2, n, W, L, KEY, IV, mode=orc.MODE_FULL)
+    ins = [to_dev(s[slice(*st["rec_in"][k])], dev) for k, s in zip("abc", (oa, ob, oc2))]
+    out, rep = se.fragment_recover_stripe(*ins, n, W, L, KEY, IV, st["row_begin"], st["row_end"],
+                                          st["rec_row0"], st["rec_rows"])
+    assert np.array_equal(out.cpu().numpy(), oback[st["byte_begin"]: st["byte_end"]])
+    first, bad = rep.cpu().tolist()
+    assert (first + st["block_offset"], bad) == orep if orep[1] else (first, bad) == (-1, 0)
+    # a window without its halo is refused
+    with pytest.raises(se.SEError):
+        se.fragment_recover_stripe(*ins, n, W, L, KEY, IV, st["row_begin"], st["row_end"],
+                                   st["row_begin"], st["row_end"] - st["row_begin"])

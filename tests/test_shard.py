@@ -117,3 +117,33 @@ def test_gloo_two_ranks_stripes(tmp_path):
     result = str(tmp_path / "result.txt")
     mp.spawn(_rank_main, args=(2, _free_port(), 8 * 1024 * 9 + 500, 1024, 2, result), nprocs=2, join=True)
     assert open(result).read() == "ok"
+
+
+@pytest.mark.parametrize("L", [1, 2, 3])
+@pytest.mark.parametrize("n,W,world", [(256 * 200 + 77, 256, 3), (32768 * 64, 32768, 8), (1024 * 96, 1024, 5),
+                                       (64 * 1000 + 3, 64, 2)])
+def test_plan_full_stripes_windows(orc, n, W, L, world):
+    """FULL stripes: rows partition the matrix; protect windows add 2(2^L-1)
+    halo rows per side (clipped); recover windows add whole halo block rows
+    and start on CTR/byte-aligned block rows; output slices tile the whole
+    FULL streams (oracle layout)."""
+    lay = orc.layout(n, W, L, orc.MODE_FULL)
+    plan = [s for s in shard.plan_full_stripes(n, W, L, world) if s is not None]
+    halo = 2 * ((1 << L) - 1)
+    assert plan[0]["row_begin"] == 0 and plan[-1]["row_end"] == lay["rows"]
+    for s0, s1 in zip(plan, plan[1:]):
+        assert s0["row_end"] == s1["row_begin"]
+    bits = dict(zip("abc", shard.FULL_BITS[L]))
+    for st in plan:
+        assert st["src_row0"] == max(0, st["row_begin"] - halo)
+        assert st["src_row0"] + st["src_rows"] == min(lay["rows"], st["row_end"] + halo)
+        r0 = st["rec_row0"]
+        assert r0 <= max(0, st["row_begin"] - 8 * -(-halo // 8)) and r0 % 8 == 0
+        assert r0 + st["rec_rows"] >= min(lay["rows"], st["row_end"] + 8 * -(-halo // 8))
+        blocks_before = r0 // 8 * (W // 8)
+        assert (blocks_before * bits["a"]) % 128 == 0
+        assert all((blocks_before * b) % 8 == 0 for b in bits.values())
+    for k in "abc":
+        assert plan[0]["out"][k][0] == 0 and plan[-1]["out"][k][1] == lay[f"{k}_bytes"]
+        for s0, s1 in zip(plan, plan[1:]):
+            assert s0["out"][k][1] == s1["out"][k][0]
