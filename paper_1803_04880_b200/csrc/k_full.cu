@@ -29,68 +29,113 @@ constexpr int kTileR = 64, kTileC = 128, kFullThreads = 512;
 
 template <int L>
 struct FullTile {
-    static constexpr int H = L == 1 ? 2 : L == 2 ? 8 : 16;   // >= 2(2^L - 1), multiple of 2^L
+    static constexpr int H = L == 1 ? 4 : L == 2 ? 8 : 16;   // >= 2(2^L - 1), multiple of 2^L and of 4
     static constexpr int SR = kTileR + 2 * H, SC = kTileC + 2 * H;
-    static constexpr size_t smem = (size_t)SR * SC * sizeof(int);
+    static constexpr int P = SC + 1;                          // odd pitch: row and column chunks hit distinct banks
+    static constexpr size_t smem = (size_t)SR * P * sizeof(int);
 };
 
-// One lifting step over the tile grid along one direction.
-//   DIR 0: rows (neighbours at j +- s), DIR 1: columns (i +- s)
-//   STEP 0: predict (odd level positions), 1: update (even positions),
-//   INV: the inverse step (undo update = STEP 1, undo predict = STEP 0)
-template <int L, int DIR, int STEP, bool INV, int s>
-__device__ __forceinline__ void lift_sweep(int* g, int64_t R0, int64_t C0, int64_t R, int64_t W) {
+// One lifting pass of level spacing s along one direction of the tile
+// (DIR 0: along rows, DIR 1: along columns), predict and update together.
+// The active samples of a line are cut into chunks of 8 (4 even, 4 odd); a
+// thread loads its chunk plus the samples the chunk edges need (forward:
+// m = -2..8, so d(-1) of the previous chunk is recomputed from raw samples;
+// inverse: m = -1..9), all threads load before any stores (one barrier), and
+// the lifting runs in registers.  Consecutive threads take consecutive lines,
+// which the odd row pitch puts in distinct banks.  Matrix borders: whole-sample
+// symmetric extension per level (x(N) = x(N-2), d(-1) = d(0)); samples beyond
+// the tile edge read 0 — they only feed halo outputs, which the halo of
+// 2(2^L - 1) samples keeps away from the tile interior.
+template <int L, int DIR, int s, bool INV>
+__device__ __forceinline__ void lift_pass(int* g, int R0, int C0, int R, int W) {
     using T = FullTile<L>;
-    // positions: along DIR, index ≡ (STEP == 0 ? s : 0) mod 2s; across DIR, ≡ 0 mod s
-    const int nA = DIR == 0 ? T::SR / s : T::SC / s;             // across
-    const int nL = DIR == 0 ? T::SC / (2 * s) : T::SR / (2 * s); // along (one parity)
-    const int64_t N = DIR == 0 ? W : R;                           // signal extent (samples of level 1)
-    const int64_t O = DIR == 0 ? C0 : R0;
-    const int64_t Oa = DIR == 0 ? R0 : C0, Na = DIR == 0 ? R : W;
-    const int span = DIR == 0 ? T::SC : T::SR;
-    for (int idx = threadIdx.x; idx < nA * nL; idx += blockDim.x) {
-        // consecutive threads: along a row (DIR 0) or across columns (DIR 1),
-        // so a warp's shared-memory accesses fall in distinct banks
-        const int a = (DIR == 0 ? idx / nL : idx % nA) * s;                        // across coordinate
-        const int k = (DIR == 0 ? idx % nL : idx / nA) * 2 * s + (STEP == 0 ? s : 0);   // along coordinate
-        const int64_t ga = Oa + a, gk = O + k;
-        if (ga < 0 || ga >= Na || gk < 0 || gk >= N) continue;    // outside the matrix
-        int lo = k - s, hi = k + s;
-        if (STEP == 0) {                               // odd position: neighbours are even samples
-            if (gk + s >= N) hi = k - s;               // x(N) = x(N-2)
-        } else {                                       // even position: neighbours are d's
-            if (gk - s < 0) lo = k + s;                // d(-1) = d(0)
+    constexpr int span = DIR == 0 ? T::SC : T::SR;            // along
+    constexpr int nA = (DIR == 0 ? T::SR : T::SC) / s;         // active lines
+    constexpr int nC = span / (8 * s);                         // chunks per line
+    static_assert(span % (8 * s) == 0, "tile span must hold whole chunks");
+    constexpr int items = nA * nC;
+    constexpr int iters = (items + kFullThreads - 1) / kFullThreads;
+    constexpr int step = DIR == 0 ? s : s * T::P;              // smem distance between active samples
+    constexpr int m0 = INV ? -1 : -2;                          // first loaded sample
+    const int O = DIR == 0 ? C0 : R0, N = DIR == 0 ? W : R;    // along: global origin, extent
+    const int Oa = DIR == 0 ? R0 : C0, Na = DIR == 0 ? R : W;  // across
+    int v[iters][11];
+#pragma unroll
+    for (int it = 0; it < iters; ++it) {
+        const int idx = threadIdx.x + it * kFullThreads;
+        const int a = (idx % nA) * s, j0 = (idx / nA) * 8 * s;
+        const int base = DIR == 0 ? a * T::P + j0 : j0 * T::P + a;
+#pragma unroll
+        for (int q = 0; q < 11; ++q) {
+            const int j = j0 + (q + m0) * s;
+            v[it][q] = (idx < items && j >= 0 && j < span) ? g[base + (q + m0) * step] : 0;
         }
-        if (lo < 0 || hi >= span) continue;            // halo edge: output not needed
-        auto at = [&](int kk) -> int& { return DIR == 0 ? g[a * T::SC + kk] : g[kk * T::SC + a]; };
-        int& x = at(k);
-        const int nb = at(lo) + at(hi);
-        if (STEP == 0) x = INV ? x + (nb >> 1) : x - (nb >> 1);            // Eq. 5.1
-        else x = INV ? x - ((nb + 2) >> 2) : x + ((nb + 2) >> 2);          // Eq. 5.2 (+)
     }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < iters; ++it) {
+        const int idx = threadIdx.x + it * kFullThreads;
+        if (idx >= items) continue;
+        const int a = (idx % nA) * s, j0 = (idx / nA) * 8 * s;
+        const int ga = Oa + a;
+        if (ga < 0 || ga >= Na) continue;                      // line outside the matrix
+        const int base = DIR == 0 ? a * T::P + j0 : j0 * T::P + a;
+        const int G0 = O + j0;                                 // global coordinate of m = 0
+        int* x = v[it] - m0;                                   // x[m], m = m0 .. m0 + 10
+        if constexpr (!INV) {
+            // predict (Eq. 5.1) at odd m = -1, 1, 3, 5, 7; right neighbour reflected at the border
+#pragma unroll
+            for (int m = -1; m <= 7; m += 2) {
+                const int Gm = G0 + m * s;
+                const int r = (Gm + s >= N) ? x[m - 1] : x[m + 1];
+                x[m] -= (x[m - 1] + r) >> 1;
+            }
+            // update (Eq. 5.2, "+") at even m = 0, 2, 4, 6; d(-1) = d(0) at the left border
+#pragma unroll
+            for (int m = 0; m <= 6; m += 2) {
+                const int Gm = G0 + m * s;
+                const int l = (Gm == 0) ? x[m + 1] : x[m - 1];
+                x[m] += (l + x[m + 1] + 2) >> 2;
+            }
+        } else {
+            // undo update at even m = 0 .. 8, then undo predict at odd m = 1 .. 7
+#pragma unroll
+            for (int m = 0; m <= 8; m += 2) {
+                const int Gm = G0 + m * s;
+                const int l = (Gm == 0) ? x[m + 1] : x[m - 1];
+                x[m] -= (l + x[m + 1] + 2) >> 2;
+            }
+#pragma unroll
+            for (int m = 1; m <= 7; m += 2) {
+                const int Gm = G0 + m * s;
+                const int r = (Gm + s >= N) ? x[m - 1] : x[m + 1];
+                x[m] += (x[m - 1] + r) >> 1;
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int Gm = G0 + m * s;
+            if (Gm >= 0 && Gm < N) g[base + m * step] = x[m];
+        }
+    }
+    __syncthreads();
 }
 
-// All levels, forward (l = 1..L) / inverse (l = L..1); the sample spacing
-// s = 2^(l-1) is a compile-time constant so the sweep index arithmetic folds.
+// All levels, forward (l = 1..L: rows then columns) / inverse (l = L..1:
+// columns then rows); the spacing s = 2^(l-1) is a compile-time constant.
 template <int L, int l>
-__device__ __forceinline__ void fwd_levels(int* g, int64_t R0, int64_t C0, int64_t R, int64_t W) {
+__device__ __forceinline__ void fwd_levels(int* g, int R0, int C0, int R, int W) {
     if constexpr (l <= L) {
-        constexpr int s = 1 << (l - 1);
-        lift_sweep<L, 0, 0, false, s>(g, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 0, 1, false, s>(g, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 1, 0, false, s>(g, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 1, 1, false, s>(g, R0, C0, R, W); __syncthreads();
+        lift_pass<L, 0, 1 << (l - 1), false>(g, R0, C0, R, W);
+        lift_pass<L, 1, 1 << (l - 1), false>(g, R0, C0, R, W);
         fwd_levels<L, l + 1>(g, R0, C0, R, W);
     }
 }
 template <int L, int l>
-__device__ __forceinline__ void inv_levels(int* g, int64_t R0, int64_t C0, int64_t R, int64_t W) {
+__device__ __forceinline__ void inv_levels(int* g, int R0, int C0, int R, int W) {
     if constexpr (l >= 1) {
-        constexpr int s = 1 << (l - 1);
-        lift_sweep<L, 1, 1, true, s>(g, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 1, 0, true, s>(g, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 0, 1, true, s>(g, R0, C0, R, W); __syncthreads();
-        lift_sweep<L, 0, 0, true, s>(g, R0, C0, R, W); __syncthreads();
+        lift_pass<L, 1, 1 << (l - 1), true>(g, R0, C0, R, W);
+        lift_pass<L, 0, 1 << (l - 1), true>(g, R0, C0, R, W);
         inv_levels<L, l - 1>(g, R0, C0, R, W);
     }
 }
@@ -110,38 +155,50 @@ template <int L>
 __global__ void __launch_bounds__(kFullThreads) k_dwt_full_fwd(const __grid_constant__ DwtParams p) {
     using T = FullTile<L>;
     extern __shared__ int g[];
-    const int64_t W = p.width, R = p.rows;
-    const int64_t row0 = (int64_t)p.row0, row_end = min((int64_t)(p.row0 + p.rows_out), R);
-    const int64_t s0 = (int64_t)p.src_row0, s1 = (int64_t)(p.src_row0 + p.src_rows);
-    const int64_t tr0 = row0 + (int64_t)blockIdx.y * kTileR, tc0 = (int64_t)blockIdx.x * kTileC;
-    const int64_t R0 = tr0 - T::H, C0 = tc0 - T::H;
-    // load tile + halo, centered (C8), zero fill past n (C18); rows the caller
-    // did not provide (beyond a stripe's halo) only feed outputs not written
-    for (int idx = threadIdx.x; idx < T::SR * T::SC; idx += blockDim.x) {
-        const int i = idx / T::SC, j = idx % T::SC;
-        const int64_t gr = R0 + i, gc = C0 + j;
-        int v = 0;
-        if (gr >= 0 && gr < R && gc >= 0 && gc < W) {
+    const int W = (int)p.width, R = (int)p.rows;
+    const int row0 = (int)p.row0, row_end = min((int)(p.row0 + p.rows_out), R);
+    const int s0 = (int)p.src_row0, s1 = (int)(p.src_row0 + p.src_rows);
+    const int tr0 = row0 + (int)blockIdx.y * kTileR, tc0 = (int)blockIdx.x * kTileC;
+    const int R0 = tr0 - T::H, C0 = tc0 - T::H;
+    // load tile + halo, 4 bytes per access, centered (C8), zero fill past n
+    // (C18); rows the caller did not provide (beyond a stripe's halo) read 0
+    constexpr int WPR = T::SC / 4;
+    for (int idx = threadIdx.x; idx < T::SR * WPR; idx += kFullThreads) {
+        const int i = idx / WPR, w = idx % WPR;
+        const int gr = R0 + i, gc = C0 + 4 * w;
+        int v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+        if (gr >= 0 && gr < R && gc >= 0 && gc < W) {            // whole word inside (W % 8 == 0)
             const uint64_t o = (uint64_t)gr * W + gc;
-            if (o >= p.n_bytes) v = -128;                                   // zero fill (C18)
-            else if (gr >= s0 && gr < s1) v = (int)p.in[(uint64_t)(gr - s0) * W + gc] - 128;
+            const bool have = gr >= s0 && gr < s1;
+            if (have && o + 4 <= p.n_bytes) {
+                const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(p.in + (uint64_t)(gr - s0) * W + gc));
+                v0 = (int)(q & 0xff) - 128; v1 = (int)((q >> 8) & 0xff) - 128;
+                v2 = (int)((q >> 16) & 0xff) - 128; v3 = (int)(q >> 24) - 128;
+            } else {
+                int t[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    t[b] = (o + b >= p.n_bytes) ? -128 : have ? (int)p.in[(uint64_t)(gr - s0) * W + gc + b] - 128 : 0;
+                v0 = t[0]; v1 = t[1]; v2 = t[2]; v3 = t[3];
+            }
         }
-        g[idx] = v;
+        int* d = g + i * T::P + 4 * w;
+        d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3;
     }
     __syncthreads();
     fwd_levels<L, 1>(g, R0, C0, R, W);
     // write the tile interior band by band in Mallat layout
     for_each_band<L>([&](int l, int band) {
         const int hr = band >= 2, hc = band & 1, half = 1 << (l - 1);
-        const int br = kTileR >> l, bc = kTileC >> l;        // band rectangle of this tile
+        const int br = kTileR >> l, bc = kTileC >> l;          // band rectangle of this tile
         const int64_t mr0 = (hr ? ((int64_t)p.rows_out >> l) : 0) + ((tr0 - row0) >> l);   // local Mallat rows
-        const int64_t mc0 = (hc ? (W >> l) : 0) + (tc0 >> l);
-        for (int idx = threadIdx.x; idx < br * bc; idx += blockDim.x) {
+        const int mc0 = (hc ? (W >> l) : 0) + (tc0 >> l);
+        for (int idx = threadIdx.x; idx < br * bc; idx += kFullThreads) {
             const int bi = idx / bc, bj = idx % bc;
-            const int64_t gr = tr0 + ((int64_t)bi << l) + (hr ? half : 0);
-            const int64_t gc = tc0 + ((int64_t)bj << l) + (hc ? half : 0);
+            const int gr = tr0 + (bi << l) + (hr ? half : 0);
+            const int gc = tc0 + (bj << l) + (hc ? half : 0);
             if (gr >= row_end || gc >= W) continue;
-            const int v = g[(gr - R0) * T::SC + (gc - C0)];
+            const int v = g[(gr - R0) * T::P + (gc - C0)];
             p.coef[(uint64_t)(mr0 + bi) * W + (mc0 + bj)] = (int16_t)v;
         }
     });
@@ -153,49 +210,64 @@ __global__ void __launch_bounds__(kFullThreads) k_dwt_full_inv(const __grid_cons
     using T = FullTile<L>;
     extern __shared__ int g[];
     __shared__ unsigned int s_badmask[(kTileR / 8) * (kTileC / 8) / 32];
-    const int64_t W = p.width, R = p.rows;
-    const int64_t row0 = (int64_t)p.row0, row_end = min((int64_t)(p.row0 + p.rows_out), R);
-    const int64_t tr0 = row0 + (int64_t)blockIdx.y * kTileR, tc0 = (int64_t)blockIdx.x * kTileC;
-    const int64_t R0 = tr0 - T::H, C0 = tc0 - T::H;
-    for (int i = threadIdx.x; i < (kTileR / 8) * (kTileC / 8) / 32; i += blockDim.x) s_badmask[i] = 0;
+    const int W = (int)p.width, R = (int)p.rows;
+    const int row0 = (int)p.row0, row_end = min((int)(p.row0 + p.rows_out), R);
+    const int tr0 = row0 + (int)blockIdx.y * kTileR, tc0 = (int)blockIdx.x * kTileC;
+    const int R0 = tr0 - T::H, C0 = tc0 - T::H;
+    for (int i = threadIdx.x; i < (kTileR / 8) * (kTileC / 8) / 32; i += kFullThreads) s_badmask[i] = 0;
     // gather tile + halo from the Mallat layout into the interleaved grid, band by band
     for_each_band<L>([&](int l, int band) {
         const int hr = band >= 2, hc = band & 1, half = 1 << (l - 1);
         // band samples whose grid position falls in [R0, R0+SR) x [C0, C0+SC)
-        const int64_t b_r0 = (R0 - (hr ? half : 0) + ((1 << l) - 1)) >> l;   // ceil, R0 may be negative
-        const int64_t b_c0 = (C0 - (hc ? half : 0) + ((1 << l) - 1)) >> l;
+        const int b_r0 = (R0 - (hr ? half : 0) + ((1 << l) - 1)) >> l;   // ceil, R0 may be negative
+        const int b_c0 = (C0 - (hc ? half : 0) + ((1 << l) - 1)) >> l;
         const int nbr = (T::SR >> l) + 1, nbc = (T::SC >> l) + 1;
         // the source window holds band rows [src_row0 >> l, (src_row0 + src_rows) >> l)
-        const int64_t sb0 = (int64_t)p.src_row0 >> l, sbn = (int64_t)p.src_rows >> l;
-        for (int idx = threadIdx.x; idx < nbr * nbc; idx += blockDim.x) {
-            const int64_t bi = b_r0 + idx / nbc, bj = b_c0 + idx % nbc;
-            if (bi < 0 || bj < 0 || bi >= (R >> l) || bj >= (W >> l)) continue;
-            if (bi < sb0 || bi >= sb0 + sbn) continue;            // beyond a stripe's halo: unused
-            const int64_t gr = (bi << l) + (hr ? half : 0), gc = (bj << l) + (hc ? half : 0);
-            if (gr < R0 || gr >= R0 + T::SR || gc < C0 || gc >= C0 + T::SC) continue;
-            const int64_t mr = (hr ? sbn : 0) + (bi - sb0), mc = (hc ? (W >> l) : 0) + bj;
-            g[(gr - R0) * T::SC + (gc - C0)] = p.coef[(uint64_t)mr * W + mc];
+        const int sb0 = (int)(p.src_row0 >> l), sbn = (int)(p.src_rows >> l);
+        // rows of band samples inside the tile grid and the source window, then columns
+        const int r_lo = max(max(b_r0, 0), sb0), r_hi = min(min(b_r0 + nbr, R >> l), sb0 + sbn);
+        const int c_lo = max(b_c0, 0), c_hi = min(b_c0 + nbc, W >> l);
+        const int nr = max(r_hi - r_lo, 0), nc = max(c_hi - c_lo, 0);
+        const int16_t* src = p.coef + (hc ? (W >> l) : 0);
+        const int64_t mrow0 = (hr ? sbn : 0) - sb0;
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < nr * nc; idx += kFullThreads) {
+            const int bi = r_lo + idx / nc, bj = c_lo + idx % nc;
+            const int gr = (bi << l) + (hr ? half : 0), gc = (bj << l) + (hc ? half : 0);
+            if (gr >= R0 + T::SR || gc >= C0 + T::SC) continue;
+            g[(gr - R0) * T::P + (gc - C0)] = __ldg(src + (uint64_t)(mrow0 + bi) * W + bj);
         }
     });
     __syncthreads();
     inv_levels<L, L>(g, R0, C0, R, W);
-    // write bytes (+128), flag footprints with samples outside [0, 255]
-    for (int idx = threadIdx.x; idx < kTileR * kTileC; idx += blockDim.x) {
-        const int i = idx / kTileC, j = idx % kTileC;
-        const int64_t gr = tr0 + i, gc = tc0 + j;
+    // write bytes (+128), 4 per store; flag footprints with samples outside [0, 255]
+    constexpr int WPR = kTileC / 4;
+    for (int idx = threadIdx.x; idx < kTileR * WPR; idx += kFullThreads) {
+        const int i = idx / WPR, w = idx % WPR;
+        const int gr = tr0 + i, gc = tc0 + 4 * w;
         if (gr >= row_end || gc >= W) continue;
-        const int v = g[(i + T::H) * T::SC + (j + T::H)] + 128;
-        if (v & ~0xff) {
-            const int fp = (i / 8) * (kTileC / 8) + (j / 8);
+        const int* src = g + (i + T::H) * T::P + (4 * w + T::H);
+        const int v0 = src[0] + 128, v1 = src[1] + 128, v2 = src[2] + 128, v3 = src[3] + 128;
+        if ((v0 | v1 | v2 | v3) & ~0xff) {
+            const int fp = (i / 8) * (kTileC / 8) + (4 * w) / 8;
             atomicOr(&s_badmask[fp / 32], 1u << (fp % 32));
         }
         const uint64_t o = (uint64_t)gr * W + gc;
-        if (o < p.n_bytes) p.out[(uint64_t)(gr - row0) * W + gc] = (uint8_t)v;
+        uint8_t* dst = p.out + (uint64_t)(gr - row0) * W + gc;
+        if (o + 4 <= p.n_bytes) {
+            *reinterpret_cast<uint32_t*>(dst) = (uint32_t)(v0 & 0xff) | (uint32_t)(v1 & 0xff) << 8 |
+                                                (uint32_t)(v2 & 0xff) << 16 | (uint32_t)(v3 & 0xff) << 24;
+        } else {
+            const int vv[4] = {v0, v1, v2, v3};
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (o + b < p.n_bytes) dst[b] = (uint8_t)vv[b];
+        }
     }
     if (report) {
         __syncthreads();
         const int nfp = (kTileR / 8) * (kTileC / 8);
-        for (int fp = threadIdx.x; fp < nfp; fp += blockDim.x) {
+        for (int fp = threadIdx.x; fp < nfp; fp += kFullThreads) {
             if (s_badmask[fp / 32] & (1u << (fp % 32))) {
                 const int64_t fbr = tr0 / 8 + fp / (kTileC / 8), fbc = tc0 / 8 + fp % (kTileC / 8);
                 if (fbr < row_end / 8 && fbc < W / 8) {                   // block index local to row0
