@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "se_device.cuh"
+#include "sha2_spec.cuh"
 
 namespace se {
 
@@ -144,7 +145,14 @@ __device__ __forceinline__ void xor_g2s(uint32_t* s, const uint8_t* __restrict__
 }
 
 // SHA-256 mask of B from the plain A record (framing C15: K||IV||be64(b)||A).
-template <int L, int MODE>
+#ifndef SE_SPEC
+#define SE_SPEC 2      // bit 0: SHA-256 (B mask), bit 1: SHA-512 (C mask) schedules specialised
+                       // (2: the SHA-256 one costs more in instruction fetch than it saves)
+#endif
+// SPEC: the message schedule specialised with the launch's host-computed
+// constants (p.s256 / p.s512, sha2_spec.cuh); batches (per-file IV) use the
+// generic schedule.
+template <int L, int MODE, bool SPEC = true>
 __device__ __forceinline__ void mask_b(const FusedParams& p, uint64_t gb, const uint32_t (&A)[Rec<L, MODE>::AW],
                                        uint32_t (&B)[Rec<L, MODE>::BW]) {
     using R = Rec<L, MODE>;
@@ -165,7 +173,8 @@ __device__ __forceinline__ void mask_b(const FusedParams& p, uint64_t gb, const 
     const uint32_t h0[8] = {p.h256[0], p.h256[1], p.h256[2], p.h256[3],
                             p.h256[4], p.h256[5], p.h256[6], p.h256[7]};
     uint32_t H[8];
-    sha256_from_round8(st, h0, W, H, p.one);
+    if constexpr (SPEC && (SE_SPEC & 1)) sha256_from_round8_spec<msg_var256(R::ABYTES)>(st, h0, W, p.s256, H, p.one);
+    else sha256_from_round8(st, h0, W, H, p.one);
 #pragma unroll
     for (int k = 0; k < R::BW; ++k) {
         const uint32_t m = (k == R::BW - 1) ? (H[k] & head_mask(R::BBITS % 32)) : H[k];
@@ -174,7 +183,7 @@ __device__ __forceinline__ void mask_b(const FusedParams& p, uint64_t gb, const 
 }
 
 // SHA-512 mask of C from the record `src` (B' for L >= 2, plain A for L = 1).
-template <int NW, int SBYTES>
+template <int NW, int SBYTES, bool SPEC = true>
 __device__ __forceinline__ void mask_c(const FusedParams& p, uint64_t gb, const uint32_t (&src)[NW],
                                        uint32_t (&C)[15]) {
     W64 W[16];
@@ -200,7 +209,8 @@ __device__ __forceinline__ void mask_c(const FusedParams& p, uint64_t gb, const 
     const uint64_t h0[8] = {p.h512[0], p.h512[1], p.h512[2], p.h512[3],
                             p.h512[4], p.h512[5], p.h512[6], p.h512[7]};
     uint64_t H[8];
-    sha512_from_round4(st, h0, W, H, p.one);
+    if constexpr (SPEC && (SE_SPEC & 2)) sha512_from_round4_spec<msg_var512(SBYTES)>(st, h0, W, p.s512, H, p.one);
+    else sha512_from_round4(st, h0, W, H, p.one);
 #pragma unroll
     for (int k = 0; k < 15; ++k) C[k] ^= (k & 1) ? (uint32_t)H[k / 2] : (uint32_t)(H[k / 2] >> 32);
 }
@@ -273,7 +283,7 @@ __device__ __forceinline__ void footprint_full(const FusedParams& p, uint64_t br
 // the lifting and hashing and the fused kernel carries no AES tables.
 // BPC = blocks (threads) per CTA: 128 everywhere but the single-file BLOCK8
 // kernels at L = 1, 2, where 32 or 64 give finer work units (k_block8.cu).
-template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta>
+template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta, bool SPEC = true>
 __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
     static_assert((BPC * R::ABITS) % 128 == 0 && (BPC * R::BBITS) % 128 == 0 && (BPC * R::CBITS) % 128 == 0,
@@ -318,10 +328,10 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
         if (MASK) {
             const uint64_t gb = p.block_offset + blk;
             if (R::BBITS) {
-                mask_b<L, MODE>(p, gb, A, B);                               // row a7
-                mask_c<R::BW, R::BBYTES>(p, gb, B, C);                      // row a8
+                mask_b<L, MODE, SPEC>(p, gb, A, B);                         // row a7
+                mask_c<R::BW, R::BBYTES, SPEC>(p, gb, B, C);                // row a8
             } else {
-                mask_c<R::AW, R::ABYTES>(p, gb, A, C);                      // C21 (L = 1)
+                mask_c<R::AW, R::ABYTES, SPEC>(p, gb, A, C);                // C21 (L = 1)
             }
         }
         smem_put_record<R::AW, R::ABITS>(sa, (uint32_t)tid * R::ABITS, A);
@@ -350,7 +360,7 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
 // The keystream of the whole A stream sits in p.ks (k_cipher_ctr, launched
 // before with programmatic stream serialization); it is waited for and
 // applied after the SHA-512 unmask of C, which does not need A.
-template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta>
+template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta, bool SPEC = true>
 __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
     static_assert((BPC * R::ABITS) % 128 == 0 && (BPC * R::BBITS) % 128 == 0 && (BPC * R::CBITS) % 128 == 0,
@@ -385,7 +395,7 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         if (R::BBITS) smem_get_record<R::BW, R::BBITS>(sb, SB_W, (uint32_t)tid * R::BBITS, B);
         else B[0] = 0;
         smem_get_record<R::CW, R::CBITS>(sc, SC_W, (uint32_t)tid * R::CBITS, C);
-        if (MASK && R::BBITS) mask_c<R::BW, R::BBYTES>(p, gb, B, C);          // C from B'
+        if (MASK && R::BBITS) mask_c<R::BW, R::BBYTES, SPEC>(p, gb, B, C);    // C from B'
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");                      // keystream kernel complete
     xor_g2s<BPC>(sa, p.ks + a0, alen, tid);                                       // A' -> A
@@ -395,8 +405,8 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
     if (valid) {
         smem_get_record<R::AW, R::ABITS>(sa, SA_W, (uint32_t)tid * R::ABITS, A);
         if (MASK) {
-            if (R::BBITS) mask_b<L, MODE>(p, gb, A, B);                      // B from A
-            else mask_c<R::AW, R::ABYTES>(p, gb, A, C);                      // C21 (L = 1)
+            if (R::BBITS) mask_b<L, MODE, SPEC>(p, gb, A, B);                // B from A
+            else mask_c<R::AW, R::ABYTES, SPEC>(p, gb, A, C);                // C21 (L = 1)
         }
         int v[8][8];
         for_each_field<L, MODE>([&](int s, int pos, int i, int j, int w) {

@@ -114,8 +114,8 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
     }
     __syncthreads();
     const uint64_t cta = x - job.cta_begin;
-    if (RECOVER) recover_cta<L, MASK, 0>(sp, cta);
-    else protect_cta<L, MASK, 0>(sp, cta);
+    if (RECOVER) recover_cta<L, MASK, 0, kBlocksPerCta, false>(sp, cta);      // per-file IV: generic schedule
+    else protect_cta<L, MASK, 0, kBlocksPerCta, false>(sp, cta);
 }
 
 __global__ void k_report_init(se_report* r, uint32_t n) {

@@ -114,6 +114,51 @@ static int check_geom(const se_geom* g) {
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// FIPS 180-4 §4.1.2 / §4.1.3 small sigmas
+static uint32_t s0_256(uint32_t x) { return ror32(x, 7) ^ ror32(x, 18) ^ (x >> 3); }
+static uint32_t s1_256(uint32_t x) { return ror32(x, 17) ^ ror32(x, 19) ^ (x >> 10); }
+static uint64_t s0_512(uint64_t x) { return ror64(x, 1) ^ ror64(x, 8) ^ (x >> 7); }
+static uint64_t s1_512(uint64_t x) { return ror64(x, 19) ^ ror64(x, 61) ^ (x >> 6); }
+
+// Block-independent schedule data (sha2_spec.cuh) for message words w[16]
+// whose block-dependent words (mask) are ignored.
+template <typename T, typename S0, typename S1>
+static void sched_consts(uint32_t mask, const T w[16], const T* K, S0 s0, S1 s1, T c[16], T kw[32]) {
+    const uint64_t V = sched_var(mask);
+    auto var = [&](int t) { return ((V >> t) & 1u) != 0; };
+    T W[32];
+    for (int t = 0; t < 16; ++t) W[t] = var(t) ? 0 : w[t];
+    for (int t = 16; t < 32; ++t) {
+        T part = 0;
+        if (!var(t - 2)) part += s1(W[t - 2]);
+        if (!var(t - 7)) part += W[t - 7];
+        if (!var(t - 15)) part += s0(W[t - 15]);
+        if (!var(t - 16)) part += W[t - 16];
+        W[t] = var(t) ? 0 : part;
+        c[t - 16] = part;                        // == W_t when no term depends on the block
+    }
+    for (int t = 0; t < 32; ++t) kw[t] = var(t) ? 0 : (T)(K[t] + W[t]);
+}
+
+static void fill_sched(FusedParams& p, const se_layout& lay) {
+    const int L = lay.b_bits == 0 ? 1 : 2;       // L = 1: the C mask hashes A; else B', B from A
+    // SHA-512 of the C mask: K||IV||be64(b)||record, record = B' (L >= 2) or A (L = 1)
+    const int sb = (int)((L == 1 ? lay.a_bits : lay.b_bits) + 7) / 8;
+    uint64_t w5[16] = {0};
+    for (int i = 0; i < 4; ++i) w5[i] = (uint64_t)p.kiv[2 * i] << 32 | p.kiv[2 * i + 1];
+    w5[(40 + sb) / 8] |= 0x80ull << (56 - 8 * ((40 + sb) % 8));         // FIPS 180-4 §5.1.2
+    w5[15] = (uint64_t)(40 + sb) * 8;
+    sched_consts<uint64_t>(msg_var512(sb), w5, kK512, s0_512, s1_512, p.s512.c, p.s512.kw);
+    if (lay.b_bits) {                            // SHA-256 of the B mask: K||IV||be64(b)||A
+        const int ab = (int)(lay.a_bits + 7) / 8;
+        uint32_t w2[16] = {0};
+        for (int i = 0; i < 8; ++i) w2[i] = p.kiv[i];
+        w2[(40 + ab) / 4] |= 0x80u << (24 - 8 * ((40 + ab) % 4));      // FIPS 180-4 §5.1.1
+        w2[15] = (uint32_t)(40 + ab) * 8;
+        sched_consts<uint32_t>(msg_var256(ab), w2, kK256, s0_256, s1_256, p.s256.c, p.s256.kw);
+    }
+}
+
 static void fill_fused(FusedParams& p, const se_geom* g, const se_layout& lay, const uint8_t key[16],
                        const uint8_t iv[16]) {
     memset(&p, 0, sizeof p);
@@ -133,6 +178,7 @@ static void fill_fused(FusedParams& p, const se_geom* g, const se_layout& lay, c
     for (int i = 0; i < 4; ++i) w[i] = (uint64_t)p.kiv[2 * i] << 32 | p.kiv[2 * i + 1];
     sha512_mid(w, p.mid512);
     memcpy(p.h512, kH512, sizeof kH512);
+    fill_sched(p, lay);
 }
 
 // Keep the stream-ordered pool's memory across calls (default release

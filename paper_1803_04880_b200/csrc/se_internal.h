@@ -11,6 +11,39 @@ namespace se {
 
 constexpr int kBlocksPerCta = 128;   // one thread per 8x8 block, 128 blocks per CTA
 
+// ---- message-schedule specialisation of the B / C mask hashes (sha2_spec.cuh)
+// bit t set: schedule word W_t depends on the block (t < 64)
+__host__ __device__ constexpr uint64_t sched_var(uint32_t msg_mask) {
+    uint64_t v = msg_mask;
+    for (int t = 16; t < 64; ++t)
+        if (((v >> (t - 2)) | (v >> (t - 7)) | (v >> (t - 15)) | (v >> (t - 16))) & 1u) v |= 1ull << t;
+    return v;
+}
+// block-dependent message words: SHA-512 over K||IV||be64(b)||record (64-bit
+// words: b is word 4, record bytes from byte 40), SHA-256 over the same
+// framing (32-bit words: b is words 8, 9)
+__host__ __device__ constexpr uint32_t msg_var512(int rec_bytes) {
+    uint32_t m = 1u << 4;
+    for (int w = 5; w <= (40 + rec_bytes - 1) / 8; ++w) m |= 1u << w;
+    return m;
+}
+__host__ __device__ constexpr uint32_t msg_var256(int rec_bytes) {
+    uint32_t m = (1u << 8) | (1u << 9);
+    for (int w = 10; w <= (40 + rec_bytes - 1) / 4; ++w) m |= 1u << w;
+    return m;
+}
+// block-independent schedule data of one launch (host-computed):
+// c[t-16] for t = 16..31 = W_t if block-independent, else the sum of its
+// block-independent terms; kw[t] = K_t + W_t for block-independent W_t, t < 32
+struct SchedConst512 {
+    uint64_t c[16];
+    uint64_t kw[32];
+};
+struct SchedConst256 {
+    uint32_t c[16];
+    uint32_t kw[32];
+};
+
 // Everything a fused protect/recover launch needs (passed by value; lives in
 // the constant bank, so round keys and midstates are uniform operands).
 struct FusedParams {
@@ -37,6 +70,8 @@ struct FusedParams {
     uint32_t h256[8];         // SHA-256 H(0)
     uint64_t mid512[8];       // SHA-512 state after rounds 0..3 over K||IV
     uint64_t h512[8];         // SHA-512 H(0)
+    SchedConst512 s512;       // C-mask schedule constants (single-file / FULL kernels)
+    SchedConst256 s256;       // B-mask schedule constants
 };
 
 // Library-private layout of se_job.derived[] (filled by fragment_batch_plan).
