@@ -41,14 +41,17 @@ L2_BYTES = 126 * (1 << 20)
 # minimal 32-bit mapping.  Adds are excluded (they may issue on the FMA pipe
 # as IMAD), so these ops alone set a lower bound on ALU-pipe cycles.
 #   SHA-256 rounds 8..63 (host midstate covers 0..7):  8*10 + 48*18 = 944
-#   SHA-512 rounds 4..79 (host midstate covers 0..3): 12*20 + 64*36 = 2544
+#   SHA-512 rounds 4..79 (host midstate covers 0..3): 12*20 + 64*36 = 2544,
+#     less what the launch-constant schedule (sha2_spec.cuh) removes: 8 ops per
+#     sigma not evaluated in W16..W31 (18 at L = 2, 17 at L = 1, 3) and the low
+#     half of K_t + W_t for the block-independent W_t (12 / 11 / 11 rounds)
 #   5/3 lifting shifts: L1 16 lifts*8 + L2 8 lifts*4 (+ L3 4 lifts*2) = 160 (168)
 #   byte unpack 64; field pack/unpack ~2 per field + word splits = 140
 #   mask XORs: B + C words = 19;  AES-CTR: 260 ops per AES block * a_bits/128
 ALU_OPS = {
-    1: {"sha256": 0, "sha512": 2544, "dwt": 128 + 64, "pack": 140, "xor": 15, "aes": 260 * 160 / 128},
-    2: {"sha256": 944, "sha512": 2544, "dwt": 160 + 64, "pack": 140, "xor": 19, "aes": 260 * 40 / 128},
-    3: {"sha256": 944, "sha512": 2544, "dwt": 168 + 64, "pack": 140, "xor": 20, "aes": 260 * 10 / 128},
+    1: {"sha256": 0, "sha512": 2544 - 8 * 17 - 11, "dwt": 128 + 64, "pack": 140, "xor": 15, "aes": 260 * 160 / 128},
+    2: {"sha256": 944, "sha512": 2544 - 8 * 18 - 12, "dwt": 160 + 64, "pack": 140, "xor": 19, "aes": 260 * 40 / 128},
+    3: {"sha256": 944, "sha512": 2544 - 8 * 17 - 11, "dwt": 168 + 64, "pack": 140, "xor": 20, "aes": 260 * 10 / 128},
 }
 ALU_LANES_PER_SM_CLK = 64      # B300_MICROARCH.md: IADD3/LOP3/SHF/PRMT on alu-pipe, rt_SMSP = 2
 NUM_SMS = 148
