@@ -563,10 +563,15 @@ def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=8 << 
 # Table 4.1 / 4.9 image sizes (grey scale)
 DCT_SIZES = [(1024, 768), (1600, 1200), (3240, 2592), (4800, 4800)]
 # ALU-pipe ops per 8x8 block at level 2 (DESIGN.md §5 f3): SHA-512 of one
-# message block from round 0 (16 message rounds x 20 + 64 schedule rounds x
-# 36), pixel byte PRMTs (64 in, 48 pack), mask XOR 16, record pack ~30,
-# AES-CTR share 260 * 66/128.  The fp32 DCT work issues on the FMA pipe.
-DCT_ALU_OPS = {"sha512": 16 * 20 + 64 * 36, "bytes": 64 + 48, "xor": 16, "record": 30, "aes": 260 * 66 / 128}
+# message block (unkeyed: from round 0, 16 message rounds x 20 + 64 schedule
+# rounds x 36; keyed: from the round-4 midstate, 12 x 20 + 64 x 36), less what
+# the launch-constant schedule removes (sha2_spec.cuh: 8 per sigma of
+# W16..W31 not evaluated - 16 unkeyed, 18 keyed - and the low half of K + W
+# for the 14 / 12 block-independent words), pixel byte PRMTs (64 in, 48
+# pack), mask XOR 16, record pack ~30, AES-CTR share 260 * 66/128.  The fp32
+# DCT work issues on the FMA pipe.
+DCT_ALU_OPS = {"bytes": 64 + 48, "xor": 16, "record": 30, "aes": 260 * 66 / 128}
+DCT_SHA512_OPS = {False: 16 * 20 + 64 * 36 - 8 * 16 - 14, True: 12 * 20 + 64 * 36 - 8 * 18 - 12}
 
 
 def run_dct(args):
@@ -666,7 +671,7 @@ def run_dct(args):
     traffic, traffic_src = load_traffic(kkey)
     alg_bytes = 2 * n + lay["a_bytes"]
     if level == 2:
-        ops_blk = sum(DCT_ALU_OPS.values())
+        ops_blk = sum(DCT_ALU_OPS.values()) + DCT_SHA512_OPS[bool(flags)]
         ach = ops_blk * lay["records"] / (dom_ms / 1e3) / 1e9
         peak_alu = NUM_SMS * ALU_LANES_PER_SM_CLK * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
         roofline = {"bound": "alu", "kernel": kkey, "achieved": round(ach, 1), "peak": round(peak_alu, 1),

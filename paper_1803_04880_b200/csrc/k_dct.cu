@@ -25,6 +25,7 @@
 
 #include "fused_cta.cuh"
 #include "sha2_device.cuh"
+#include "sha2_spec.cuh"
 #include "tables.h"
 
 namespace se {
@@ -229,12 +230,12 @@ __device__ __forceinline__ void mask_level2(const DctParams& p, uint64_t gr, con
         W[15].lo = 49 * 8;
         const uint64_t st[8] = {p.mid512[0], p.mid512[1], p.mid512[2], p.mid512[3],
                                 p.mid512[4], p.mid512[5], p.mid512[6], p.mid512[7]};
-        sha512_from_round<4>(st, h0, W, H, p.one);
+        sha512_from_round_spec<4, kDctMsgKeyed>(st, h0, W, p.s512, H, p.one);
     } else {                                             // rec9, 9 bytes
         W[0] = W64{r[1], r[0]};
         W[1] = W64{0u, r[2] | 0x00800000u};               // pad at byte 9
         W[15].lo = 9 * 8;
-        sha512_from_round<0>(h0, h0, W, H, p.one);
+        sha512_from_round_spec<0, kDctMsgUnkeyed>(h0, h0, W, p.s512, H, p.one);   // zero words folded
     }
 #pragma unroll
     for (int x = 0; x < 8; ++x) {                        // digest byte 8x+y on pixel (x, y)

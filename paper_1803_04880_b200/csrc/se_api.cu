@@ -140,6 +140,20 @@ static void sched_consts(uint32_t mask, const T w[16], const T* K, S0 s0, S1 s1,
     for (int t = 0; t < 32; ++t) kw[t] = var(t) ? 0 : (T)(K[t] + W[t]);
 }
 
+// level-2 DCT mask (k_dct.cu): the 9-byte record alone, or K||IV||be64(r)||rec9
+void dct_sched_consts(DctParams& p, bool keyed) {
+    uint64_t w[16] = {0};
+    if (keyed) {
+        for (int i = 0; i < 4; ++i) w[i] = (uint64_t)p.kiv[2 * i] << 32 | p.kiv[2 * i + 1];
+        w[6] = 0x80ull << 48;                    // pad at byte 49 (a record word; kept for clarity)
+        w[15] = 49 * 8;
+        sched_consts<uint64_t>(kDctMsgKeyed, w, kK512, s0_512, s1_512, p.s512.c, p.s512.kw);
+    } else {
+        w[15] = 9 * 8;
+        sched_consts<uint64_t>(kDctMsgUnkeyed, w, kK512, s0_512, s1_512, p.s512.c, p.s512.kw);
+    }
+}
+
 static void fill_sched(FusedParams& p, const se_layout& lay) {
     const int L = lay.b_bits == 0 ? 1 : 2;       // L = 1: the C mask hashes A; else B', B from A
     // SHA-512 of the C mask: K||IV||be64(b)||record, record = B' (L >= 2) or A (L = 1)

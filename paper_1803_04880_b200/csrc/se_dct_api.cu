@@ -74,7 +74,10 @@ int dct_protect(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
     p.in = (const uint8_t*)d_in;
     p.out = (uint8_t*)d_p;
     p.a = (uint8_t*)d_a;
-    if (g->level == 2) sha512_kiv(key, iv, p.kiv, p.mid512, p.h512);
+    if (g->level == 2) {
+        sha512_kiv(key, iv, p.kiv, p.mid512, p.h512);
+        dct_sched_consts(p, (g->flags & SE_DCT_KEYED) != 0);
+    }
     if (launch_ks(key, iv, g, p.a, lay.a_bytes, stream)) return SE_ECUDA;
     return launch_dct(p, g->channels, g->level, (g->flags & SE_DCT_KEYED) != 0, 0, stream) ? SE_ECUDA : SE_OK;
 }
@@ -90,7 +93,10 @@ int dct_recover(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
     p.in = (const uint8_t*)d_p;
     p.out = (uint8_t*)d_out;
     p.a = (uint8_t*)d_a;
-    if (g->level == 2) sha512_kiv(key, iv, p.kiv, p.mid512, p.h512);
+    if (g->level == 2) {
+        sha512_kiv(key, iv, p.kiv, p.mid512, p.h512);
+        dct_sched_consts(p, (g->flags & SE_DCT_KEYED) != 0);
+    }
     keep_pool();
     cudaStream_t s = (cudaStream_t)stream;
     void* ks = nullptr;

@@ -139,7 +139,13 @@ struct DctParams {
     uint32_t kiv[8];          // K || IV words (KEYED)
     uint64_t mid512[8];       // SHA-512 state after rounds 0..3 over K||IV (KEYED)
     uint64_t h512[8];         // SHA-512 H(0)
+    SchedConst512 s512;       // level-2 mask schedule constants (sha2_spec.cuh)
 };
+// message words of the level-2 hash that depend on the record: unkeyed rec9
+// (words 0, 1), keyed K||IV||be64(r)||rec9 (words 4, 5, 6)
+constexpr uint32_t kDctMsgUnkeyed = 0x3u;
+constexpr uint32_t kDctMsgKeyed = 0x70u;
+void dct_sched_consts(DctParams& p, bool keyed);
 
 // host helpers shared by the API translation units (se_api.cu)
 void cipher_setup(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block, CipherParams& cp);

@@ -63,18 +63,19 @@ __device__ __forceinline__ void sha512_spec_sched(W64 (&S)[8], const W64 (&W)[16
     }
 }
 
-// SHA-512 of one block resuming after round 3 (W[0..3] = K||IV in the host
-// midstate), schedule specialised for message-word mask MSG.  Digest -> H.
-template <uint32_t MSG>
-__device__ __forceinline__ void sha512_from_round4_spec(const uint64_t (&st)[8], const uint64_t (&h0)[8],
-                                                        const W64 (&W)[16], const SchedConst512& sc,
-                                                        uint64_t (&H)[8], uint32_t one) {
+// SHA-512 of one block resuming at round R0 from state st (R0 = 4: W[0..3]
+// = K||IV in the host midstate; R0 = 0: st = H(0)), schedule specialised for
+// message-word mask MSG.  Digest -> H.
+template <int R0, uint32_t MSG>
+__device__ __forceinline__ void sha512_from_round_spec(const uint64_t (&st)[8], const uint64_t (&h0)[8],
+                                                       const W64 (&W)[16], const SchedConst512& sc,
+                                                       uint64_t (&H)[8], uint32_t one) {
     constexpr uint64_t V = sched_var(MSG);
     static_assert(((V >> 32) & 0xffffffffull) == 0xffffffffull, "t >= 32 must be block-dependent");
     W64 S[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) S[(i - 4) & 7] = w64(st[i]);
-    sha512_spec_msg<V, 4>(S, W, sc, one);
+    for (int i = 0; i < 8; ++i) S[(i - R0) & 7] = w64(st[i]);
+    sha512_spec_msg<V, R0>(S, W, sc, one);
     W64 N[16];                                               // W_16 .. W_31
     sha512_spec_sched<V, 16>(S, W, N, sc, one);
 #pragma unroll 1
@@ -125,6 +126,13 @@ __device__ __forceinline__ void sha256_spec_sched(uint32_t (&S)[8], const uint32
         sha256_round<T>(S, kw, one);
         sha256_spec_sched<V, T + 1>(S, W, N, sc, one);
     }
+}
+
+template <uint32_t MSG>
+__device__ __forceinline__ void sha512_from_round4_spec(const uint64_t (&st)[8], const uint64_t (&h0)[8],
+                                                        const W64 (&W)[16], const SchedConst512& sc,
+                                                        uint64_t (&H)[8], uint32_t one) {
+    sha512_from_round_spec<4, MSG>(st, h0, W, sc, H, one);
 }
 
 // SHA-256 resuming after round 7 (W[0..7] = K||IV in the host midstate).
