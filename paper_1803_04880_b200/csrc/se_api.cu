@@ -449,7 +449,7 @@ int fragment_protect_stripe(const se_geom* g, const se_stripe* st, const uint8_t
     int rc = stripe_checks(g, st, key, iv, lay, false);
     if (rc) return rc;
     if (!d_in || !d_a || !d_c || (lay.b_bits && !d_b)) return SE_EINVAL;
-    if (!aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
+    if (!aligned16(d_in) || !aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
     FusedParams p;
     stripe_fused(p, g, lay, key, iv, st->row_begin, st->row_end);
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
