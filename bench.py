@@ -667,7 +667,8 @@ def run_dct(args):
     peaks, peak_src = load_peaks()
     ms_step = tp + tr
     dom_name, dom_ms = ("k_dct_protect", tp) if tp >= tr else ("k_dct_recover", tr)
-    kkey = f"{dom_name}<1, {level}, {1 if flags else 0}>"
+    aesf = 1 if (dom_name == "k_dct_recover" or level == 1) else 0   # AES inside the kernel (k_dct.cu)
+    kkey = f"{dom_name}<1, {level}, {1 if flags else 0}, {aesf}>"
     traffic, traffic_src = load_traffic(kkey)
     alg_bytes = 2 * n + lay["a_bytes"]
     if level == 2:

@@ -72,15 +72,15 @@ typedef struct {
 int dct_layout(const se_dct_geom* g, se_dct_layout* out);
 
 /* Protect one image: d_in (p_bytes) -> d_a (a_bytes, encrypted Fragment 1)
- * and d_p (p_bytes, Fragment 2, masked at level 2).  Two kernel launches (the
- * AES-CTR keystream into d_a, then the fused DCT kernel).  d_in must not
- * alias d_a or d_p. */
+ * and d_p (p_bytes, Fragment 2, masked at level 2).  Level 1: one kernel
+ * (DCT, records and their AES-CTR); level 2: the AES-CTR keystream into d_a,
+ * then the DCT + SHA-512 kernel.  d_in must not alias d_a or d_p. */
 int dct_protect(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in,
                 void* d_a, void* d_p, void* stream);
 
 /* Rebuild the image from both fragments into d_out (p_bytes).  Lossy by
- * design (see above); a wrong key yields a wrong image, not an error.  Uses
- * a_bytes of stream-ordered pool scratch for the keystream. */
+ * design (see above); a wrong key yields a wrong image, not an error.  One
+ * kernel (AES-CTR of Fragment 1 inside). */
 int dct_recover(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
                 const void* d_p, void* d_out, void* stream);
 

@@ -284,13 +284,36 @@ __device__ __forceinline__ void recover_layer(const DctParams& p, const uint32_t
     store_rows<C, CH>(p.out, p.width, br, bc, pw);
 }
 
-template <int C, int LEVEL, bool KEYED>
+// AESF: the AES-CTR of Fragment 1 runs in this kernel (the CTA's A slice is
+// 66*C whole counter blocks; 5 KB T-tables in shared memory), no keystream
+// kernel.  Otherwise the keystream comes from k_cipher_ctr (programmatic
+// launch) and is XORed at the copy-out.
+#ifndef SE_DCT_FUSED_AES
+#define SE_DCT_FUSED_AES 1
+#endif
+
+template <int C>
+__device__ __forceinline__ void xor_keystream(const DctParams& p, const AesSmem& aes, uint32_t* sa, uint64_t a0,
+                                              uint64_t alen, int tid) {
+    const uint32_t nblk = (uint32_t)((alen + 15) / 16);
+    for (uint32_t j = tid; j < nblk; j += kBlocksPerCta) {
+        uint32_t x[4];
+        ctr_add(p.ctr, a0 / 16 + j, x);
+        aes128_block(aes, p.rk, x);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sa[4 * j + k] ^= bswap32(x[k]);
+    }
+}
+
+template <int C, int LEVEL, bool KEYED, bool AESF>
 __global__ void __launch_bounds__(kBlocksPerCta) k_dct_protect(const DctParams p) {
     constexpr int SA_W = DctCta<C>::kSaWords;
     __shared__ __align__(16) uint32_t sa[SA_W];
+    __shared__ AesSmem aes;
     const int tid = threadIdx.x;
     const uint64_t pos = (uint64_t)blockIdx.x * kBlocksPerCta + tid;
     for (int i = tid; i < SA_W; i += kBlocksPerCta) sa[i] = 0;
+    if constexpr (AESF) aes_load_tables(aes, tid, kBlocksPerCta);
     __syncthreads();
     if (pos < p.n_pos) {
         const uint64_t br = pos / p.bpr, bc = pos - br * p.bpr;
@@ -303,25 +326,39 @@ __global__ void __launch_bounds__(kBlocksPerCta) k_dct_protect(const DctParams p
     }
     __syncthreads();
     const uint64_t a0 = (uint64_t)blockIdx.x * SA_W * 4;
-    asm volatile("griddepcontrol.wait;" ::: "memory");          // keystream kernel complete
-    copy_s2g_xor_global(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
+    const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
+    if constexpr (AESF) {
+        xor_keystream<C>(p, aes, sa, a0, alen, tid);                  // Fragment 1 encrypted
+        __syncthreads();
+        copy_s2g(p.a + a0, sa, alen, tid);
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");          // keystream kernel complete
+        copy_s2g_xor_global(p.a + a0, sa, alen, tid);
+    }
 }
 
-template <int C, int LEVEL, bool KEYED>
+template <int C, int LEVEL, bool KEYED, bool AESF>
 __global__ void __launch_bounds__(kBlocksPerCta) k_dct_recover(const DctParams p) {
     constexpr int SA_W = DctCta<C>::kSaWords;
     __shared__ __align__(16) uint32_t sa[SA_W];
+    __shared__ AesSmem aes;
     const int tid = threadIdx.x;
     const uint64_t pos = (uint64_t)blockIdx.x * kBlocksPerCta + tid;
     const uint64_t a0 = (uint64_t)blockIdx.x * SA_W * 4;
     const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
     copy_g2s(sa, p.a + a0, alen, SA_W * 4, tid);
+    if constexpr (AESF) aes_load_tables(aes, tid, kBlocksPerCta);
     const bool valid = pos < p.n_pos;
     const uint64_t br = valid ? pos / p.bpr : 0, bc = valid ? pos - br * p.bpr : 0;
     uint32_t w[8][2 * C];
     if (valid) load_rows<C>(p.in, p.width, br, bc, w);
-    asm volatile("griddepcontrol.wait;" ::: "memory");          // keystream kernel complete
-    xor_g2s(sa, p.ks + a0, alen, tid);
+    if constexpr (AESF) {
+        __syncthreads();
+        xor_keystream<C>(p, aes, sa, a0, alen, tid);                  // Fragment 1 decrypted
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");          // keystream kernel complete
+        xor_g2s(sa, p.ks + a0, alen, tid);
+    }
     __syncthreads();
     if (valid) {
         recover_layer<C, 0, LEVEL, KEYED>(p, w, pos, br, bc, sa, tid);
@@ -492,8 +529,13 @@ __global__ void __launch_bounds__(kBlocksPerCta) k_dct8_inv(const DctParams p) {
 
 template <int C, int LEVEL, bool KEYED>
 void launch_c(const DctParams& p, int op, unsigned grid, cudaStream_t s) {
-    if (op == 0) launch_pdl(k_dct_protect<C, LEVEL, KEYED>, grid, kBlocksPerCta, s, p);
-    else launch_pdl(k_dct_recover<C, LEVEL, KEYED>, grid, kBlocksPerCta, s, p);
+    if (dct_fused_aes(op, LEVEL)) {
+        if (op == 0) k_dct_protect<C, LEVEL, KEYED, true><<<grid, kBlocksPerCta, 0, s>>>(p);
+        else k_dct_recover<C, LEVEL, KEYED, true><<<grid, kBlocksPerCta, 0, s>>>(p);
+    } else {
+        if (op == 0) launch_pdl(k_dct_protect<C, LEVEL, KEYED, false>, grid, kBlocksPerCta, s, p);
+        else launch_pdl(k_dct_recover<C, LEVEL, KEYED, false>, grid, kBlocksPerCta, s, p);
+    }
 }
 
 template <int C>
@@ -507,6 +549,14 @@ void launch_level(const DctParams& p, uint32_t level, bool keyed, int op, unsign
 }
 
 }  // namespace
+
+// Measured (4800x4800): the fused AES pays off where the kernel has issue
+// slots to spare (level 1, and recovery, which also skips the keystream
+// scratch), not in the ALU-bound level-2 protect (100.4 vs 97.3 us).
+bool dct_fused_aes(int op, uint32_t level) {
+    if (!SE_DCT_FUSED_AES) return false;
+    return op == 1 || level == 1;
+}
 
 int launch_dct(const DctParams& p, uint32_t channels, uint32_t level, bool keyed, int op, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;

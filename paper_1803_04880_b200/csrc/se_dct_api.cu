@@ -48,6 +48,14 @@ static int launch_ks(const uint8_t key[16], const uint8_t iv[16], const se_dct_g
     return launch_cipher_ctr(cp, stream);
 }
 
+static void aes_params(DctParams& p, const uint8_t key[16], const uint8_t iv[16], const se_dct_geom* g) {
+    CipherParams cp;
+    memset(&cp, 0, sizeof cp);
+    cipher_setup(key, iv, g->block_offset * 66 / 128, cp);
+    memcpy(p.ctr, cp.ctr, sizeof p.ctr);
+    memcpy(p.rk, cp.rk, sizeof p.rk);
+}
+
 extern "C" {
 
 int dct_layout(const se_dct_geom* g, se_dct_layout* out) {
@@ -78,7 +86,8 @@ int dct_protect(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
         sha512_kiv(key, iv, p.kiv, p.mid512, p.h512);
         dct_sched_consts(p, (g->flags & SE_DCT_KEYED) != 0);
     }
-    if (launch_ks(key, iv, g, p.a, lay.a_bytes, stream)) return SE_ECUDA;
+    aes_params(p, key, iv, g);
+    if (!dct_fused_aes(0, g->level) && launch_ks(key, iv, g, p.a, lay.a_bytes, stream)) return SE_ECUDA;
     return launch_dct(p, g->channels, g->level, (g->flags & SE_DCT_KEYED) != 0, 0, stream) ? SE_ECUDA : SE_OK;
 }
 
@@ -97,6 +106,9 @@ int dct_recover(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
         sha512_kiv(key, iv, p.kiv, p.mid512, p.h512);
         dct_sched_consts(p, (g->flags & SE_DCT_KEYED) != 0);
     }
+    aes_params(p, key, iv, g);
+    if (dct_fused_aes(1, g->level))
+        return launch_dct(p, g->channels, g->level, (g->flags & SE_DCT_KEYED) != 0, 1, stream) ? SE_ECUDA : SE_OK;
     keep_pool();
     cudaStream_t s = (cudaStream_t)stream;
     void* ks = nullptr;

@@ -140,7 +140,12 @@ struct DctParams {
     uint64_t mid512[8];       // SHA-512 state after rounds 0..3 over K||IV (KEYED)
     uint64_t h512[8];         // SHA-512 H(0)
     SchedConst512 s512;       // level-2 mask schedule constants (sha2_spec.cuh)
+    uint32_t ctr[4];          // Fragment-1 AES-CTR: IV + block_offset*66/128 (fused AES)
+    uint32_t rk[44];          // AES-128 round keys
 };
+// whether the DCT kernel of `op` (0 protect, 1 recover) runs the AES of
+// Fragment 1 itself (k_dct.cu) instead of a keystream kernel before it
+bool dct_fused_aes(int op, uint32_t level);
 // message words of the level-2 hash that depend on the record: unkeyed rec9
 // (words 0, 1), keyed K||IV||be64(r)||rec9 (words 4, 5, 6)
 constexpr uint32_t kDctMsgUnkeyed = 0x3u;

@@ -112,7 +112,7 @@ def test_protect_parity(dev, orc, W, H, C, level, flags):
     se.launch_count(reset=True)
     a, p = se.dct_protect(to_dev(x, dev), W, H, C, level, KEY, IV, flags=flags, block_offset=off)
     torch.cuda.synchronize()
-    assert se.launch_count() == 2                                       # keystream + fused DCT kernel
+    assert se.launch_count() == (1 if level == 1 else 2)                # (keystream +) fused DCT kernel
     check_protect(orc, x, W, H, C, level, flags, off, a.cpu().numpy(), p.cpu().numpy())
 
 
@@ -127,7 +127,7 @@ def test_recover_parity(dev, orc, W, H, C, level, flags):
     se.launch_count(reset=True)
     got = se.dct_recover(to_dev(a, dev), to_dev(p, dev), W, H, C, level, KEY, IV, flags=flags,
                          block_offset=off).cpu().numpy()
-    assert se.launch_count() == 2
+    assert se.launch_count() == 1                                       # AES inside the DCT kernel
     n = W * H * C // 64
     g, r = blocks(got, W, H, C).reshape(n, 64), blocks(ref, W, H, C).reshape(n, 64)
     tie = near_half(real, TAU_P)
