@@ -397,8 +397,24 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         smem_get_record<R::CW, R::CBITS>(sc, SC_W, (uint32_t)tid * R::CBITS, C);
         if (MASK && R::BBITS) mask_c<R::BW, R::BBYTES, SPEC>(p, gb, B, C);    // C from B'
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");                      // keystream kernel complete
-    xor_g2s<BPC>(sa, p.ks + a0, alen, tid);                                       // A' -> A
+    if constexpr (!MASK && SE_REC_FUSED_AES) {
+        // unmasked (latency-bound) recovery: decrypt the CTA's A slice - whole
+        // AES counter blocks - here instead of waiting for a keystream kernel
+        __shared__ AesSmem aes;
+        aes_load_tables(aes, tid, BPC);
+        __syncthreads();
+        const uint32_t nblk = (uint32_t)((alen + 15) / 16);
+        for (uint32_t j = tid; j < nblk; j += BPC) {
+            uint32_t x[4];
+            ctr_add(p.ctr, a0 / 16 + j, x);
+            aes128_block(aes, p.rk, x);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sa[4 * j + k] ^= bswap32(x[k]);
+        }
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");                  // keystream kernel complete
+        xor_g2s<BPC>(sa, p.ks + a0, alen, tid);                                   // A' -> A
+    }
     __syncthreads();                                                         // plain A ready
 
     bool bad = false;

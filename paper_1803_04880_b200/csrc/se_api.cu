@@ -355,6 +355,8 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     p.report = d_report;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
+    if (SE_REC_FUSED_AES && !mask && g->mode == SE_MODE_BLOCK8)   // AES inside the kernel (fused_cta.cuh)
+        return launch_recover_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
     // keystream scratch (a_bytes, 7.8% of n at L = 2): the caller's, else the stream-ordered pool
     void* ks = d_ks;
     if (!ks) {
@@ -362,7 +364,7 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
         if (cudaMallocAsync(&ks, lay.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
     }
     p.ks = (const uint8_t*)ks;
-    int e = launch_keystream(p, (uint8_t*)ks, lay.a_bytes, stream);
+    int e = (!mask && SE_REC_FUSED_AES) ? 0 : launch_keystream(p, (uint8_t*)ks, lay.a_bytes, stream);
     if (g->mode == SE_MODE_BLOCK8) {
         if (!e) e = launch_recover_block8(p, g->levels, mask, stream);
         if (!d_ks) cudaFreeAsync(ks, s);
@@ -504,7 +506,7 @@ int fragment_recover_stripe(const se_geom* g, const se_stripe* st, const uint8_t
     dp.out = (uint8_t*)d_out; dp.coef = (int16_t*)ws;
     dp.row0 = st->row_begin; dp.rows_out = st->row_end - st->row_begin;
     dp.src_row0 = e0; dp.src_rows = e1 - e0;
-    int e = launch_keystream(p, (uint8_t*)ks, p.a_bytes, stream);
+    int e = (!mask && SE_REC_FUSED_AES) ? 0 : launch_keystream(p, (uint8_t*)ks, p.a_bytes, stream);
     if (!e) e = launch_recover_full(p, g->levels, mask, stream);             // unmask + scatter (halo too)
     if (!e) e = launch_dwt_full_inv(dp, g->levels, d_report, stream);        // the stripe's rows
     cudaFreeAsync(ws, s);
@@ -617,12 +619,13 @@ static int batch_common(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ct
     const bool mask = !(flags & SE_FLAG_PUBLIC_PLAIN);
     cudaStream_t s = (cudaStream_t)stream;
     void* ks = nullptr;
-    if (recover && total_ctas) {                      // keystream scratch for every file's A stream
+    const bool aes_inside = recover && !mask && SE_REC_FUSED_AES;   // unmasked recovery decrypts in-kernel
+    if (recover && total_ctas && !aes_inside) {       // keystream scratch for every file's A stream
         keep_pool();
         if (cudaMallocAsync(&ks, total_ctas * 16ull * lay.a_bits + 16, s) != cudaSuccess) return SE_ECUDA;
         bp.ks = (uint8_t*)ks;
     }
-    int e = total_ctas ? launch_batch_keystream(bp, lay.a_bits, stream) : 0;
+    int e = (total_ctas && !aes_inside) ? launch_batch_keystream(bp, lay.a_bits, stream) : 0;
     if (!e) e = launch_batch_block8(bp, total_ctas, levels, mask, recover, stream);
     if (ks) cudaFreeAsync(ks, s);
     return e ? SE_ECUDA : SE_OK;

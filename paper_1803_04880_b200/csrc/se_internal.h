@@ -11,6 +11,12 @@ namespace se {
 
 constexpr int kBlocksPerCta = 128;   // one thread per 8x8 block, 128 blocks per CTA
 
+#ifndef SE_REC_FUSED_AES
+#define SE_REC_FUSED_AES 1   // unmasked recover: AES of the A slice inside the fused kernel (measured:
+                             // C2 plain recover 489 -> 532 GB/s; masked recover keeps the keystream
+                             // kernel, 175 vs 171.5 with the AES inside)
+#endif
+
 // ---- message-schedule specialisation of the B / C mask hashes (sha2_spec.cuh)
 // bit t set: schedule word W_t depends on the block (t < 64)
 __host__ __device__ constexpr uint64_t sched_var(uint32_t msg_mask) {
