@@ -343,8 +343,26 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
     // row a9: 128-bit coalesced stores of the CTA's slice of each stream;
     // A' = A ^ keystream on the way out (row a6, XOR half)
     const uint64_t a0 = cta * (BPC / 8ull) * R::ABITS, c0 = cta * (BPC / 8ull) * R::CBITS;
-    asm volatile("griddepcontrol.wait;" ::: "memory");              // keystream kernel complete
-    copy_s2g_xor_global<BPC>(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
+    if constexpr (!MASK && SE_PROT_FUSED_AES) {
+        // unmasked protect: encrypt the CTA's A slice (whole AES counter blocks) here
+        __shared__ AesSmem aes;
+        aes_load_tables(aes, tid, BPC);
+        __syncthreads();
+        const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
+        const uint32_t nblk = (uint32_t)((alen + 15) / 16);
+        for (uint32_t j = tid; j < nblk; j += BPC) {
+            uint32_t x[4];
+            ctr_add(p.ctr, a0 / 16 + j, x);
+            aes128_block(aes, p.rk, x);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sa[4 * j + k] ^= bswap32(x[k]);
+        }
+        __syncthreads();
+        copy_s2g<BPC>(p.a + a0, sa, alen, tid);
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");          // keystream kernel complete
+        copy_s2g_xor_global<BPC>(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
+    }
     if (R::BBITS) {
         const uint64_t b0 = cta * (BPC / 8ull) * R::BBITS;
         copy_s2g<BPC>(p.b + b0, sb, min((uint64_t)SB_W * 4, p.b_bytes - b0), tid);

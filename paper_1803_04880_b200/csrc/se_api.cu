@@ -311,7 +311,7 @@ int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
-        if (launch_keystream(p, p.a, lay.a_bytes, stream)) return SE_ECUDA;
+        if (!(SE_PROT_FUSED_AES && !mask) && launch_keystream(p, p.a, lay.a_bytes, stream)) return SE_ECUDA;
         return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
     }
     keep_pool();
@@ -322,7 +322,7 @@ int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     dp.in = p.in; dp.coef = ws;
     p.ws = ws; p.rows = lay.rows;
     int e = launch_dwt_full_fwd(dp, g->levels, stream);
-    if (!e) e = launch_keystream(p, p.a, lay.a_bytes, stream);
+    if (!e && !(SE_PROT_FUSED_AES && !mask)) e = launch_keystream(p, p.a, lay.a_bytes, stream);
     if (!e) e = launch_protect_full(p, g->levels, mask, stream);
     cudaFreeAsync(ws, s);
     return e ? SE_ECUDA : SE_OK;
@@ -467,7 +467,7 @@ int fragment_protect_stripe(const se_geom* g, const se_stripe* st, const uint8_t
     p.ws = (int16_t*)ws;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     int e = launch_dwt_full_fwd(dp, g->levels, stream);
-    if (!e) e = launch_keystream(p, p.a, p.a_bytes, stream);
+    if (!e && !(SE_PROT_FUSED_AES && !mask)) e = launch_keystream(p, p.a, p.a_bytes, stream);
     if (!e) e = launch_protect_full(p, g->levels, mask, stream);
     cudaFreeAsync(ws, s);
     return e ? SE_ECUDA : SE_OK;
@@ -619,7 +619,7 @@ static int batch_common(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ct
     const bool mask = !(flags & SE_FLAG_PUBLIC_PLAIN);
     cudaStream_t s = (cudaStream_t)stream;
     void* ks = nullptr;
-    const bool aes_inside = recover && !mask && SE_REC_FUSED_AES;   // unmasked recovery decrypts in-kernel
+    const bool aes_inside = !mask && (recover ? SE_REC_FUSED_AES : SE_PROT_FUSED_AES);   // unmasked: in-kernel AES
     if (recover && total_ctas && !aes_inside) {       // keystream scratch for every file's A stream
         keep_pool();
         if (cudaMallocAsync(&ks, total_ctas * 16ull * lay.a_bits + 16, s) != cudaSuccess) return SE_ECUDA;

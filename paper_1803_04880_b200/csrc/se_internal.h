@@ -11,6 +11,9 @@ namespace se {
 
 constexpr int kBlocksPerCta = 128;   // one thread per 8x8 block, 128 blocks per CTA
 
+#ifndef SE_PROT_FUSED_AES
+#define SE_PROT_FUSED_AES 0  // unmasked protect: AES of the A slice inside the fused kernel
+#endif
 #ifndef SE_REC_FUSED_AES
 #define SE_REC_FUSED_AES 1   // unmasked recover: AES of the A slice inside the fused kernel (measured:
                              // C2 plain recover 489 -> 532 GB/s; masked recover keeps the keystream
