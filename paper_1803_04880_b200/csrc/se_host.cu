@@ -44,6 +44,13 @@ struct Chunk {
     uint64_t nblk;
 };
 
+// SE_HOST_RAMP: chunk sizes ramping up at the start and down at the end
+// (1/8, 1/4, 1/2 of the nominal size) to shorten the pipeline's fill and
+// drain.  Measured slower on C2 (11.3 vs 12.5 GB/s at 4 MiB: the per-chunk
+// copy and launch costs of the extra chunks outweigh it), so off.
+#ifndef SE_HOST_RAMP
+#define SE_HOST_RAMP 0
+#endif
 static std::vector<Chunk> make_chunks(const se_geom* g, const se_layout& lay, uint64_t chunk_bytes) {
     const uint64_t bpr = g->width / 8, block_rows = lay.rows / 8;
     const uint64_t ga = chunk_block_align(lay);
@@ -51,15 +58,38 @@ static std::vector<Chunk> make_chunks(const se_geom* g, const se_layout& lay, ui
     const uint64_t row_bytes = 8ull * g->width;
     uint64_t rows_per = std::max<uint64_t>(1, chunk_bytes / row_bytes);
     rows_per = std::max<uint64_t>(unit, rows_per / unit * unit);
+    auto units = [&](uint64_t rows) { return std::max<uint64_t>(unit, rows / unit * unit); };
+    // sizes in block rows: ramp up, full chunks, ramp down
+    std::vector<uint64_t> head, tail;
+    if (SE_HOST_RAMP)
+        for (uint64_t d = 8; d >= 2; d /= 2) head.push_back(units(rows_per / d));
+    uint64_t ramp = 0;
+    for (uint64_t h : head) ramp += 2 * h;
+    std::vector<uint64_t> sizes;
+    if (head.empty() || block_rows < ramp + rows_per) {
+        for (uint64_t br = 0; br < block_rows; br += rows_per) sizes.push_back(std::min(rows_per, block_rows - br));
+    } else {
+        sizes = head;
+        uint64_t mid = block_rows - ramp;
+        while (mid > 0) {
+            const uint64_t r = std::min(rows_per, mid);
+            sizes.push_back(r);
+            mid -= r;
+        }
+        for (auto it = head.rbegin(); it != head.rend(); ++it) sizes.push_back(*it);
+    }
     std::vector<Chunk> v;
-    for (uint64_t br = 0; br < block_rows; br += rows_per) {
-        const uint64_t br1 = std::min(block_rows, br + rows_per);
+    uint64_t br = 0;
+    for (uint64_t r : sizes) {
+        const uint64_t br1 = std::min(block_rows, br + r);
+        if (br1 <= br) break;
         Chunk c;
         c.byte0 = std::min(g->n_bytes, br * row_bytes);
         c.byte1 = std::min(g->n_bytes, br1 * row_bytes);
         c.blk0 = br * bpr;
         c.nblk = (br1 - br) * bpr;
         v.push_back(c);
+        br = br1;
     }
     return v;
 }
