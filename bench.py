@@ -249,9 +249,16 @@ def run_se(args):
         ms_step = total_ms / args.steps
 
     # ---- e2e: same metric with host buffers, H2D/D2H inside the timed region
-    e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, args.e2e_steps, chunk_bytes=args.e2e_chunk_kib << 10,
+    e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags | (se.FLAG_HOST_MAPPED if args.e2e_mapped else 0), dev,
+                  args.e2e_steps, chunk_bytes=args.e2e_chunk_kib << 10,
                   n_streams=args.e2e_streams) if args.e2e_steps > 0 else \
         {"value": None, "unit": "GB/s", "note": "skipped (--e2e-steps 0, profiling runs only)"}
+
+    # the same through the zero-copy host mode (SE_FLAG_HOST_MAPPED: the kernels read and write the
+    # pinned host buffers over PCIe instead of staged copies) - reported next to e2e
+    if args.e2e_steps > 0 and not args.e2e_mapped:
+        e2e["mapped_variant"] = run_e2e(se, torch, x_np, W, L, key, iv, flags | se.FLAG_HOST_MAPPED, dev,
+                                        args.e2e_steps)
 
     # ---- comparator: full-file AES-128-CTR on the same GPU (paper methodology)
     aes_gbs = None
@@ -552,10 +559,13 @@ def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=8 << 
     ms = (time.perf_counter() - t0) * 1e3 / steps
     assert torch.equal(hout, hx) and rep == (-1, 0)
     frag_bytes = lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"]
+    mapped = bool(flags & se.FLAG_HOST_MAPPED)
+    how = ("SE_FLAG_HOST_MAPPED: the kernels read / write the pinned host buffers over PCIe, no staging"
+           if mapped else f"{chunk_bytes >> 10} KiB chunks on {n_streams} streams")
     return {"value": round(n / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n + frag_bytes,
             "d2h_bytes_per_step": frag_bytes + n, "ms_per_step": round(ms, 4),
-            "path": f"fragment_protect_host + fragment_recover_host (C ABI, pinned host buffers, "
-                    f"{chunk_bytes >> 10} KiB chunks on {n_streams} streams), host wall clock"}
+            "path": f"fragment_protect_host + fragment_recover_host (C ABI, pinned host buffers, {how}), "
+                    f"host wall clock"}
 
 
 # ---------------------------------------------------------------- NEXT row f3: Chapter 4 DCT SE
@@ -850,6 +860,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-chunk-kib", type=int, default=4096, help="host-API chunk size (input KiB)")
     ap.add_argument("--e2e-streams", type=int, default=3, help="host-API CUDA streams")
+    ap.add_argument("--e2e-mapped", type=int, default=0, help="1: zero-copy host API (SE_FLAG_HOST_MAPPED)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparator", action="store_true")

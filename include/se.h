@@ -61,8 +61,12 @@ typedef enum {
 enum { SE_MODE_BLOCK8 = 0,   /* per-8x8-block DWT: the paper   */
        SE_MODE_FULL = 1 };   /* whole-matrix Mallat DWT: extension row a11       */
 
-enum { SE_FLAG_PUBLIC_PLAIN = 1u << 0 };  /* skip the SHA masks on B and C:
+enum { SE_FLAG_PUBLIC_PLAIN = 1u << 0,   /* skip the SHA masks on B and C:
                                              measurement mode (C26) */
+       SE_FLAG_HOST_MAPPED = 1u << 1 };  /* *_host calls only (BLOCK8): the
+                                             host buffers are page-locked and the
+                                             kernels read / write them directly
+                                             over PCIe (zero-copy), no staging */
 
 /* block_offset: global index of this input's first 8x8 block inside the
  * logical file (0 for a whole file).  It is the hash nonce base (C16) and

@@ -28,6 +28,7 @@ SE_OK, SE_EINVAL, SE_EALIGN, SE_ECUDA, SE_ENOTSUP = 0, -1, -2, -3, -4
 SE_EFORMAT, SE_EINTEGRITY = -5, -6
 MODE_BLOCK8, MODE_FULL = 0, 1
 FLAG_PUBLIC_PLAIN = 1
+FLAG_HOST_MAPPED = 2      # *_host calls: kernels access the pinned host buffers directly (zero-copy)
 
 
 def sources():

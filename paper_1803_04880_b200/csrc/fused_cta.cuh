@@ -131,6 +131,20 @@ __device__ __forceinline__ void copy_s2g_xor_global(uint8_t* __restrict__ g, con
     for (uint32_t i = nv * 16 + tid; i < len; i += NT) g[i] = sb[i] ^ g[i];
 }
 
+// A' = A ^ KS with the keystream in separate (device) memory: A' is written
+// once, e.g. straight into mapped host memory.
+template <int NT = kBlocksPerCta>
+__device__ __forceinline__ void copy_s2g_xor(uint8_t* __restrict__ g, const uint32_t* s,
+                                             const uint8_t* __restrict__ ks, uint64_t len, int tid) {
+    const uint32_t nv = (uint32_t)(len / 16);
+    for (uint32_t i = tid; i < nv; i += NT) {
+        const uint4 a = reinterpret_cast<const uint4*>(s)[i], k = reinterpret_cast<const uint4*>(ks)[i];
+        reinterpret_cast<uint4*>(g)[i] = make_uint4(a.x ^ k.x, a.y ^ k.y, a.z ^ k.z, a.w ^ k.w);
+    }
+    const uint8_t* sb = reinterpret_cast<const uint8_t*>(s);
+    for (uint32_t i = nv * 16 + tid; i < len; i += NT) g[i] = sb[i] ^ ks[i];
+}
+
 // A = A' ^ KS in shared memory, keystream read from global memory.
 template <int NT = kBlocksPerCta>
 __device__ __forceinline__ void xor_g2s(uint32_t* s, const uint8_t* __restrict__ ks, uint64_t len, int tid) {
@@ -361,7 +375,9 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
         copy_s2g<BPC>(p.a + a0, sa, alen, tid);
     } else {
         asm volatile("griddepcontrol.wait;" ::: "memory");          // keystream kernel complete
-        copy_s2g_xor_global<BPC>(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
+        const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
+        if (p.ks) copy_s2g_xor<BPC>(p.a + a0, sa, p.ks + a0, alen, tid);   // keystream in device scratch
+        else copy_s2g_xor_global<BPC>(p.a + a0, sa, alen, tid);           // keystream already in A'
     }
     if (R::BBITS) {
         const uint64_t b0 = cta * (BPC / 8ull) * R::BBITS;

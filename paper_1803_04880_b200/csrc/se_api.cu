@@ -108,7 +108,7 @@ static int check_geom(const se_geom* g) {
     if (g->width == 0 || g->width % 8) return SE_EINVAL;
     if (g->levels < 1 || g->levels > 3) return SE_EINVAL;
     if (g->mode > SE_MODE_FULL) return SE_EINVAL;
-    if (g->flags & ~(uint32_t)SE_FLAG_PUBLIC_PLAIN) return SE_EINVAL;
+    if (g->flags & ~(uint32_t)(SE_FLAG_PUBLIC_PLAIN | SE_FLAG_HOST_MAPPED)) return SE_EINVAL;
     return SE_OK;
 }
 
@@ -297,8 +297,15 @@ static int16_t* ws_alloc(const se_layout& lay, uint32_t width, cudaStream_t s) {
     return (int16_t*)ws;
 }
 
-int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in,
-                     void* d_a, void* d_b, void* d_c, void* stream) {
+}  // extern "C"
+
+namespace se {
+
+// fragment_protect with an optional device keystream scratch d_ks (>= a_bytes
+// + 16): the keystream goes there and is XORed in on the way out, so A' is
+// written once (used when A' lives in mapped host memory).
+int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in, void* d_a,
+                 void* d_b, void* d_c, void* d_ks, void* stream) {
     se_layout lay;
     int rc = fused_checks(g, key, iv, lay);
     if (rc) return rc;
@@ -309,11 +316,15 @@ int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     fill_fused(p, g, lay, key, iv);
     p.in = (const uint8_t*)d_in;
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
+    p.ks = (const uint8_t*)d_ks;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
-        if (!(SE_PROT_FUSED_AES && !mask) && launch_keystream(p, p.a, lay.a_bytes, stream)) return SE_ECUDA;
+        if (!(SE_PROT_FUSED_AES && !mask) &&
+            launch_keystream(p, d_ks ? (uint8_t*)d_ks : p.a, lay.a_bytes, stream))
+            return SE_ECUDA;
         return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
     }
+    if (d_ks) return SE_ENOTSUP;
     keep_pool();
     cudaStream_t s = (cudaStream_t)stream;
     int16_t* ws = ws_alloc(lay, g->width, s);
@@ -326,6 +337,15 @@ int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
     if (!e) e = launch_protect_full(p, g->levels, mask, stream);
     cudaFreeAsync(ws, s);
     return e ? SE_ECUDA : SE_OK;
+}
+
+}  // namespace se
+
+extern "C" {
+
+int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in,
+                     void* d_a, void* d_b, void* d_c, void* stream) {
+    return protect_impl(g, key, iv, d_in, d_a, d_b, d_c, nullptr, stream);
 }
 
 }  // extern "C"

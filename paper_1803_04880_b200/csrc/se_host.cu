@@ -273,6 +273,18 @@ static int grow(void*& p, size_t& cap, size_t need, HostCtx& c) {
     return SE_OK;
 }
 
+// Mapped (zero-copy) mode: the device address of a page-locked host buffer
+// (with unified addressing it is the host address itself).
+static int mapped_ptr(const void* h, void** d) {
+    *d = nullptr;
+    if (!h) return SE_OK;
+    if (cudaHostGetDevicePointer(d, const_cast<void*>(h), 0) != cudaSuccess) {
+        cudaGetLastError();
+        return SE_EINVAL;                    // not page-locked / not mapped
+    }
+    return SE_OK;
+}
+
 }  // namespace se
 
 using namespace se;
@@ -287,6 +299,25 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
     if (!key || !iv) return SE_EINVAL;
     if (g->n_bytes == 0) return SE_OK;
     if (!h_in || !h_a || !h_c || (lay.b_bytes && !h_b)) return SE_EINVAL;
+    if (g->flags & SE_FLAG_HOST_MAPPED) {      // zero-copy: one pass, the kernels move the bytes over PCIe
+        if (g->mode != SE_MODE_BLOCK8) return SE_ENOTSUP;
+        void *din, *da, *db, *dc;
+        if (mapped_ptr(h_in, &din) || mapped_ptr(h_a, &da) || mapped_ptr(h_b, &db) || mapped_ptr(h_c, &dc))
+            return SE_EINVAL;
+        se_geom g2 = *g;
+        g2.flags &= ~(uint32_t)SE_FLAG_HOST_MAPPED;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        HostCtx& ctx = host_ctx(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        if (ensure(ctx, 1)) return SE_ECUDA;
+        Slot& sl = ctx.slots[0];
+        if (lay.a_bytes + 16 > sl.cap[4]) cudaStreamSynchronize(ctx.streams[0]);
+        if (grow(sl.buf[4], sl.cap[4], lay.a_bytes + 16, ctx)) return SE_ECUDA;   // keystream scratch
+        int st = protect_impl(&g2, key, iv, din, da, db, dc, sl.buf[4], ctx.streams[0]);
+        if (cudaStreamSynchronize(ctx.streams[0]) != cudaSuccess) st = SE_ECUDA;
+        return st;
+    }
     if (chunk_bytes == 0) chunk_bytes = 32ull << 20;
     if (n_streams == 0) n_streams = 3;
     // FULL mode transforms the whole matrix: one chunk
@@ -350,6 +381,40 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
     if (h_report) { h_report->first_bad_block = -1; h_report->bad_blocks = 0; }
     if (g->n_bytes == 0) return SE_OK;
     if (!h_out || !h_a || !h_c || (lay.b_bytes && !h_b)) return SE_EINVAL;
+    if (g->flags & SE_FLAG_HOST_MAPPED) {      // zero-copy recovery
+        if (g->mode != SE_MODE_BLOCK8) return SE_ENOTSUP;
+        void *da, *db, *dc, *dout;
+        if (mapped_ptr(h_a, &da) || mapped_ptr(h_b, &db) || mapped_ptr(h_c, &dc) || mapped_ptr(h_out, &dout))
+            return SE_EINVAL;
+        se_geom g2 = *g;
+        g2.flags &= ~(uint32_t)SE_FLAG_HOST_MAPPED;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        HostCtx& ctx = host_ctx(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        if (ensure(ctx, 1)) return SE_ECUDA;
+        if (ctx.reps_cap < 1) {
+            drop_graphs(ctx);
+            if (cudaMalloc((void**)&ctx.reps, sizeof(se_report)) != cudaSuccess ||
+                cudaMallocHost((void**)&ctx.hreps, sizeof(se_report)) != cudaSuccess ||
+                cudaMallocHost((void**)&ctx.hinit, sizeof(se_report)) != cudaSuccess)
+                return SE_ECUDA;
+            ctx.hinit[0].first_bad_block = -1;
+            ctx.hinit[0].bad_blocks = 0;
+            ctx.reps_cap = 1;
+        }
+        Slot& sl = ctx.slots[0];
+        if (lay.a_bytes + 16 > sl.cap[4]) cudaStreamSynchronize(ctx.streams[0]);
+        if (grow(sl.buf[4], sl.cap[4], lay.a_bytes + 16, ctx)) return SE_ECUDA;
+        cudaStream_t s0 = ctx.streams[0];
+        int st = recover_impl(&g2, key, iv, da, db, dc, dout, ctx.reps, sl.buf[4], false, s0);
+        if (st == SE_OK &&
+            cudaMemcpyAsync(ctx.hreps, ctx.reps, sizeof(se_report), cudaMemcpyDeviceToHost, s0) != cudaSuccess)
+            st = SE_ECUDA;
+        if (cudaStreamSynchronize(s0) != cudaSuccess) st = SE_ECUDA;
+        if (st == SE_OK && h_report) *h_report = ctx.hreps[0];
+        return st;
+    }
     if (chunk_bytes == 0) chunk_bytes = 32ull << 20;
     if (n_streams == 0) n_streams = 3;
     const std::vector<Chunk> chunks = g->mode == SE_MODE_FULL

@@ -97,3 +97,29 @@ def test_graph_replay_reads_new_contents(dev, orc):
     frag[2][60 * 7] ^= 0xFF
     _, rep = se.fragment_recover_host(*frag, n, W, L, KEY, IV, out=out, chunk_bytes=96 * 1024, n_streams=3)
     assert rep == orc.recover(frag[0].numpy(), frag[1].numpy(), frag[2].numpy(), n, W, L, KEY, IV)[1]
+
+
+@pytest.mark.parametrize("L", [1, 2, 3])
+@pytest.mark.parametrize("flags", [0, se.FLAG_PUBLIC_PLAIN])
+def test_host_mapped_zero_copy(dev, orc, L, flags):
+    """SE_FLAG_HOST_MAPPED: the kernels read and write the page-locked host
+    buffers directly (no staging copies): same bytes as the oracle, same report."""
+    n, W = 1024 * 8 * 21 + 777, 1024
+    x = synth.random_bytes(n, 40 + L)
+    fl = flags | se.FLAG_HOST_MAPPED
+    a, b, c = se.fragment_protect_host(host(x), W, L, KEY, IV, flags=fl)
+    oa, ob, oc = orc.protect(x, W, L, KEY, IV, flags=flags)
+    assert np.array_equal(a.numpy(), oa) and np.array_equal(b.numpy(), ob) and np.array_equal(c.numpy(), oc)
+    back, rep = se.fragment_recover_host(a, b, c, n, W, L, KEY, IV, flags=fl)
+    assert np.array_equal(back.numpy(), x) and rep == (-1, 0)
+    c2 = c.clone().pin_memory()                                       # mapped mode needs page-locked buffers
+    c2[60 * 9 + 4] ^= 0xFF
+    back, rep = se.fragment_recover_host(a, b, c2, n, W, L, KEY, IV, flags=fl)
+    oback, orep = orc.recover(oa, ob, c2.numpy(), n, W, L, KEY, IV, flags=flags)
+    assert np.array_equal(back.numpy(), oback) and rep == orep
+
+
+def test_host_mapped_needs_pinned(dev):
+    x = torch.from_numpy(synth.random_bytes(4096, 1))              # pageable
+    with pytest.raises(se.SEError):
+        se.fragment_protect_host(x, 64, 2, KEY, IV, flags=se.FLAG_HOST_MAPPED)
