@@ -77,7 +77,7 @@ def test_layout_full_mode_widths(lib):
 
 
 @pytest.mark.parametrize("W,L,mode,flags", [(0, 2, 0, 0), (12, 2, 0, 0), (8, 0, 0, 0), (8, 4, 0, 0),
-                                            (8, 2, 2, 0), (8, 2, 0, 2)])
+                                            (8, 2, 2, 0), (8, 2, 0, 4)])
 def test_layout_rejects_bad_geometry(lib, W, L, mode, flags):
     with pytest.raises(se.SEError) as e:
         se.fragment_layout(64, W, L, mode, flags)
