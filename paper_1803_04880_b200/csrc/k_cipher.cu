@@ -21,6 +21,10 @@ __global__ void __launch_bounds__(kCipherThreads) k_cipher_ctr(const __grid_cons
     // a dependent kernel launched with programmatic stream serialization may
     // start now; it waits (griddepcontrol.wait) before reading our output
     asm volatile("griddepcontrol.launch_dependents;");
+    if (p.report && blockIdx.x == 0 && threadIdx.x == 0) {
+        p.report->first_bad_block = -1;
+        p.report->bad_blocks = 0;
+    }
     extern __shared__ __align__(16) uint32_t lut[];
     __shared__ AesSmem small;
     if constexpr (LANE) aes_load_lut(lut, threadIdx.x, kCipherThreads);

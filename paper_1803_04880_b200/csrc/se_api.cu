@@ -277,12 +277,14 @@ static DwtParams dwt_params(const se_geom* g, const se_layout& lay) {
 // Row a6, keystream half: AES-128-CTR keystream of the whole A stream
 // (counter base p.ctr) written to `out`; the fused kernel that follows is
 // launched with programmatic stream serialization and XORs it in.
-static int launch_keystream(const FusedParams& p, uint8_t* out, uint64_t n, void* stream) {
+static int launch_keystream(const FusedParams& p, uint8_t* out, uint64_t n, void* stream,
+                            se_report* init_report = nullptr) {
     CipherParams cp;
     memset(&cp, 0, sizeof cp);
     cp.in = nullptr;
     cp.out = out;
     cp.n = n;
+    cp.report = init_report;
     memcpy(cp.ctr, p.ctr, sizeof cp.ctr);
     memcpy(cp.rk, p.rk, sizeof cp.rk);
     return launch_cipher_ctr(cp, stream);
@@ -361,7 +363,11 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     int rc = fused_checks(g, key, iv, lay);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    if (d_report && !report_ready) {   // first_bad_block = -1 (all ones), bad_blocks = 0
+    const bool plain_fused = SE_REC_FUSED_AES && (g->flags & SE_FLAG_PUBLIC_PLAIN) && g->mode == SE_MODE_BLOCK8;
+    // the report ({-1, 0}) is initialised by the keystream kernel in the masked
+    // BLOCK8 path (one fewer stream operation); elsewhere by memsets
+    const bool init_in_ks = d_report && !report_ready && g->n_bytes && g->mode == SE_MODE_BLOCK8 && !plain_fused;
+    if (d_report && !report_ready && !init_in_ks) {
         if (cudaMemsetAsync(&d_report->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
             cudaMemsetAsync(&d_report->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
             return SE_ECUDA;
@@ -384,7 +390,8 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
         if (cudaMallocAsync(&ks, lay.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
     }
     p.ks = (const uint8_t*)ks;
-    int e = (!mask && SE_REC_FUSED_AES) ? 0 : launch_keystream(p, (uint8_t*)ks, lay.a_bytes, stream);
+    int e = (!mask && SE_REC_FUSED_AES) ? 0
+          : launch_keystream(p, (uint8_t*)ks, lay.a_bytes, stream, init_in_ks ? d_report : nullptr);
     if (g->mode == SE_MODE_BLOCK8) {
         if (!e) e = launch_recover_block8(p, g->levels, mask, stream);
         if (!d_ks) cudaFreeAsync(ks, s);

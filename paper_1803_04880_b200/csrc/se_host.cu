@@ -463,15 +463,14 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
             Slot& sl = ctx.slots[k % n_streams];
             const se_layout& cl = cls[k];
             const uint64_t sizes[4] = {cgs[k].n_bytes, cl.a_bytes, cl.b_bytes, cl.c_bytes};
-            if (cudaMemcpyAsync(ctx.reps + k, ctx.hinit + k, sizeof(se_report), cudaMemcpyHostToDevice, s) !=
-                cudaSuccess)
-                return SE_ECUDA;
             for (int i = 0; i < 3; ++i)
                 if (sizes[i + 1] && cudaMemcpyAsync(sl.buf[i + 1], hin[i] + c.blk0 * bits[i] / 8, sizes[i + 1],
                                                     cudaMemcpyHostToDevice, s) != cudaSuccess)
                     return SE_ECUDA;
+            // report_ready = false: the chunk's report is initialised by its keystream kernel
+            // (or memsets on the unmasked path) - no host-to-device copy per chunk
             int st = recover_impl(&cgs[k], key, iv, sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr, sl.buf[3],
-                                  sl.buf[0], ctx.reps + k, sl.buf[4], true, s);
+                                  sl.buf[0], ctx.reps + k, sl.buf[4], false, s);
             if (st) return st;
             if (cudaMemcpyAsync((uint8_t*)h_out + c.byte0, sl.buf[0], sizes[0], cudaMemcpyDeviceToHost, s) !=
                     cudaSuccess ||

@@ -110,6 +110,8 @@ struct CipherParams {
     uint32_t rk[44];
     uint32_t lane_lut;        // keystream (in == nullptr) with the 64 KB lane table
     uint32_t pad_;
+    se_report* report;        // nullable: initialised to {-1, 0} by this kernel (the fused recover
+                              // kernel that follows updates it only after griddepcontrol.wait)
 };
 
 struct DwtParams {
