@@ -9,6 +9,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "se_internal.h"
 #include "../../include/se_container.h"
@@ -210,6 +212,39 @@ void keep_pool() {
     done_dev = dev;
 }
 
+// Keystream scratch for recovery, cached per (device, stream): calls on one
+// stream are ordered, so they can share a buffer (grown with cudaFreeAsync /
+// cudaMallocAsync on that stream); the stream id (cudaStreamGetId) is never
+// reused, unlike the handle.  Bounded: past 64 streams the cache is flushed
+// after a device synchronisation.
+void* ks_scratch(cudaStream_t s, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    unsigned long long sid = 0;
+    if (cudaStreamGetId(s, &sid) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    static std::mutex m;
+    static std::map<std::pair<int, unsigned long long>, std::pair<void*, size_t>> cache;
+    std::lock_guard<std::mutex> lock(m);
+    if (cache.size() > 64) {
+        cudaDeviceSynchronize();
+        for (auto& kv : cache) cudaFree(kv.second.first);
+        cache.clear();
+    }
+    auto& e = cache[{dev, sid}];
+    if (e.second < bytes) {
+        if (e.first) cudaFreeAsync(e.first, s);
+        keep_pool();
+        e = {nullptr, 0};
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
+        e = {p, bytes};
+    }
+    return e.first;
+}
+
 }  // namespace se
 
 using namespace se;
@@ -384,11 +419,9 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     if (SE_REC_FUSED_AES && !mask && g->mode == SE_MODE_BLOCK8)   // AES inside the kernel (fused_cta.cuh)
         return launch_recover_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
     // keystream scratch (a_bytes, 7.8% of n at L = 2): the caller's, else the stream-ordered pool
-    void* ks = d_ks;
-    if (!ks) {
-        keep_pool();
-        if (cudaMallocAsync(&ks, lay.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
-    }
+    void* ks = d_ks ? d_ks : ks_scratch(s, lay.a_bytes + 16);
+    if (!ks) return SE_ECUDA;
+    d_ks = ks;                                    // cached per stream: nothing to free below
     p.ks = (const uint8_t*)ks;
     int e = (!mask && SE_REC_FUSED_AES) ? 0
           : launch_keystream(p, (uint8_t*)ks, lay.a_bytes, stream, init_in_ks ? d_report : nullptr);

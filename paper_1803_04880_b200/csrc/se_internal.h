@@ -167,6 +167,7 @@ void dct_sched_consts(DctParams& p, bool keyed);
 void cipher_setup(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block, CipherParams& cp);
 void sha512_kiv(const uint8_t key[16], const uint8_t iv[16], uint32_t kiv[8], uint64_t mid[8], uint64_t h0[8]);
 void keep_pool();
+void* ks_scratch(cudaStream_t s, size_t bytes);     // per-stream cached recovery keystream scratch
 int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in, void* d_a,
                  void* d_b, void* d_c, void* d_ks, void* stream);
 int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a, const void* d_b,
