@@ -795,9 +795,14 @@ def cpu_baseline(x_np, W, L, key, iv, flags, seconds):
     reps = max(1, min(50, int(want // nb)))
     done, dt = oracle_time(x_np, W, L, key, iv, flags, nb, threads, reps)
     gbs = done * 64 / dt / 1e9
+    # the same on one core (SURVEY.md §8.1 row d: 1 core and all host cores), a ~3 s sample
+    nb1 = int(min(total_nb, max(128, rate / threads * 3.0)))
+    done1, dt1 = oracle_time(x_np, W, L, key, iv, flags, nb1, 1)
     return {"value": round(gbs, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
             "sample": f"{reps} pass(es) over the first {nb} of {total_nb} 8x8 blocks of the same input "
                       f"(protect+recover), {threads} host threads, {dt:.1f} s",
+            "one_core": {"value": round(done1 * 64 / dt1 / 1e9, 6), "unit": "GB/s", "cores": 1,
+                         "sample": f"first {nb1} blocks, {dt1:.1f} s"},
             "host_cpu": cpu_model()}
 
 
