@@ -120,3 +120,25 @@ def test_dct_layout_rejects_bad_geometry(lib, W, H, C, level, flags, off):
     with pytest.raises(se.SEError) as e:
         se.dct_layout(W, H, C, level, flags, off)
     assert e.value.status == se.SE_EINVAL
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libse.so the package raises instead of
+    computing anything (run in a subprocess so the loaded library is untouched)."""
+    import sys
+    code = ("import paper_1803_04880_b200 as se\n"
+            "try:\n    se.lib()\nexcept RuntimeError as e:\n    print('raised', e)\n")
+    env = dict(os.environ, SE_LIB_PATH=str(tmp_path / "missing.so"), PYTHONPATH=ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
+    assert "raised" in out.stdout and "not built" in out.stdout
+
+
+def test_product_never_imports_the_oracle():
+    """The product package and its sources do not reference oracle/ (the
+    oracle is test infrastructure only)."""
+    pkg = os.path.join(ROOT, "paper_1803_04880_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "oracle.h" not in src and "liboracle" not in src, f
