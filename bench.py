@@ -152,6 +152,36 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- distributed plumbing
 
+def init_dist(local: int):
+    """One process per GPU over NCCL (barrier + max-over-ranks timing only).
+    SE_BENCH_TEST_GLOO=1 (test only): gloo, ranks sharing the visible GPUs
+    round-robin - exercises the multi-rank code path on a one-GPU box; the
+    ranks' kernels never wait on one another (independent inputs)."""
+    import torch
+    import torch.distributed as dist
+    if os.environ.get("SE_BENCH_TEST_GLOO") == "1":
+        dev = torch.device(f"cuda:{local % torch.cuda.device_count()}")
+        torch.cuda.set_device(dev)
+        dist.init_process_group("gloo")
+        return dev
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    dist.init_process_group("nccl", device_id=dev)
+    return dev
+
+
+def allreduce_max(t):
+    """In-place max over ranks of a small float64 tensor (CPU hop for gloo)."""
+    import torch.distributed as dist
+    if dist.get_backend() == "gloo":
+        c = t.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        t.copy_(c)
+    else:
+        allreduce_max(t)
+    return t
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -174,10 +204,7 @@ def run_se(args):
     import paper_1803_04880_b200 as se
 
     rank, world, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    dev = torch.device(f"cuda:{local}")
+    dev = init_dist(local) if world > 1 else torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     se.lib()
     c, x_np = workload(args.config)
@@ -208,7 +235,7 @@ def run_se(args):
     assert torch.equal(out, x), "recover(protect(x)) != x in the timed configuration"
     assert rep.cpu().tolist() == [-1, 0]
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev.index if dev.index is not None else local)
     clocks.start()
     # warm-up: at least W steps and ~1 s of sustained load (clock sampling)
     t_end = time.time() + args.soak
@@ -244,7 +271,7 @@ def run_se(args):
     ms_step = total_ms / args.steps
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce_max(t)
         total_ms = float(t.item())
         ms_step = total_ms / args.steps
 
@@ -377,10 +404,7 @@ def run_multi(args):
     from paper_1803_04880_b200 import shard
 
     rank, world, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    dev = torch.device(f"cuda:{local}")
+    dev = init_dist(local) if world > 1 else torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     se.lib()
     key, L = synth.KEY, 2
@@ -478,7 +502,7 @@ def run_multi(args):
     recover()
     torch.cuda.synchronize()
     assert check(), "recover(protect(x)) != x"
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev.index if dev.index is not None else local)
     clocks.start()
     i, t_end = 0, time.time() + args.soak          # >= W steps and ~soak s of load for the clock samples
     while i < args.warmup or time.time() < t_end:
@@ -504,7 +528,7 @@ def run_multi(args):
     t_r = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
     t = torch.tensor([t_p + t_r, t_p, t_r], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce_max(t)
         dist.destroy_process_group()
     if rank != 0:
         return None
