@@ -31,8 +31,15 @@ template <int L>
 struct FullTile {
     static constexpr int H = L == 1 ? 4 : L == 2 ? 8 : 16;   // >= 2(2^L - 1), multiple of 2^L and of 4
     static constexpr int SR = kTileR + 2 * H, SC = kTileC + 2 * H;
-    static constexpr int P = SC + 1;                          // odd pitch: row and column chunks hit distinct banks
-    static constexpr size_t smem = (size_t)SR * P * sizeof(int);
+    // the grid sits inside a margin of 2 s_max samples before and s_max + 1
+    // after it (s_max = 2^(L-1)), so a lifting chunk's edge loads (forward
+    // m = -2..8, inverse m = -1..9) never leave shared memory and need no
+    // bounds test (values there only feed halo outputs)
+    static constexpr int S_MAX = 1 << (L - 1), PAD_LO = 2 * S_MAX, PAD_HI = S_MAX + 1;
+    static constexpr int P = (SC + PAD_LO + PAD_HI) | 1;      // odd pitch: row / column chunks in distinct banks
+    static constexpr int ROWS = SR + PAD_LO + PAD_HI;
+    static constexpr int OFF = PAD_LO * P + PAD_LO;           // grid origin inside the buffer
+    static constexpr size_t smem = (size_t)ROWS * P * sizeof(int);
 };
 
 // One lifting pass of level spacing s along one direction of the tile
@@ -59,17 +66,17 @@ __device__ __forceinline__ void lift_pass(int* g, int R0, int C0, int R, int W) 
     constexpr int m0 = INV ? -1 : -2;                          // first loaded sample
     const int O = DIR == 0 ? C0 : R0, N = DIR == 0 ? W : R;    // along: global origin, extent
     const int Oa = DIR == 0 ? R0 : C0, Na = DIR == 0 ? R : W;  // across
+    static_assert(INV ? (s <= T::PAD_LO && s + 1 <= T::PAD_HI) : (2 * s <= T::PAD_LO && 1 <= T::PAD_HI),
+                  "margin must cover the chunk edge loads");
     int v[iters][11];
 #pragma unroll
     for (int it = 0; it < iters; ++it) {
         const int idx = threadIdx.x + it * kFullThreads;
         const int a = (idx % nA) * s, j0 = (idx / nA) * 8 * s;
         const int base = DIR == 0 ? a * T::P + j0 : j0 * T::P + a;
+        const bool live = (items % kFullThreads == 0 || it + 1 < iters) || idx < items;
 #pragma unroll
-        for (int q = 0; q < 11; ++q) {
-            const int j = j0 + (q + m0) * s;
-            v[it][q] = (idx < items && j >= 0 && j < span) ? g[base + (q + m0) * step] : 0;
-        }
+        for (int q = 0; q < 11; ++q) v[it][q] = live ? g[base + (q + m0) * step] : 0;   // margin: no bounds test
     }
     __syncthreads();
 #pragma unroll
@@ -82,6 +89,23 @@ __device__ __forceinline__ void lift_pass(int* g, int R0, int C0, int R, int W) 
         const int base = DIR == 0 ? a * T::P + j0 : j0 * T::P + a;
         const int G0 = O + j0;                                 // global coordinate of m = 0
         int* x = v[it] - m0;                                   // x[m], m = m0 .. m0 + 10
+        if (G0 - 2 * s >= 0 && G0 + 8 * s < N) {
+            // interior chunk (every tile but those on the matrix border): no reflection, no store test
+            if constexpr (!INV) {
+#pragma unroll
+                for (int m = -1; m <= 7; m += 2) x[m] -= (x[m - 1] + x[m + 1]) >> 1;
+#pragma unroll
+                for (int m = 0; m <= 6; m += 2) x[m] += (x[m - 1] + x[m + 1] + 2) >> 2;
+            } else {
+#pragma unroll
+                for (int m = 0; m <= 8; m += 2) x[m] -= (x[m - 1] + x[m + 1] + 2) >> 2;
+#pragma unroll
+                for (int m = 1; m <= 7; m += 2) x[m] += (x[m - 1] + x[m + 1]) >> 1;
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) g[base + m * step] = x[m];
+            continue;
+        }
         if constexpr (!INV) {
             // predict (Eq. 5.1) at odd m = -1, 1, 3, 5, 7; right neighbour reflected at the border
 #pragma unroll
@@ -121,6 +145,21 @@ __device__ __forceinline__ void lift_pass(int* g, int R0, int C0, int R, int W) 
     __syncthreads();
 }
 
+// Zero the margin around the grid (keeps the unused edge arithmetic defined).
+template <int L>
+__device__ __forceinline__ void zero_margin(int* buf) {
+    using T = FullTile<L>;
+    constexpr int top = T::PAD_LO * T::P, bot0 = (T::PAD_LO + T::SR) * T::P;
+    constexpr int side = T::P - T::SC;                          // margin columns per grid row
+    for (int i = threadIdx.x; i < top + T::PAD_LO; i += kFullThreads) buf[i] = 0;   // + row 0's left margin
+    for (int i = threadIdx.x; i < T::ROWS * T::P - bot0; i += kFullThreads) buf[bot0 + i] = 0;
+    for (int i = threadIdx.x; i < T::SR * side; i += kFullThreads) {
+        const int r = i / side, c = i % side;                   // columns [SC, P) then wrap to [0, PAD_LO)
+        const int col = T::PAD_LO + T::SC + c;                  // right margin + left margin of the next row
+        buf[(T::PAD_LO + r) * T::P + col] = 0;
+    }
+}
+
 // All levels, forward (l = 1..L: rows then columns) / inverse (l = L..1:
 // columns then rows); the spacing s = 2^(l-1) is a compile-time constant.
 template <int L, int l>
@@ -154,7 +193,9 @@ __device__ __forceinline__ void for_each_band(F&& f) {
 template <int L>
 __global__ void __launch_bounds__(kFullThreads) k_dwt_full_fwd(const __grid_constant__ DwtParams p) {
     using T = FullTile<L>;
-    extern __shared__ int g[];
+    extern __shared__ int g_buf[];
+    int* g = g_buf + T::OFF;                                    // grid origin inside the margin
+    zero_margin<L>(g_buf);
     const int W = (int)p.width, R = (int)p.rows;
     const int row0 = (int)p.row0, row_end = min((int)(p.row0 + p.rows_out), R);
     const int s0 = (int)p.src_row0, s1 = (int)(p.src_row0 + p.src_rows);
@@ -208,7 +249,9 @@ template <int L>
 __global__ void __launch_bounds__(kFullThreads) k_dwt_full_inv(const __grid_constant__ DwtParams p,
                                                                se_report* report) {
     using T = FullTile<L>;
-    extern __shared__ int g[];
+    extern __shared__ int g_buf[];
+    int* g = g_buf + T::OFF;                                    // grid origin inside the margin
+    zero_margin<L>(g_buf);
     __shared__ unsigned int s_badmask[(kTileR / 8) * (kTileC / 8) / 32];
     const int W = (int)p.width, R = (int)p.rows;
     const int row0 = (int)p.row0, row_end = min((int)(p.row0 + p.rows_out), R);
