@@ -465,8 +465,11 @@ __device__ __forceinline__ void dct8_layer(const DctParams& p, const uint32_t (&
     }
 }
 
+#ifndef SE_DCT8_MINB
+#define SE_DCT8_MINB 1
+#endif
 template <int C>
-__global__ void __launch_bounds__(kBlocksPerCta) k_dct8_fwd(const DctParams p) {
+__global__ void __launch_bounds__(kBlocksPerCta, SE_DCT8_MINB) k_dct8_fwd(const DctParams p) {
     const uint64_t pos = (uint64_t)blockIdx.x * kBlocksPerCta + threadIdx.x;
     if (pos >= p.n_pos) return;
     const uint64_t br = pos / p.bpr, bc = pos - br * p.bpr;
@@ -517,7 +520,7 @@ __device__ __forceinline__ void idct8_layer(const DctParams& p, uint64_t br, uin
 }
 
 template <int C>
-__global__ void __launch_bounds__(kBlocksPerCta) k_dct8_inv(const DctParams p) {
+__global__ void __launch_bounds__(kBlocksPerCta, SE_DCT8_MINB) k_dct8_inv(const DctParams p) {
     const uint64_t pos = (uint64_t)blockIdx.x * kBlocksPerCta + threadIdx.x;
     if (pos >= p.n_pos) return;
     const uint64_t br = pos / p.bpr, bc = pos - br * p.bpr;
