@@ -3,7 +3,7 @@
 // comparator).  Lane-replicated T-table in 64 KB of
 // dynamic shared memory (conflict-free lookups, se_device.cuh); one 16-byte
 // counter block per thread per iteration, 128-bit coalesced loads/stores,
-// grid sized to whole waves of the 148 SMs (3 CTAs of 256 threads per SM).
+// grid sized to whole waves of the 148 SMs (2 CTAs of 1024 threads per SM).
 #include <cuda_runtime.h>
 
 #include "se_device.cuh"
@@ -11,13 +11,18 @@
 namespace se {
 
 constexpr int kCipherThreads = 256;
+#ifndef SE_LANE_THREADS
+#define SE_LANE_THREADS 1024
+#endif
+constexpr int kLaneThreads = SE_LANE_THREADS;       // CTA size of the lane-table cipher (one 64 KB table per CTA)
 
 // p.in == nullptr: write the keystream itself (used by the fused kernels,
 // which then XOR it into the private fragment, see fused_cta.cuh).
 // LANE: the 64 KB lane-replicated table (standalone cipher), else the 5 KB
 // tables (keystream next to a running fused kernel).
 template <bool LANE>
-__global__ void __launch_bounds__(kCipherThreads) k_cipher_ctr(const __grid_constant__ CipherParams p) {
+__global__ void __launch_bounds__(LANE ? kLaneThreads : kCipherThreads) k_cipher_ctr(const __grid_constant__ CipherParams p) {
+    constexpr int NT = LANE ? kLaneThreads : kCipherThreads;
     // a dependent kernel launched with programmatic stream serialization may
     // start now; it waits (griddepcontrol.wait) before reading our output
     asm volatile("griddepcontrol.launch_dependents;");
@@ -27,13 +32,13 @@ __global__ void __launch_bounds__(kCipherThreads) k_cipher_ctr(const __grid_cons
     }
     extern __shared__ __align__(16) uint32_t lut[];
     __shared__ AesSmem small;
-    if constexpr (LANE) aes_load_lut(lut, threadIdx.x, kCipherThreads);
-    else aes_load_tables(small, threadIdx.x, kCipherThreads);
+    if constexpr (LANE) aes_load_lut(lut, threadIdx.x, NT);
+    else aes_load_tables(small, threadIdx.x, NT);
     __syncthreads();
     const AesLane lane = aes_lane(lut);
     const uint64_t nblk = (p.n + 15) / 16;
-    const uint64_t stride = (uint64_t)gridDim.x * kCipherThreads;
-    for (uint64_t j = (uint64_t)blockIdx.x * kCipherThreads + threadIdx.x; j < nblk; j += stride) {
+    const uint64_t stride = (uint64_t)gridDim.x * NT;
+    for (uint64_t j = (uint64_t)blockIdx.x * NT + threadIdx.x; j < nblk; j += stride) {
         uint32_t x[4];
         ctr_add(p.ctr, j, x);
         if constexpr (LANE) aes128_block(lane, p.rk, x);
@@ -134,14 +139,17 @@ int launch_cipher_ctr(const CipherParams& p, void* stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t nblk = (p.n + 15) / 16;
-    const uint64_t want = (nblk + kCipherThreads - 1) / kCipherThreads;
     const bool lane = p.in != nullptr || p.lane_lut;
-    const uint64_t cap = (uint64_t)sms * (lane ? kCipherCtasPerSm : kKeystreamCtasPerSm);
+    const int nt = lane ? kLaneThreads : kCipherThreads;
+    const uint64_t want = (nblk + nt - 1) / nt;
+    // lane table: 64 KB per CTA -> at most 3 CTAs per SM, and 2048 threads per SM
+    const int lane_ctas = kCipherCtasPerSm < 2048 / kLaneThreads ? kCipherCtasPerSm : 2048 / kLaneThreads;
+    const uint64_t cap = (uint64_t)sms * (lane ? lane_ctas : kKeystreamCtasPerSm);
     const unsigned grid = (unsigned)(want < cap ? want : cap);
     if (grid == 0) return 0;
     if (lane) {
         allow_lut<k_cipher_ctr<true>>();
-        k_cipher_ctr<true><<<grid, kCipherThreads, kAesLutBytes, (cudaStream_t)stream>>>(p);
+        k_cipher_ctr<true><<<grid, kLaneThreads, kAesLutBytes, (cudaStream_t)stream>>>(p);
     } else {
         k_cipher_ctr<false><<<grid, kCipherThreads, 0, (cudaStream_t)stream>>>(p);
     }
