@@ -45,16 +45,50 @@ namespace se {
 #endif
 template <int L>
 __host__ __device__ constexpr int bpc_for() { return L == 3 ? kBlocksPerCta : SE_BPC; }
+// resident CTAs per SM the masked kernels' register budget must allow
+#ifndef SE_MINB_MASK
+#define SE_MINB_MASK(bpc) (SE_MIN_CTAS * kBlocksPerCta / (bpc))
+#endif
+
+// SE_TRACE (diagnostic builds only, tools/cta_trace.py): per CTA, the SM id
+// and %globaltimer at entry and exit, read back with se_trace_read.
+#ifdef SE_TRACE
+constexpr int kTraceMax = 1 << 16;
+__device__ unsigned long long g_trace[3 * kTraceMax];
+struct CtaTrace {
+    unsigned long long t0;
+    __device__ CtaTrace() {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    }
+    __device__ ~CtaTrace() {
+        __syncthreads();
+        if (threadIdx.x == 0 && blockIdx.x < kTraceMax) {
+            unsigned long long t1;
+            unsigned sm;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_trace[3 * blockIdx.x] = sm;
+            g_trace[3 * blockIdx.x + 1] = t0;
+            g_trace[3 * blockIdx.x + 2] = t1;
+        }
+    }
+};
+#define SE_CTA_TRACE CtaTrace trace_;
+#else
+#define SE_CTA_TRACE
+#endif
 
 template <int L, bool MASK>
-__global__ void __launch_bounds__(bpc_for<L>(), (MASK ? SE_MIN_CTAS : SE_MIN_CTAS_PLAIN_P) * kBlocksPerCta / bpc_for<L>())
+__global__ void __launch_bounds__(bpc_for<L>(), MASK ? SE_MINB_MASK(bpc_for<L>()) : SE_MIN_CTAS_PLAIN_P * kBlocksPerCta / bpc_for<L>())
 k_protect_block8(const __grid_constant__ FusedParams p) {
+    SE_CTA_TRACE
     protect_cta<L, MASK, 0, bpc_for<L>()>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
-__global__ void __launch_bounds__(bpc_for<L>(), (MASK ? SE_MIN_CTAS : SE_MIN_CTAS_PLAIN_R) * kBlocksPerCta / bpc_for<L>())
+__global__ void __launch_bounds__(bpc_for<L>(), MASK ? SE_MINB_MASK(bpc_for<L>()) : SE_MIN_CTAS_PLAIN_R * kBlocksPerCta / bpc_for<L>())
 k_recover_block8(const __grid_constant__ FusedParams p) {
+    SE_CTA_TRACE
     recover_cta<L, MASK, 0, bpc_for<L>()>(p, blockIdx.x);
 }
 
@@ -175,6 +209,13 @@ __global__ void __launch_bounds__(kBlocksPerCta) k_dwt_inv_block8(const __grid_c
 }
 
 // ---------------------------------------------------------------- launchers
+
+#ifdef SE_TRACE
+extern "C" int se_trace_read(unsigned long long* host, int n_ctas) {
+    if (n_ctas > kTraceMax) n_ctas = kTraceMax;
+    return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 3 * n_ctas);
+}
+#endif
 
 // Launch with programmatic stream serialization: the kernel may start while
 // the preceding keystream kernel (k_cipher_ctr) still runs; it synchronises

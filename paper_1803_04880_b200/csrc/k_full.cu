@@ -7,320 +7,444 @@
 // then regrouped per 8x8 input footprint (4 / 12 / 48 coefficients at L = 2)
 // and protected exactly like BLOCK8 records (fused_cta.cuh, MODE 1).
 //
-// Transform kernels: one CTA per 64 x 128 output tile.  The tile is loaded
-// into shared memory with a halo of H = 2(2^L - 1) samples (rounded up to a
-// multiple of 2^L so the lifting phase of the tile grid equals the global
-// one): every 1-D lifting pass consumes 2 samples of its level on each side,
-// so after L levels the tile interior is exact while the halo absorbs the
-// error of the cut.  Lifting runs in place on the interleaved grid (level l
-// touches every 2^(l-1)-th sample; even positions hold s, odd hold d), one
-// shared-memory sweep per predict / update step; neighbours beyond the
-// matrix border are reflected per level, neighbours beyond the halo are never
-// read for interior outputs.  Coefficients move between the interleaved grid
-// and the Mallat layout band by band, so global reads and writes are row
-// segments (coalesced).
+// Transform kernels: line-based (streaming) lifting.  A warp owns a column
+// group and a segment of rows; each lane owns an 8-column chunk of every row.
+// Rows stream through the lane in order: the horizontal lifting of a row runs
+// in registers with the chunk-edge neighbours exchanged by warp shuffles, the
+// vertical lifting keeps the few rows it needs (pending even / odd row and the
+// previous detail row, per level) in registers and emits a finished row pair
+// as soon as the next even row arrives; the low-low part of every level-l
+// pair is the next row of level l + 1.  One pass over the input, no shared
+// memory, no barriers: a global load of 8 bytes per lane per input row and
+// 8-byte (4- / 2-byte at levels 2 / 3) Mallat stores per band.
+//   Halos.  Every lifting step reads one neighbour of its level on each
+// side, so after L levels an output depends on inputs within 2(2^L - 1)
+// samples.  Warps overlap by HC chunks on each side (their edge lanes compute
+// but do not store); segments process H rows before and after their output
+// rows (H = 4 / 8 / 16: >= 2(2^L - 1), a multiple of 2^L so the lifting
+// phase of the segment equals the global one).  The first pair of a segment
+// and the last one take the matrix-border rules (d(-1) = d(0), x(N) = x(N-2));
+// exact at the matrix borders, elsewhere their error stays inside the halo.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "fused_cta.cuh"
 
 namespace se {
 
-constexpr int kTileR = 64, kTileC = 128, kFullThreads = 512;
+constexpr unsigned kLanes = 0xffffffffu;
+constexpr int kStreamThreads = 128, kStreamWarps = kStreamThreads / 32;
 
 template <int L>
-struct FullTile {
-    static constexpr int H = L == 1 ? 4 : L == 2 ? 8 : 16;   // >= 2(2^L - 1), multiple of 2^L and of 4
-    static constexpr int SR = kTileR + 2 * H, SC = kTileC + 2 * H;
-    // the grid sits inside a margin of 2 s_max samples before and s_max + 1
-    // after it (s_max = 2^(L-1)), so a lifting chunk's edge loads (forward
-    // m = -2..8, inverse m = -1..9) never leave shared memory and need no
-    // bounds test (values there only feed halo outputs)
-    static constexpr int S_MAX = 1 << (L - 1), PAD_LO = 2 * S_MAX, PAD_HI = S_MAX + 1;
-    static constexpr int P = (SC + PAD_LO + PAD_HI) | 1;      // odd pitch: row / column chunks in distinct banks
-    static constexpr int ROWS = SR + PAD_LO + PAD_HI;
-    static constexpr int OFF = PAD_LO * P + PAD_LO;           // grid origin inside the buffer
-    static constexpr size_t smem = (size_t)ROWS * P * sizeof(int);
+struct FStream {
+    static constexpr int HC = L == 3 ? 2 : 1;                  // overlap chunks per warp side
+    static constexpr int USE = 32 - 2 * HC;                    // chunks a warp stores
+    static constexpr int H = L == 1 ? 4 : L == 2 ? 8 : 16;      // halo rows
 };
 
-// One lifting pass of level spacing s along one direction of the tile
-// (DIR 0: along rows, DIR 1: along columns), predict and update together.
-// The active samples of a line are cut into chunks of 8 (4 even, 4 odd); a
-// thread loads its chunk plus the samples the chunk edges need (forward:
-// m = -2..8, so d(-1) of the previous chunk is recomputed from raw samples;
-// inverse: m = -1..9), all threads load before any stores (one barrier), and
-// the lifting runs in registers.  Consecutive threads take consecutive lines,
-// which the odd row pitch puts in distinct banks.  Matrix borders: whole-sample
-// symmetric extension per level (x(N) = x(N-2), d(-1) = d(0)); samples beyond
-// the tile edge read 0 — they only feed halo outputs, which the halo of
-// 2(2^L - 1) samples keeps away from the tile interior.
-template <int L, int DIR, int s, bool INV>
-__device__ __forceinline__ void lift_pass(int* g, int R0, int C0, int R, int W) {
-    using T = FullTile<L>;
-    constexpr int span = DIR == 0 ? T::SC : T::SR;            // along
-    constexpr int nA = (DIR == 0 ? T::SR : T::SC) / s;         // active lines
-    constexpr int nC = span / (8 * s);                         // chunks per line
-    static_assert(span % (8 * s) == 0, "tile span must hold whole chunks");
-    constexpr int items = nA * nC;
-    constexpr int iters = (items + kFullThreads - 1) / kFullThreads;
-    constexpr int step = DIR == 0 ? s : s * T::P;              // smem distance between active samples
-    constexpr int m0 = INV ? -1 : -2;                          // first loaded sample
-    const int O = DIR == 0 ? C0 : R0, N = DIR == 0 ? W : R;    // along: global origin, extent
-    const int Oa = DIR == 0 ? R0 : C0, Na = DIR == 0 ? R : W;  // across
-    static_assert(INV ? (s <= T::PAD_LO && s + 1 <= T::PAD_HI) : (2 * s <= T::PAD_LO && 1 <= T::PAD_HI),
-                  "margin must cover the chunk edge loads");
-    int v[iters][11];
+// Forward 1-D lifting of one level along a row: v holds NV samples of the
+// level (columns gcol .. gcol + NV - 1 of a level row of Nl samples), even =
+// s, odd = d on return.  Predict (Eq. 5.1) then update (Eq. 5.2, "+").
+template <int NV>
+__device__ __forceinline__ void hfwd(int (&v)[NV], int gcol, int Nl) {
+    int xr = __shfl_down_sync(kLanes, v[0], 1);                // next chunk's first sample
+    if (gcol + NV >= Nl) xr = v[NV - 2];                        // x(N) = x(N - 2)
 #pragma unroll
-    for (int it = 0; it < iters; ++it) {
-        const int idx = threadIdx.x + it * kFullThreads;
-        const int a = (idx % nA) * s, j0 = (idx / nA) * 8 * s;
-        const int base = DIR == 0 ? a * T::P + j0 : j0 * T::P + a;
-        const bool live = (items % kFullThreads == 0 || it + 1 < iters) || idx < items;
+    for (int m = 1; m < NV; m += 2) v[m] -= (v[m - 1] + (m + 1 < NV ? v[m + 1] : xr)) >> 1;
+    int dl = __shfl_up_sync(kLanes, v[NV - 1], 1);             // previous chunk's last d
+    if (gcol == 0) dl = v[1];                                   // d(-1) = d(0)
 #pragma unroll
-        for (int q = 0; q < 11; ++q) v[it][q] = live ? g[base + (q + m0) * step] : 0;   // margin: no bounds test
+    for (int m = 0; m < NV; m += 2) v[m] += ((m ? v[m - 1] : dl) + v[m + 1] + 2) >> 2;
+}
+
+// Inverse of hfwd: undo the update, then the predict.
+template <int NV>
+__device__ __forceinline__ void hinv(int (&v)[NV], int gcol, int Nl) {
+    int dl = __shfl_up_sync(kLanes, v[NV - 1], 1);
+    if (gcol == 0) dl = v[1];
+#pragma unroll
+    for (int m = 0; m < NV; m += 2) v[m] -= ((m ? v[m - 1] : dl) + v[m + 1] + 2) >> 2;
+    int xr = __shfl_down_sync(kLanes, v[0], 1);
+    if (gcol + NV >= Nl) xr = v[NV - 2];
+#pragma unroll
+    for (int m = 1; m < NV; m += 2) v[m] += (v[m - 1] + (m + 1 < NV ? v[m + 1] : xr)) >> 1;
+}
+
+// NH int16 values (v[OFF], v[OFF + 2], ...) -> 2*NH bytes at g (aligned)
+template <int NH, int OFF, int NV>
+__device__ __forceinline__ void st_band(int16_t* g, const int (&v)[NV]) {
+    if constexpr (NH == 4) {
+        uint2 q;
+        q.x = (uint32_t)(v[OFF] & 0xffff) | ((uint32_t)v[OFF + 2] << 16);
+        q.y = (uint32_t)(v[OFF + 4] & 0xffff) | ((uint32_t)v[OFF + 6] << 16);
+        *reinterpret_cast<uint2*>(g) = q;
+    } else if constexpr (NH == 2) {
+        *reinterpret_cast<uint32_t*>(g) = (uint32_t)(v[OFF] & 0xffff) | ((uint32_t)v[OFF + 2] << 16);
+    } else {
+        *g = (int16_t)v[OFF];
     }
-    __syncthreads();
+}
+
+template <int NH>
+__device__ __forceinline__ void ld_band(const int16_t* g, int (&v)[NH]) {
+    if constexpr (NH == 4) {
+        const uint2 q = __ldg(reinterpret_cast<const uint2*>(g));
+        v[0] = (int)(int16_t)(q.x & 0xffff); v[1] = (int)q.x >> 16;
+        v[2] = (int)(int16_t)(q.y & 0xffff); v[3] = (int)q.y >> 16;
+    } else if constexpr (NH == 2) {
+        const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(g));
+        v[0] = (int)(int16_t)(q & 0xffff); v[1] = (int)q >> 16;
+    } else {
+        v[0] = __ldg(g);
+    }
+}
+
+struct StreamCtx {
+    int W, R;
+    int c0;               // first column of the lane's chunk (outside [0, W): a dummy lane)
+    bool out_lane;        // lane stores (not an overlap lane, chunk inside the matrix)
+    int A, B;             // output rows of the segment (global, multiples of 8)
+    int row0, rows_out;   // the call's output window (local Mallat / byte offsets)
+    int src0, src_rows;   // inverse: rows present in the local Mallat source
+};
+
+// ---------------------------------------------------------------- forward
+
+template <int NV>
+struct FwdLine {          // vertical lifting state of one level
+    int E[NV], O[NV], D[NV];
+    int n;                // rows received in this segment
+};
+struct FwdState {
+    FwdLine<8> l1;
+    FwdLine<4> l2;
+    FwdLine<2> l3;
+    int kf;               // first input row of the segment
+};
+template <int l>
+__device__ __forceinline__ auto& fline(FwdState& s) {
+    if constexpr (l == 1) return s.l1;
+    else if constexpr (l == 2) return s.l2;
+    else return s.l3;
+}
+
+template <int L, int l>
+__device__ __forceinline__ void fwd_push(FwdState& st, int (&x)[8 >> (l - 1)], int16_t* coef, const StreamCtx& c);
+
+// A finished pair of level l (rows 2k, 2k+1 of the level): s row (vertical
+// low) and d row.  Stores HL / LH / HH (and LL at l = L); LL feeds level l+1.
+template <int L, int l>
+__device__ __forceinline__ void fwd_emit(FwdState& st, int (&sv)[8 >> (l - 1)], const int (&d)[8 >> (l - 1)],
+                                         int k, int16_t* coef, const StreamCtx& c) {
+    constexpr int NV = 8 >> (l - 1), NH = NV / 2;
+    const int r_in = k << l;                                    // first input row of the pair
+    if (c.out_lane && r_in >= c.A && r_in < c.B) {
+        const int64_t top = k - (c.row0 >> l), bot = top + (c.rows_out >> l);
+        const int colL = c.c0 >> l, colH = (c.W >> l) + colL;
+        st_band<NH, 1>(coef + top * c.W + colH, sv);             // HL: vertical low, horizontal high
+        st_band<NH, 0>(coef + bot * c.W + colL, d);              // LH
+        st_band<NH, 1>(coef + bot * c.W + colH, d);              // HH
+        if constexpr (l == L) st_band<NH, 0>(coef + top * c.W + colL, sv);   // LL_L
+    }
+    if constexpr (l < L) {
+        int y[NH];
 #pragma unroll
-    for (int it = 0; it < iters; ++it) {
-        const int idx = threadIdx.x + it * kFullThreads;
-        if (idx >= items) continue;
-        const int a = (idx % nA) * s, j0 = (idx / nA) * 8 * s;
-        const int ga = Oa + a;
-        if (ga < 0 || ga >= Na) continue;                      // line outside the matrix
-        const int base = DIR == 0 ? a * T::P + j0 : j0 * T::P + a;
-        const int G0 = O + j0;                                 // global coordinate of m = 0
-        int* x = v[it] - m0;                                   // x[m], m = m0 .. m0 + 10
-        if (G0 - 2 * s >= 0 && G0 + 8 * s < N) {
-            // interior chunk (every tile but those on the matrix border): no reflection, no store test
-            if constexpr (!INV) {
+        for (int i = 0; i < NH; ++i) y[i] = sv[2 * i];
+        fwd_push<L, l + 1>(st, y, coef, c);
+    }
+}
+
+// Pair (E, O) completed by the next even row xn (x(N) = x(N-2) at the end: xn = E).
+template <int L, int l>
+__device__ __forceinline__ void fwd_pair(FwdState& st, const int (&xn)[8 >> (l - 1)], int16_t* coef,
+                                         const StreamCtx& c) {
+    constexpr int NV = 8 >> (l - 1);
+    auto& s = fline<l>(st);
+    int d[NV], sv[NV];
 #pragma unroll
-                for (int m = -1; m <= 7; m += 2) x[m] -= (x[m - 1] + x[m + 1]) >> 1;
+    for (int i = 0; i < NV; ++i) d[i] = s.O[i] - ((s.E[i] + xn[i]) >> 1);
+    const bool first = s.n == 2;                                // d(-1) = d(0)
 #pragma unroll
-                for (int m = 0; m <= 6; m += 2) x[m] += (x[m - 1] + x[m + 1] + 2) >> 2;
+    for (int i = 0; i < NV; ++i) sv[i] = s.E[i] + (((first ? d[i] : s.D[i]) + d[i] + 2) >> 2);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) s.D[i] = d[i];
+    const int k = ((st.kf >> (l - 1)) + s.n - 2) >> 1;
+    fwd_emit<L, l>(st, sv, d, k, coef, c);
+}
+
+template <int L, int l>
+__device__ __forceinline__ void fwd_push(FwdState& st, int (&x)[8 >> (l - 1)], int16_t* coef, const StreamCtx& c) {
+    constexpr int NV = 8 >> (l - 1);
+    auto& s = fline<l>(st);
+    hfwd<NV>(x, c.c0 >> (l - 1), c.W >> (l - 1));             // row pass of level l
+    if ((s.n & 1) == 0) {
+        if (s.n >= 2) fwd_pair<L, l>(st, x, coef, c);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) s.E[i] = x[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) s.O[i] = x[i];
+    }
+    ++s.n;
+}
+
+template <int L, int l>
+__device__ __forceinline__ void fwd_finish(FwdState& st, int16_t* coef, const StreamCtx& c) {
+    auto& s = fline<l>(st);
+    if (s.n >= 2 && (s.n & 1) == 0) {
+        int e[8 >> (l - 1)];
+#pragma unroll
+        for (int i = 0; i < (8 >> (l - 1)); ++i) e[i] = s.E[i];
+        fwd_pair<L, l>(st, e, coef, c);                         // x(N) = x(N - 2)
+    }
+    if constexpr (l < L) fwd_finish<L, l + 1>(st, coef, c);
+}
+
+// 8 bytes of row r at columns c0..c0+7 as raw bytes: centering (C8) is
+// applied by the caller (x = b - 128); bytes past n read 0 (-> -128, C18),
+// other bytes of rows outside the source window read 0x80 (-> 0; they only
+// feed halo rows).
+__device__ __forceinline__ uint2 fetch_row(const DwtParams& p, int r, int c0, bool col_ok) {
+    const uint2 none = make_uint2(0x80808080u, 0x80808080u);
+    if (!col_ok) return none;
+    const uint64_t o = (uint64_t)r * p.width + c0;
+    const bool have = r >= (int)p.src_row0 && r < (int)(p.src_row0 + p.src_rows);
+    const uint8_t* src = p.in + (uint64_t)(r - (int)p.src_row0) * p.width + c0;
+    if (o + 8 <= p.n_bytes) return have ? __ldg(reinterpret_cast<const uint2*>(src)) : none;
+    uint32_t w[2] = {0, 0};
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+        if (o + b < p.n_bytes) w[b >> 2] |= (have ? (uint32_t)src[b] : 0x80u) << (8 * (b & 3));
+    return make_uint2(w[0], w[1]);
+}
+
+__device__ __forceinline__ void stream_ctx(StreamCtx& c, const DwtParams& p, int HC, int USE, int seg, int ncg,
+                                           int& sg) {
+    const int lane = threadIdx.x & 31;
+    const int wid = (int)blockIdx.x * kStreamWarps + (int)(threadIdx.x >> 5);
+    const int cg = wid % ncg;
+    sg = wid / ncg;
+    c.W = (int)p.width;
+    c.R = (int)p.rows;
+    c.c0 = 8 * (cg * USE - HC + lane);
+    c.out_lane = lane >= HC && lane < 32 - HC && c.c0 < c.W;
+    c.row0 = (int)p.row0;
+    c.rows_out = (int)p.rows_out;
+    const int row_end = min((int)(p.row0 + p.rows_out), c.R);
+    c.A = c.row0 + sg * seg;
+    c.B = min(c.A + seg, row_end);
+    c.src0 = (int)p.src_row0;
+    c.src_rows = (int)p.src_rows;
+}
+
+template <int L>
+__global__ void __launch_bounds__(kStreamThreads) k_dwt_full_fwd(const __grid_constant__ DwtParams p, int seg,
+                                                                 int ncg, int nseg) {
+    using F = FStream<L>;
+    StreamCtx c;
+    int sg;
+    stream_ctx(c, p, F::HC, F::USE, seg, ncg, sg);
+    if (sg >= nseg) return;                                     // whole warp
+    const int P0 = max(c.A - F::H, 0), P1 = min(c.B + F::H, c.R);
+    const bool col_ok = c.c0 >= 0 && c.c0 < c.W;
+    FwdState st;
+    st.kf = P0;
+    st.l1.n = 0;
+    st.l2.n = 0;
+    st.l3.n = 0;
+    uint2 nxt = fetch_row(p, P0, c.c0, col_ok);
+    for (int r = P0; r < P1; ++r) {
+        const uint2 q = nxt;
+        if (r + 1 < P1) nxt = fetch_row(p, r + 1, c.c0, col_ok);
+        int x[8];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            x[b] = (int)((q.x >> (8 * b)) & 0xff) - 128;
+            x[4 + b] = (int)((q.y >> (8 * b)) & 0xff) - 128;
+        }
+        fwd_push<L, 1>(st, x, p.coef, c);
+    }
+    fwd_finish<L, 1>(st, p.coef, c);
+}
+
+// ---------------------------------------------------------------- inverse
+
+template <int NV>
+struct InvLine {
+    int X[NV], D[NV];     // last even row rebuilt (x_2k) and d_k
+    int n;                // pairs received in this segment
+};
+struct InvState {
+    InvLine<8> l1;
+    InvLine<4> l2;
+    InvLine<2> l3;
+    int kf;               // first input row of the segment
+    uint32_t bad;         // footprint row flag (level 1 output)
+};
+template <int l>
+__device__ __forceinline__ auto& iline(InvState& s) {
+    if constexpr (l == 1) return s.l1;
+    else if constexpr (l == 2) return s.l2;
+    else return s.l3;
+}
+
+struct InvOut {
+    const int16_t* coef;
+    uint8_t* out;
+    uint64_t n_bytes;
+    se_report* report;
+};
+
+template <int L, int l>
+__device__ __forceinline__ void inv_push(InvState& st, const int (&sr)[8 >> (l - 1)],
+                                         const int (&dr)[8 >> (l - 1)], const InvOut& o, const StreamCtx& c);
+
+// band row j of level l (NH values at the lane's columns), 0 outside the source window
+template <int l, int NH>
+__device__ __forceinline__ void load_band(int (&v)[NH], const InvOut& o, const StreamCtx& c, int j, bool hr, bool hc) {
+    const int sb0 = c.src0 >> l, sbn = c.src_rows >> l;
+    if (c.c0 < 0 || c.c0 >= c.W || j < sb0 || j >= sb0 + sbn) {
+#pragma unroll
+        for (int i = 0; i < NH; ++i) v[i] = 0;
+        return;
+    }
+    const int64_t row = (hr ? sbn : 0) + (j - sb0);
+    const int col = (hc ? (c.W >> l) : 0) + (c.c0 >> l);
+    ld_band<NH>(o.coef + row * c.W + col, v);
+}
+
+// A row j of level l - 1's low-low band (or of the output, l = 1) rebuilt
+// vertically at level l: undo the row pass, then hand it down.
+template <int L, int l>
+__device__ __forceinline__ void inv_emit(InvState& st, int (&v)[8 >> (l - 1)], int j, const InvOut& o,
+                                         const StreamCtx& c) {
+    constexpr int NV = 8 >> (l - 1);
+    hinv<NV>(v, c.c0 >> (l - 1), c.W >> (l - 1));
+    if constexpr (l == 1) {
+        if (c.out_lane && j >= c.A && j < c.B) {
+            uint32_t w[2] = {0, 0};
+            int orv = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int b = v[i] + 128;
+                orv |= b;
+                w[i >> 2] |= (uint32_t)(b & 0xff) << (8 * (i & 3));
+            }
+            if (orv & ~0xff) st.bad = 1;                        // a sample outside [0, 255]
+            const uint64_t off = (uint64_t)j * c.W + c.c0;
+            uint8_t* dst = o.out + (uint64_t)(j - c.row0) * c.W + c.c0;
+            if (off + 8 <= o.n_bytes) {
+                *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
             } else {
 #pragma unroll
-                for (int m = 0; m <= 8; m += 2) x[m] -= (x[m - 1] + x[m + 1] + 2) >> 2;
-#pragma unroll
-                for (int m = 1; m <= 7; m += 2) x[m] += (x[m - 1] + x[m + 1]) >> 1;
+                for (int b = 0; b < 8; ++b)
+                    if (off + b < o.n_bytes) dst[b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
             }
-#pragma unroll
-            for (int m = 0; m < 8; ++m) g[base + m * step] = x[m];
-            continue;
-        }
-        if constexpr (!INV) {
-            // predict (Eq. 5.1) at odd m = -1, 1, 3, 5, 7; right neighbour reflected at the border
-#pragma unroll
-            for (int m = -1; m <= 7; m += 2) {
-                const int Gm = G0 + m * s;
-                const int r = (Gm + s >= N) ? x[m - 1] : x[m + 1];
-                x[m] -= (x[m - 1] + r) >> 1;
-            }
-            // update (Eq. 5.2, "+") at even m = 0, 2, 4, 6; d(-1) = d(0) at the left border
-#pragma unroll
-            for (int m = 0; m <= 6; m += 2) {
-                const int Gm = G0 + m * s;
-                const int l = (Gm == 0) ? x[m + 1] : x[m - 1];
-                x[m] += (l + x[m + 1] + 2) >> 2;
-            }
-        } else {
-            // undo update at even m = 0 .. 8, then undo predict at odd m = 1 .. 7
-#pragma unroll
-            for (int m = 0; m <= 8; m += 2) {
-                const int Gm = G0 + m * s;
-                const int l = (Gm == 0) ? x[m + 1] : x[m - 1];
-                x[m] -= (l + x[m + 1] + 2) >> 2;
-            }
-#pragma unroll
-            for (int m = 1; m <= 7; m += 2) {
-                const int Gm = G0 + m * s;
-                const int r = (Gm + s >= N) ? x[m - 1] : x[m + 1];
-                x[m] += (x[m - 1] + r) >> 1;
-            }
-        }
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-            const int Gm = G0 + m * s;
-            if (Gm >= 0 && Gm < N) g[base + m * step] = x[m];
-        }
-    }
-    __syncthreads();
-}
-
-// Zero the margin around the grid (keeps the unused edge arithmetic defined).
-template <int L>
-__device__ __forceinline__ void zero_margin(int* buf) {
-    using T = FullTile<L>;
-    constexpr int top = T::PAD_LO * T::P, bot0 = (T::PAD_LO + T::SR) * T::P;
-    constexpr int side = T::P - T::SC;                          // margin columns per grid row
-    for (int i = threadIdx.x; i < top + T::PAD_LO; i += kFullThreads) buf[i] = 0;   // + row 0's left margin
-    for (int i = threadIdx.x; i < T::ROWS * T::P - bot0; i += kFullThreads) buf[bot0 + i] = 0;
-    for (int i = threadIdx.x; i < T::SR * side; i += kFullThreads) {
-        const int r = i / side, c = i % side;                   // columns [SC, P) then wrap to [0, PAD_LO)
-        const int col = T::PAD_LO + T::SC + c;                  // right margin + left margin of the next row
-        buf[(T::PAD_LO + r) * T::P + col] = 0;
-    }
-}
-
-// All levels, forward (l = 1..L: rows then columns) / inverse (l = L..1:
-// columns then rows); the spacing s = 2^(l-1) is a compile-time constant.
-template <int L, int l>
-__device__ __forceinline__ void fwd_levels(int* g, int R0, int C0, int R, int W) {
-    if constexpr (l <= L) {
-        lift_pass<L, 0, 1 << (l - 1), false>(g, R0, C0, R, W);
-        lift_pass<L, 1, 1 << (l - 1), false>(g, R0, C0, R, W);
-        fwd_levels<L, l + 1>(g, R0, C0, R, W);
-    }
-}
-template <int L, int l>
-__device__ __forceinline__ void inv_levels(int* g, int R0, int C0, int R, int W) {
-    if constexpr (l >= 1) {
-        lift_pass<L, 1, 1 << (l - 1), true>(g, R0, C0, R, W);
-        lift_pass<L, 0, 1 << (l - 1), true>(g, R0, C0, R, W);
-        inv_levels<L, l - 1>(g, R0, C0, R, W);
-    }
-}
-
-// Visit the Mallat band rectangles covered by a tile region: for level l and
-// band (0 LL (l == L only), 1 HL, 2 LH, 3 HH), grid offset (pr, pc) of the
-// band's samples inside each 2^l x 2^l cell and Mallat origin.
-template <int L, typename F>
-__device__ __forceinline__ void for_each_band(F&& f) {
-#pragma unroll
-    for (int l = 1; l <= L; ++l)
-#pragma unroll
-        for (int band = (l == L ? 0 : 1); band < 4; ++band) f(l, band);
-}
-
-template <int L>
-__global__ void __launch_bounds__(kFullThreads) k_dwt_full_fwd(const __grid_constant__ DwtParams p) {
-    using T = FullTile<L>;
-    extern __shared__ int g_buf[];
-    int* g = g_buf + T::OFF;                                    // grid origin inside the margin
-    zero_margin<L>(g_buf);
-    const int W = (int)p.width, R = (int)p.rows;
-    const int row0 = (int)p.row0, row_end = min((int)(p.row0 + p.rows_out), R);
-    const int s0 = (int)p.src_row0, s1 = (int)(p.src_row0 + p.src_rows);
-    const int tr0 = row0 + (int)blockIdx.y * kTileR, tc0 = (int)blockIdx.x * kTileC;
-    const int R0 = tr0 - T::H, C0 = tc0 - T::H;
-    // load tile + halo, 4 bytes per access, centered (C8), zero fill past n
-    // (C18); rows the caller did not provide (beyond a stripe's halo) read 0
-    constexpr int WPR = T::SC / 4;
-    for (int idx = threadIdx.x; idx < T::SR * WPR; idx += kFullThreads) {
-        const int i = idx / WPR, w = idx % WPR;
-        const int gr = R0 + i, gc = C0 + 4 * w;
-        int v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-        if (gr >= 0 && gr < R && gc >= 0 && gc < W) {            // whole word inside (W % 8 == 0)
-            const uint64_t o = (uint64_t)gr * W + gc;
-            const bool have = gr >= s0 && gr < s1;
-            if (have && o + 4 <= p.n_bytes) {
-                const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(p.in + (uint64_t)(gr - s0) * W + gc));
-                v0 = (int)(q & 0xff) - 128; v1 = (int)((q >> 8) & 0xff) - 128;
-                v2 = (int)((q >> 16) & 0xff) - 128; v3 = (int)(q >> 24) - 128;
-            } else {
-                int t[4];
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    t[b] = (o + b >= p.n_bytes) ? -128 : have ? (int)p.in[(uint64_t)(gr - s0) * W + gc + b] - 128 : 0;
-                v0 = t[0]; v1 = t[1]; v2 = t[2]; v3 = t[3];
-            }
-        }
-        int* d = g + i * T::P + 4 * w;
-        d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3;
-    }
-    __syncthreads();
-    fwd_levels<L, 1>(g, R0, C0, R, W);
-    // write the tile interior band by band in Mallat layout
-    for_each_band<L>([&](int l, int band) {
-        const int hr = band >= 2, hc = band & 1, half = 1 << (l - 1);
-        const int br = kTileR >> l, bc = kTileC >> l;          // band rectangle of this tile
-        const int64_t mr0 = (hr ? ((int64_t)p.rows_out >> l) : 0) + ((tr0 - row0) >> l);   // local Mallat rows
-        const int mc0 = (hc ? (W >> l) : 0) + (tc0 >> l);
-        for (int idx = threadIdx.x; idx < br * bc; idx += kFullThreads) {
-            const int bi = idx / bc, bj = idx % bc;
-            const int gr = tr0 + (bi << l) + (hr ? half : 0);
-            const int gc = tc0 + (bj << l) + (hc ? half : 0);
-            if (gr >= row_end || gc >= W) continue;
-            const int v = g[(gr - R0) * T::P + (gc - C0)];
-            p.coef[(uint64_t)(mr0 + bi) * W + (mc0 + bj)] = (int16_t)v;
-        }
-    });
-}
-
-template <int L>
-__global__ void __launch_bounds__(kFullThreads) k_dwt_full_inv(const __grid_constant__ DwtParams p,
-                                                               se_report* report) {
-    using T = FullTile<L>;
-    extern __shared__ int g_buf[];
-    int* g = g_buf + T::OFF;                                    // grid origin inside the margin
-    zero_margin<L>(g_buf);
-    __shared__ unsigned int s_badmask[(kTileR / 8) * (kTileC / 8) / 32];
-    const int W = (int)p.width, R = (int)p.rows;
-    const int row0 = (int)p.row0, row_end = min((int)(p.row0 + p.rows_out), R);
-    const int tr0 = row0 + (int)blockIdx.y * kTileR, tc0 = (int)blockIdx.x * kTileC;
-    const int R0 = tr0 - T::H, C0 = tc0 - T::H;
-    for (int i = threadIdx.x; i < (kTileR / 8) * (kTileC / 8) / 32; i += kFullThreads) s_badmask[i] = 0;
-    // gather tile + halo from the Mallat layout into the interleaved grid, band by band
-    for_each_band<L>([&](int l, int band) {
-        const int hr = band >= 2, hc = band & 1, half = 1 << (l - 1);
-        // band samples whose grid position falls in [R0, R0+SR) x [C0, C0+SC)
-        const int b_r0 = (R0 - (hr ? half : 0) + ((1 << l) - 1)) >> l;   // ceil, R0 may be negative
-        const int b_c0 = (C0 - (hc ? half : 0) + ((1 << l) - 1)) >> l;
-        const int nbr = (T::SR >> l) + 1, nbc = (T::SC >> l) + 1;
-        // the source window holds band rows [src_row0 >> l, (src_row0 + src_rows) >> l)
-        const int sb0 = (int)(p.src_row0 >> l), sbn = (int)(p.src_rows >> l);
-        // rows of band samples inside the tile grid and the source window, then columns
-        const int r_lo = max(max(b_r0, 0), sb0), r_hi = min(min(b_r0 + nbr, R >> l), sb0 + sbn);
-        const int c_lo = max(b_c0, 0), c_hi = min(b_c0 + nbc, W >> l);
-        const int nr = max(r_hi - r_lo, 0), nc = max(c_hi - c_lo, 0);
-        const int16_t* src = p.coef + (hc ? (W >> l) : 0);
-        const int64_t mrow0 = (hr ? sbn : 0) - sb0;
-#pragma unroll 4
-        for (int idx = threadIdx.x; idx < nr * nc; idx += kFullThreads) {
-            const int bi = r_lo + idx / nc, bj = c_lo + idx % nc;
-            const int gr = (bi << l) + (hr ? half : 0), gc = (bj << l) + (hc ? half : 0);
-            if (gr >= R0 + T::SR || gc >= C0 + T::SC) continue;
-            g[(gr - R0) * T::P + (gc - C0)] = __ldg(src + (uint64_t)(mrow0 + bi) * W + bj);
-        }
-    });
-    __syncthreads();
-    inv_levels<L, L>(g, R0, C0, R, W);
-    // write bytes (+128), 4 per store; flag footprints with samples outside [0, 255]
-    constexpr int WPR = kTileC / 4;
-    for (int idx = threadIdx.x; idx < kTileR * WPR; idx += kFullThreads) {
-        const int i = idx / WPR, w = idx % WPR;
-        const int gr = tr0 + i, gc = tc0 + 4 * w;
-        if (gr >= row_end || gc >= W) continue;
-        const int* src = g + (i + T::H) * T::P + (4 * w + T::H);
-        const int v0 = src[0] + 128, v1 = src[1] + 128, v2 = src[2] + 128, v3 = src[3] + 128;
-        if ((v0 | v1 | v2 | v3) & ~0xff) {
-            const int fp = (i / 8) * (kTileC / 8) + (4 * w) / 8;
-            atomicOr(&s_badmask[fp / 32], 1u << (fp % 32));
-        }
-        const uint64_t o = (uint64_t)gr * W + gc;
-        uint8_t* dst = p.out + (uint64_t)(gr - row0) * W + gc;
-        if (o + 4 <= p.n_bytes) {
-            *reinterpret_cast<uint32_t*>(dst) = (uint32_t)(v0 & 0xff) | (uint32_t)(v1 & 0xff) << 8 |
-                                                (uint32_t)(v2 & 0xff) << 16 | (uint32_t)(v3 & 0xff) << 24;
-        } else {
-            const int vv[4] = {v0, v1, v2, v3};
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (o + b < p.n_bytes) dst[b] = (uint8_t)vv[b];
-        }
-    }
-    if (report) {
-        __syncthreads();
-        const int nfp = (kTileR / 8) * (kTileC / 8);
-        for (int fp = threadIdx.x; fp < nfp; fp += kFullThreads) {
-            if (s_badmask[fp / 32] & (1u << (fp % 32))) {
-                const int64_t fbr = tr0 / 8 + fp / (kTileC / 8), fbc = tc0 / 8 + fp % (kTileC / 8);
-                if (fbr < row_end / 8 && fbc < W / 8) {                   // block index local to row0
-                    const unsigned long long b = (unsigned long long)((fbr - row0 / 8) * (W / 8) + fbc);
-                    atomicMin(reinterpret_cast<unsigned long long*>(&report->first_bad_block), b);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&report->bad_blocks), 1ull);
+            if ((j & 7) == 7) {                                 // footprint row complete
+                if (st.bad && o.report) {
+                    const unsigned long long blk =
+                        (unsigned long long)((j >> 3) - (c.row0 >> 3)) * (c.W >> 3) + (c.c0 >> 3);
+                    atomicMin(reinterpret_cast<unsigned long long*>(&o.report->first_bad_block), blk);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&o.report->bad_blocks), 1ull);
                 }
+                st.bad = 0;
             }
         }
+    } else {
+        // pair j of level l - 1: s row = (LL_{l-1}[j], HL_{l-1}[j]) interleaved, d row = (LH, HH)
+        constexpr int NV2 = 2 * NV;
+        int hl[NV], lh[NV], hh[NV];
+        load_band<l - 1, NV>(hl, o, c, j, false, true);
+        load_band<l - 1, NV>(lh, o, c, j, true, false);
+        load_band<l - 1, NV>(hh, o, c, j, true, true);
+        int sr[NV2], dr[NV2];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            sr[2 * i] = v[i];
+            sr[2 * i + 1] = hl[i];
+            dr[2 * i] = lh[i];
+            dr[2 * i + 1] = hh[i];
+        }
+        inv_push<L, l - 1>(st, sr, dr, o, c);
     }
+}
+
+// Pair k of level l arrives: x_2k = s_k - (d_{k-1} + d_k + 2) >> 2, then
+// x_{2k-1} = d_{k-1} + (x_{2k-2} + x_2k) >> 1; rows leave in order.
+template <int L, int l>
+__device__ __forceinline__ void inv_push(InvState& st, const int (&sr)[8 >> (l - 1)],
+                                         const int (&dr)[8 >> (l - 1)], const InvOut& o, const StreamCtx& c) {
+    constexpr int NV = 8 >> (l - 1);
+    auto& s = iline<l>(st);
+    const int k = (st.kf >> l) + s.n;
+    int x[NV];
+    const bool first = s.n == 0;                                // d(-1) = d(0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) x[i] = sr[i] - (((first ? dr[i] : s.D[i]) + dr[i] + 2) >> 2);
+    if (!first) {
+        int xo[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) xo[i] = s.D[i] + ((s.X[i] + x[i]) >> 1);
+        inv_emit<L, l>(st, xo, 2 * k - 1, o, c);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        s.X[i] = x[i];
+        s.D[i] = dr[i];
+    }
+    ++s.n;
+    inv_emit<L, l>(st, x, 2 * k, o, c);
+}
+
+// last odd row of each level: x_{2K+2} = x_2K (reflection; exact at the matrix bottom)
+template <int L, int l>
+__device__ __forceinline__ void inv_finish(InvState& st, const InvOut& o, const StreamCtx& c) {
+    constexpr int NV = 8 >> (l - 1);
+    auto& s = iline<l>(st);
+    if (s.n > 0) {
+        int xo[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) xo[i] = s.D[i] + s.X[i];   // d + (2x >> 1)
+        inv_emit<L, l>(st, xo, 2 * ((st.kf >> l) + s.n - 1) + 1, o, c);
+    }
+    if constexpr (l > 1) inv_finish<L, l - 1>(st, o, c);
+}
+
+template <int L>
+__global__ void __launch_bounds__(kStreamThreads) k_dwt_full_inv(const __grid_constant__ DwtParams p,
+                                                                 se_report* report, int seg, int ncg, int nseg) {
+    using F = FStream<L>;
+    constexpr int NV = 8 >> (L - 1), NH = NV / 2;
+    StreamCtx c;
+    int sg;
+    stream_ctx(c, p, F::HC, F::USE, seg, ncg, sg);
+    if (sg >= nseg) return;
+    const int P0 = max(c.A - F::H, 0), P1 = min(c.B + F::H, c.R);
+    InvOut o{p.coef, p.out, p.n_bytes, report};
+    InvState st;
+    st.kf = P0;
+    st.l1.n = 0;
+    st.l2.n = 0;
+    st.l3.n = 0;
+    st.bad = 0;
+    for (int k = P0 >> L; k < (P1 >> L); ++k) {
+        int ll[NH], hl[NH], lh[NH], hh[NH];
+        load_band<L, NH>(ll, o, c, k, false, false);
+        load_band<L, NH>(hl, o, c, k, false, true);
+        load_band<L, NH>(lh, o, c, k, true, false);
+        load_band<L, NH>(hh, o, c, k, true, true);
+        int sr[NV], dr[NV];
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+            sr[2 * i] = ll[i];
+            sr[2 * i + 1] = hl[i];
+            dr[2 * i] = lh[i];
+            dr[2 * i + 1] = hh[i];
+        }
+        inv_push<L, L>(st, sr, dr, o, c);
+    }
+    inv_finish<L, L>(st, o, c);
 }
 
 template <int L, bool MASK>
@@ -335,21 +459,34 @@ __global__ void __launch_bounds__(kBlocksPerCta, 4) k_recover_full(const __grid_
 
 // ---------------------------------------------------------------- launchers
 
+// Launch shape: warps = column groups x row segments; segments of 256 rows,
+// halved (down to 32) until the grid holds enough warps to fill the SMs.
+template <int L>
+static void stream_shape(const DwtParams& p, int& seg, int& ncg, int& nseg, unsigned& grid) {
+    using F = FStream<L>;
+    ncg = (int)((p.width / 8 + F::USE - 1) / F::USE);
+    const uint64_t rows = std::min<uint64_t>(p.row0 + p.rows_out, p.rows) - p.row0;
+    seg = 256;
+    while (seg > 32 && (uint64_t)ncg * ((rows + seg - 1) / seg) < 148ull * 48) seg /= 2;
+    nseg = (int)((rows + seg - 1) / seg);
+    grid = (unsigned)(((uint64_t)ncg * nseg + kStreamWarps - 1) / kStreamWarps);
+}
+
 template <int L>
 static int full_fwd_l(const DwtParams& p, cudaStream_t s) {
-    using T = FullTile<L>;
-    cudaFuncSetAttribute(k_dwt_full_fwd<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
-    const dim3 grid((unsigned)((p.width + kTileC - 1) / kTileC), (unsigned)((p.rows_out + kTileR - 1) / kTileR));
-    k_dwt_full_fwd<L><<<grid, kFullThreads, T::smem, s>>>(p);
+    int seg, ncg, nseg;
+    unsigned grid;
+    stream_shape<L>(p, seg, ncg, nseg, grid);
+    if (grid) k_dwt_full_fwd<L><<<grid, kStreamThreads, 0, s>>>(p, seg, ncg, nseg);
     return (int)cudaGetLastError();
 }
 
 template <int L>
 static int full_inv_l(const DwtParams& p, se_report* rep, cudaStream_t s) {
-    using T = FullTile<L>;
-    cudaFuncSetAttribute(k_dwt_full_inv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::smem);
-    const dim3 grid((unsigned)((p.width + kTileC - 1) / kTileC), (unsigned)((p.rows_out + kTileR - 1) / kTileR));
-    k_dwt_full_inv<L><<<grid, kFullThreads, T::smem, s>>>(p, rep);
+    int seg, ncg, nseg;
+    unsigned grid;
+    stream_shape<L>(p, seg, ncg, nseg, grid);
+    if (grid) k_dwt_full_inv<L><<<grid, kStreamThreads, 0, s>>>(p, rep, seg, ncg, nseg);
     return (int)cudaGetLastError();
 }
 

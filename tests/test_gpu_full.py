@@ -1,5 +1,5 @@
 """GPU parity of FULL-matrix mode (row a11) against the oracle, bit-exact:
-whole-matrix Mallat coefficients (tiles with halos, borders reflected per
+whole-matrix Mallat coefficients (line-based lifting with row / column halos, borders reflected per
 level), footprint fragments with the FULL widths (C23), recover and the
 corruption report.  Sizes span several 64 x 128 tiles in both directions,
 ragged tails and matrices smaller than one tile."""
