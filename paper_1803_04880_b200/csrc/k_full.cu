@@ -21,8 +21,9 @@
 // side, so after L levels an output depends on inputs within 2(2^L - 1)
 // samples.  Warps overlap by HC chunks on each side (their edge lanes compute
 // but do not store); segments process H rows before and after their output
-// rows (H = 4 / 8 / 16: >= 2(2^L - 1), a multiple of 2^L so the lifting
-// phase of the segment equals the global one).  The first pair of a segment
+// rows (H = 8 / 8 / 16: >= 2(2^L - 1), a multiple of 8, so the lifting phase
+// of the segment equals the global one and rows go in blocks of 8 whose
+// parities at every level are compile-time constants).  The first pair of a segment
 // and the last one take the matrix-border rules (d(-1) = d(0), x(N) = x(N-2));
 // exact at the matrix borders, elsewhere their error stays inside the halo.
 #include <cuda_runtime.h>
@@ -40,7 +41,7 @@ template <int L>
 struct FStream {
     static constexpr int HC = L == 3 ? 2 : 1;                  // overlap chunks per warp side
     static constexpr int USE = 32 - 2 * HC;                    // chunks a warp stores
-    static constexpr int H = L == 1 ? 4 : L == 2 ? 8 : 16;      // halo rows
+    static constexpr int H = L == 3 ? 16 : 8;                   // halo rows (>= 2(2^L - 1), multiple of 8)
 };
 
 // Forward 1-D lifting of one level along a row: v holds NV samples of the
@@ -86,20 +87,6 @@ __device__ __forceinline__ void st_band(int16_t* g, const int (&v)[NV]) {
     }
 }
 
-template <int NH>
-__device__ __forceinline__ void ld_band(const int16_t* g, int (&v)[NH]) {
-    if constexpr (NH == 4) {
-        const uint2 q = __ldg(reinterpret_cast<const uint2*>(g));
-        v[0] = (int)(int16_t)(q.x & 0xffff); v[1] = (int)q.x >> 16;
-        v[2] = (int)(int16_t)(q.y & 0xffff); v[3] = (int)q.y >> 16;
-    } else if constexpr (NH == 2) {
-        const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(g));
-        v[0] = (int)(int16_t)(q & 0xffff); v[1] = (int)q >> 16;
-    } else {
-        v[0] = __ldg(g);
-    }
-}
-
 struct StreamCtx {
     int W, R;
     int c0;               // first column of the lane's chunk (outside [0, W): a dummy lane)
@@ -129,12 +116,16 @@ __device__ __forceinline__ auto& fline(FwdState& s) {
     else return s.l3;
 }
 
-template <int L, int l>
+// QM: the level-l row index of the row being pushed, mod 2^(L - l + 1) — a
+// compile-time constant (blocks of 8 input rows from a multiple of 8), so the
+// even / odd roles of the rows are static and the registers get renamed
+// instead of copied.  The LL row a level-l pair hands down has index k = q/2 - 1.
+template <int L, int l, int QM>
 __device__ __forceinline__ void fwd_push(FwdState& st, int (&x)[8 >> (l - 1)], int16_t* coef, const StreamCtx& c);
 
 // A finished pair of level l (rows 2k, 2k+1 of the level): s row (vertical
 // low) and d row.  Stores HL / LH / HH (and LL at l = L); LL feeds level l+1.
-template <int L, int l>
+template <int L, int l, int QM>
 __device__ __forceinline__ void fwd_emit(FwdState& st, int (&sv)[8 >> (l - 1)], const int (&d)[8 >> (l - 1)],
                                          int k, int16_t* coef, const StreamCtx& c) {
     constexpr int NV = 8 >> (l - 1), NH = NV / 2;
@@ -151,12 +142,12 @@ __device__ __forceinline__ void fwd_emit(FwdState& st, int (&sv)[8 >> (l - 1)], 
         int y[NH];
 #pragma unroll
         for (int i = 0; i < NH; ++i) y[i] = sv[2 * i];
-        fwd_push<L, l + 1>(st, y, coef, c);
+        fwd_push<L, l + 1, ((QM >> 1) - 1) & ((1 << (L - l)) - 1)>(st, y, coef, c);
     }
 }
 
 // Pair (E, O) completed by the next even row xn (x(N) = x(N-2) at the end: xn = E).
-template <int L, int l>
+template <int L, int l, int QM>
 __device__ __forceinline__ void fwd_pair(FwdState& st, const int (&xn)[8 >> (l - 1)], int16_t* coef,
                                          const StreamCtx& c) {
     constexpr int NV = 8 >> (l - 1);
@@ -164,22 +155,25 @@ __device__ __forceinline__ void fwd_pair(FwdState& st, const int (&xn)[8 >> (l -
     int d[NV], sv[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) d[i] = s.O[i] - ((s.E[i] + xn[i]) >> 1);
-    const bool first = s.n == 2;                                // d(-1) = d(0)
+    if (s.n == 2) {                                             // first pair: d(-1) = d(0)
 #pragma unroll
-    for (int i = 0; i < NV; ++i) sv[i] = s.E[i] + (((first ? d[i] : s.D[i]) + d[i] + 2) >> 2);
+        for (int i = 0; i < NV; ++i) s.D[i] = d[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) sv[i] = s.E[i] + ((s.D[i] + d[i] + 2) >> 2);
 #pragma unroll
     for (int i = 0; i < NV; ++i) s.D[i] = d[i];
     const int k = ((st.kf >> (l - 1)) + s.n - 2) >> 1;
-    fwd_emit<L, l>(st, sv, d, k, coef, c);
+    fwd_emit<L, l, QM>(st, sv, d, k, coef, c);
 }
 
-template <int L, int l>
+template <int L, int l, int QM>
 __device__ __forceinline__ void fwd_push(FwdState& st, int (&x)[8 >> (l - 1)], int16_t* coef, const StreamCtx& c) {
     constexpr int NV = 8 >> (l - 1);
     auto& s = fline<l>(st);
     hfwd<NV>(x, c.c0 >> (l - 1), c.W >> (l - 1));             // row pass of level l
-    if ((s.n & 1) == 0) {
-        if (s.n >= 2) fwd_pair<L, l>(st, x, coef, c);
+    if constexpr ((QM & 1) == 0) {
+        if (s.n >= 2) fwd_pair<L, l, QM>(st, x, coef, c);
 #pragma unroll
         for (int i = 0; i < NV; ++i) s.E[i] = x[i];
     } else {
@@ -192,11 +186,11 @@ __device__ __forceinline__ void fwd_push(FwdState& st, int (&x)[8 >> (l - 1)], i
 template <int L, int l>
 __device__ __forceinline__ void fwd_finish(FwdState& st, int16_t* coef, const StreamCtx& c) {
     auto& s = fline<l>(st);
-    if (s.n >= 2 && (s.n & 1) == 0) {
+    if (s.n >= 2) {                                             // pending pair (row counts are even)
         int e[8 >> (l - 1)];
 #pragma unroll
         for (int i = 0; i < (8 >> (l - 1)); ++i) e[i] = s.E[i];
-        fwd_pair<L, l>(st, e, coef, c);                         // x(N) = x(N - 2)
+        fwd_pair<L, l, 0>(st, e, coef, c);                      // x(N) = x(N - 2)
     }
     if constexpr (l < L) fwd_finish<L, l + 1>(st, coef, c);
 }
@@ -238,6 +232,20 @@ __device__ __forceinline__ void stream_ctx(StreamCtx& c, const DwtParams& p, int
     c.src_rows = (int)p.src_rows;
 }
 
+template <int L, int J>
+__device__ __forceinline__ void fwd_rows(FwdState& st, const uint2 (&q)[8], int16_t* coef, const StreamCtx& c) {
+    if constexpr (J < 8) {
+        int x[8];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            x[b] = (int)((q[J].x >> (8 * b)) & 0xff) - 128;
+            x[4 + b] = (int)((q[J].y >> (8 * b)) & 0xff) - 128;
+        }
+        fwd_push<L, 1, J & ((1 << L) - 1)>(st, x, coef, c);
+        fwd_rows<L, J + 1>(st, q, coef, c);
+    }
+}
+
 template <int L>
 __global__ void __launch_bounds__(kStreamThreads) k_dwt_full_fwd(const __grid_constant__ DwtParams p, int seg,
                                                                  int ncg, int nseg) {
@@ -253,17 +261,19 @@ __global__ void __launch_bounds__(kStreamThreads) k_dwt_full_fwd(const __grid_co
     st.l1.n = 0;
     st.l2.n = 0;
     st.l3.n = 0;
-    uint2 nxt = fetch_row(p, P0, c.c0, col_ok);
-    for (int r = P0; r < P1; ++r) {
-        const uint2 q = nxt;
-        if (r + 1 < P1) nxt = fetch_row(p, r + 1, c.c0, col_ok);
-        int x[8];
+    for (int r = P0; r < P1; r += 8) {                         // blocks of 8 rows
+        uint2 q[8];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            x[b] = (int)((q.x >> (8 * b)) & 0xff) - 128;
-            x[4 + b] = (int)((q.y >> (8 * b)) & 0xff) - 128;
+        for (int j = 0; j < 8; ++j) q[j] = fetch_row(p, r + j, c.c0, col_ok);
+        if (r + 8 < P1 && col_ok && (threadIdx.x & 15) == 0) {   // next block -> L2
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int rr = r + 8 + j - (int)p.src_row0;
+                if (rr >= 0 && rr < (int)p.src_rows)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.in + (uint64_t)rr * p.width + c.c0));
+            }
         }
-        fwd_push<L, 1>(st, x, p.coef, c);
+        fwd_rows<L, 0>(st, q, p.coef, c);
     }
     fwd_finish<L, 1>(st, p.coef, c);
 }
@@ -296,28 +306,63 @@ struct InvOut {
     se_report* report;
 };
 
-template <int L, int l>
-__device__ __forceinline__ void inv_push(InvState& st, const int (&sr)[8 >> (l - 1)],
-                                         const int (&dr)[8 >> (l - 1)], const InvOut& o, const StreamCtx& c);
-
-// band row j of level l (NH values at the lane's columns), 0 outside the source window
-template <int l, int NH>
-__device__ __forceinline__ void load_band(int (&v)[NH], const InvOut& o, const StreamCtx& c, int j, bool hr, bool hc) {
-    const int sb0 = c.src0 >> l, sbn = c.src_rows >> l;
-    if (c.c0 < 0 || c.c0 >= c.W || j < sb0 || j >= sb0 + sbn) {
-#pragma unroll
-        for (int i = 0; i < NH; ++i) v[i] = 0;
-        return;
-    }
-    const int64_t row = (hr ? sbn : 0) + (j - sb0);
-    const int col = (hc ? (c.W >> l) : 0) + (c.c0 >> l);
-    ld_band<NH>(o.coef + row * c.W + col, v);
+// One iteration's band rows, raw (8 output rows = 8 >> L top-level pairs):
+// level l rows jb_l + t, t < 8 >> l, jb_l = (k0 << (L - l)) - (2^(L - l) - 1)
+// (the rows the iteration's pairs emit), bands LL (top level only), HL, LH,
+// HH.  All loads of an iteration are issued before its arithmetic.
+struct InvPre {
+    uint2 b1[4][4];
+    uint2 b2[2][4];
+    uint2 b3[1][4];
+};
+template <int l>
+__device__ __forceinline__ auto& prow(InvPre& p) {
+    if constexpr (l == 1) return p.b1;
+    else if constexpr (l == 2) return p.b2;
+    else return p.b3;
 }
 
-// A row j of level l - 1's low-low band (or of the output, l = 1) rebuilt
-// vertically at level l: undo the row pass, then hand it down.
+template <int l>
+__device__ __forceinline__ uint2 ld_raw(const InvOut& o, const StreamCtx& c, int j, bool hr, bool hc) {
+    const int sb0 = c.src0 >> l, sbn = c.src_rows >> l;
+    if (c.c0 < 0 || c.c0 >= c.W || j < sb0 || j >= sb0 + sbn) return make_uint2(0, 0);
+    const int16_t* g = o.coef + ((int64_t)(hr ? sbn : 0) + (j - sb0)) * c.W + (hc ? (c.W >> l) : 0) + (c.c0 >> l);
+    if constexpr (l == 1) return __ldg(reinterpret_cast<const uint2*>(g));
+    else if constexpr (l == 2) return make_uint2(__ldg(reinterpret_cast<const uint32_t*>(g)), 0u);
+    else return make_uint2((uint32_t)(uint16_t)__ldg(g), 0u);
+}
+
+template <int NH>
+__device__ __forceinline__ void unpack_band(uint2 q, int (&v)[NH]) {
+    v[0] = (int)(int16_t)(q.x & 0xffff);
+    if constexpr (NH >= 2) v[1] = (int)q.x >> 16;
+    if constexpr (NH == 4) {
+        v[2] = (int)(int16_t)(q.y & 0xffff);
+        v[3] = (int)q.y >> 16;
+    }
+}
+
 template <int L, int l>
-__device__ __forceinline__ void inv_emit(InvState& st, int (&v)[8 >> (l - 1)], int j, const InvOut& o,
+__device__ __forceinline__ void preload(InvPre& pre, const InvOut& o, const StreamCtx& c, int k0) {
+    constexpr int NR = 8 >> l;
+    const int jb = (k0 << (L - l)) - ((1 << (L - l)) - 1);
+    auto& b = prow<l>(pre);
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+#pragma unroll
+        for (int band = (l == L ? 0 : 1); band < 4; ++band) b[t][band] = ld_raw<l>(o, c, jb + t, band >= 2, band & 1);
+    if constexpr (l > 1) preload<L, l - 1>(pre, o, c, k0);
+}
+
+template <int L, int l, int T>
+__device__ __forceinline__ void inv_push(InvState& st, const int (&sr)[8 >> (l - 1)], const int (&dr)[8 >> (l - 1)],
+                                         InvPre& pre, const InvOut& o, const StreamCtx& c);
+
+// A row j of level l - 1's low-low band (or of the output, l = 1) rebuilt
+// vertically at level l: undo the row pass, then hand it down.  T >= 0: the
+// row's band data sit in pre (static index); T < 0: loaded here (finish).
+template <int L, int l, int T>
+__device__ __forceinline__ void inv_emit(InvState& st, int (&v)[8 >> (l - 1)], int j, InvPre& pre, const InvOut& o,
                                          const StreamCtx& c) {
     constexpr int NV = 8 >> (l - 1);
     hinv<NV>(v, c.c0 >> (l - 1), c.W >> (l - 1));
@@ -355,9 +400,16 @@ __device__ __forceinline__ void inv_emit(InvState& st, int (&v)[8 >> (l - 1)], i
         // pair j of level l - 1: s row = (LL_{l-1}[j], HL_{l-1}[j]) interleaved, d row = (LH, HH)
         constexpr int NV2 = 2 * NV;
         int hl[NV], lh[NV], hh[NV];
-        load_band<l - 1, NV>(hl, o, c, j, false, true);
-        load_band<l - 1, NV>(lh, o, c, j, true, false);
-        load_band<l - 1, NV>(hh, o, c, j, true, true);
+        if constexpr (T >= 0) {
+            auto& b = prow<l - 1>(pre);
+            unpack_band<NV>(b[T][1], hl);
+            unpack_band<NV>(b[T][2], lh);
+            unpack_band<NV>(b[T][3], hh);
+        } else {
+            unpack_band<NV>(ld_raw<l - 1>(o, c, j, false, true), hl);
+            unpack_band<NV>(ld_raw<l - 1>(o, c, j, true, false), lh);
+            unpack_band<NV>(ld_raw<l - 1>(o, c, j, true, true), hh);
+        }
         int sr[NV2], dr[NV2];
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
@@ -366,27 +418,31 @@ __device__ __forceinline__ void inv_emit(InvState& st, int (&v)[8 >> (l - 1)], i
             dr[2 * i] = lh[i];
             dr[2 * i + 1] = hh[i];
         }
-        inv_push<L, l - 1>(st, sr, dr, o, c);
+        inv_push<L, l - 1, T>(st, sr, dr, pre, o, c);
     }
 }
 
 // Pair k of level l arrives: x_2k = s_k - (d_{k-1} + d_k + 2) >> 2, then
-// x_{2k-1} = d_{k-1} + (x_{2k-2} + x_2k) >> 1; rows leave in order.
-template <int L, int l>
-__device__ __forceinline__ void inv_push(InvState& st, const int (&sr)[8 >> (l - 1)],
-                                         const int (&dr)[8 >> (l - 1)], const InvOut& o, const StreamCtx& c) {
+// x_{2k-1} = d_{k-1} + (x_{2k-2} + x_2k) >> 1; rows leave in order.  Pair T
+// of an iteration emits rows 2T and 2T + 1 of the next level's rows.
+template <int L, int l, int T>
+__device__ __forceinline__ void inv_push(InvState& st, const int (&sr)[8 >> (l - 1)], const int (&dr)[8 >> (l - 1)],
+                                         InvPre& pre, const InvOut& o, const StreamCtx& c) {
     constexpr int NV = 8 >> (l - 1);
     auto& s = iline<l>(st);
     const int k = (st.kf >> l) + s.n;
-    int x[NV];
-    const bool first = s.n == 0;                                // d(-1) = d(0)
+    if (s.n == 0) {                                             // first pair: d(-1) = d(0)
 #pragma unroll
-    for (int i = 0; i < NV; ++i) x[i] = sr[i] - (((first ? dr[i] : s.D[i]) + dr[i] + 2) >> 2);
-    if (!first) {
+        for (int i = 0; i < NV; ++i) s.D[i] = dr[i];
+    }
+    int x[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) x[i] = sr[i] - ((s.D[i] + dr[i] + 2) >> 2);
+    if (s.n != 0) {
         int xo[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) xo[i] = s.D[i] + ((s.X[i] + x[i]) >> 1);
-        inv_emit<L, l>(st, xo, 2 * k - 1, o, c);
+        inv_emit<L, l, (T >= 0 ? 2 * T : -1)>(st, xo, 2 * k - 1, pre, o, c);
     }
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -394,28 +450,50 @@ __device__ __forceinline__ void inv_push(InvState& st, const int (&sr)[8 >> (l -
         s.D[i] = dr[i];
     }
     ++s.n;
-    inv_emit<L, l>(st, x, 2 * k, o, c);
+    inv_emit<L, l, (T >= 0 ? 2 * T + 1 : -1)>(st, x, 2 * k, pre, o, c);
 }
 
 // last odd row of each level: x_{2K+2} = x_2K (reflection; exact at the matrix bottom)
 template <int L, int l>
-__device__ __forceinline__ void inv_finish(InvState& st, const InvOut& o, const StreamCtx& c) {
+__device__ __forceinline__ void inv_finish(InvState& st, InvPre& pre, const InvOut& o, const StreamCtx& c) {
     constexpr int NV = 8 >> (l - 1);
     auto& s = iline<l>(st);
     if (s.n > 0) {
         int xo[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) xo[i] = s.D[i] + s.X[i];   // d + (2x >> 1)
-        inv_emit<L, l>(st, xo, 2 * ((st.kf >> l) + s.n - 1) + 1, o, c);
+        inv_emit<L, l, -1>(st, xo, 2 * ((st.kf >> l) + s.n - 1) + 1, pre, o, c);
     }
-    if constexpr (l > 1) inv_finish<L, l - 1>(st, o, c);
+    if constexpr (l > 1) inv_finish<L, l - 1>(st, pre, o, c);
+}
+
+template <int L, int I>
+__device__ __forceinline__ void inv_top(InvState& st, InvPre& pre, const InvOut& o, const StreamCtx& c) {
+    if constexpr (I < (8 >> L)) {
+        constexpr int NV = 8 >> (L - 1), NH = NV / 2;
+        auto& b = prow<L>(pre);
+        int ll[NH], hl[NH], lh[NH], hh[NH];
+        unpack_band<NH>(b[I][0], ll);
+        unpack_band<NH>(b[I][1], hl);
+        unpack_band<NH>(b[I][2], lh);
+        unpack_band<NH>(b[I][3], hh);
+        int sr[NV], dr[NV];
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+            sr[2 * i] = ll[i];
+            sr[2 * i + 1] = hl[i];
+            dr[2 * i] = lh[i];
+            dr[2 * i + 1] = hh[i];
+        }
+        inv_push<L, L, I>(st, sr, dr, pre, o, c);
+        inv_top<L, I + 1>(st, pre, o, c);
+    }
 }
 
 template <int L>
 __global__ void __launch_bounds__(kStreamThreads) k_dwt_full_inv(const __grid_constant__ DwtParams p,
                                                                  se_report* report, int seg, int ncg, int nseg) {
     using F = FStream<L>;
-    constexpr int NV = 8 >> (L - 1), NH = NV / 2;
     StreamCtx c;
     int sg;
     stream_ctx(c, p, F::HC, F::USE, seg, ncg, sg);
@@ -428,23 +506,12 @@ __global__ void __launch_bounds__(kStreamThreads) k_dwt_full_inv(const __grid_co
     st.l2.n = 0;
     st.l3.n = 0;
     st.bad = 0;
-    for (int k = P0 >> L; k < (P1 >> L); ++k) {
-        int ll[NH], hl[NH], lh[NH], hh[NH];
-        load_band<L, NH>(ll, o, c, k, false, false);
-        load_band<L, NH>(hl, o, c, k, false, true);
-        load_band<L, NH>(lh, o, c, k, true, false);
-        load_band<L, NH>(hh, o, c, k, true, true);
-        int sr[NV], dr[NV];
-#pragma unroll
-        for (int i = 0; i < NH; ++i) {
-            sr[2 * i] = ll[i];
-            sr[2 * i + 1] = hl[i];
-            dr[2 * i] = lh[i];
-            dr[2 * i + 1] = hh[i];
-        }
-        inv_push<L, L>(st, sr, dr, o, c);
+    InvPre pre;
+    for (int k0 = P0 >> L; k0 < (P1 >> L); k0 += 8 >> L) {     // 8 output rows per iteration
+        preload<L, L>(pre, o, c, k0);
+        inv_top<L, 0>(st, pre, o, c);
     }
-    inv_finish<L, L>(st, o, c);
+    inv_finish<L, L>(st, pre, o, c);
 }
 
 template <int L, bool MASK>
