@@ -136,7 +136,12 @@ __device__ __forceinline__ void fwd_emit(FwdState& st, int (&sv)[8 >> (l - 1)], 
         st_band<NH, 1>(coef + top * c.W + colH, sv);             // HL: vertical low, horizontal high
         st_band<NH, 0>(coef + bot * c.W + colL, d);              // LH
         st_band<NH, 1>(coef + bot * c.W + colH, d);              // HH
-        if constexpr (l == L) st_band<NH, 0>(coef + top * c.W + colL, sv);   // LL_L
+        if constexpr (l == L) {                                 // LL_L, centered (C8) here
+            int ll[NV];
+#pragma unroll
+            for (int i = 0; i < NV; i += 2) ll[i] = sv[i] - 128;
+            st_band<NH, 0>(coef + top * c.W + colL, ll);
+        }
     }
     if constexpr (l < L) {
         int y[NH];
@@ -195,10 +200,13 @@ __device__ __forceinline__ void fwd_finish(FwdState& st, int16_t* coef, const St
     if constexpr (l < L) fwd_finish<L, l + 1>(st, coef, c);
 }
 
-// 8 bytes of row r at columns c0..c0+7 as raw bytes: centering (C8) is
-// applied by the caller (x = b - 128); bytes past n read 0 (-> -128, C18),
-// other bytes of rows outside the source window read 0x80 (-> 0; they only
-// feed halo rows).
+// 8 bytes of row r at columns c0..c0+7 as raw bytes.  The lifting runs on
+// the uncentered bytes: shifting every sample by an even constant c shifts
+// each s by c and leaves each d unchanged ((a + 2c) >> 1 = (a >> 1) + c in the
+// predict; the update adds d's only), level after level, so the centering
+// (C8, x = b - 128) is applied to LL_L alone (fwd_emit; the inverse adds it
+// back on load).  Bytes past n read 0 (x = -128, C18); other bytes of rows
+// outside the source window read 0x80 (x = 0; they only feed halo rows).
 __device__ __forceinline__ uint2 fetch_row(const DwtParams& p, int r, int c0, bool col_ok) {
     const uint2 none = make_uint2(0x80808080u, 0x80808080u);
     if (!col_ok) return none;
@@ -238,8 +246,8 @@ __device__ __forceinline__ void fwd_rows(FwdState& st, const uint2 (&q)[8], int1
         int x[8];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            x[b] = (int)((q[J].x >> (8 * b)) & 0xff) - 128;
-            x[4 + b] = (int)((q[J].y >> (8 * b)) & 0xff) - 128;
+            x[b] = (int)((q[J].x >> (8 * b)) & 0xff);             // uncentered: see fwd_emit
+            x[4 + b] = (int)((q[J].y >> (8 * b)) & 0xff);
         }
         fwd_push<L, 1, J & ((1 << L) - 1)>(st, x, coef, c);
         fwd_rows<L, J + 1>(st, q, coef, c);
@@ -372,7 +380,7 @@ __device__ __forceinline__ void inv_emit(InvState& st, int (&v)[8 >> (l - 1)], i
             int orv = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int b = v[i] + 128;
+                const int b = v[i];                             // uncentered (LL_L + 128 on load)
                 orv |= b;
                 w[i >> 2] |= (uint32_t)(b & 0xff) << (8 * (i & 3));
             }
@@ -474,6 +482,8 @@ __device__ __forceinline__ void inv_top(InvState& st, InvPre& pre, const InvOut&
         auto& b = prow<L>(pre);
         int ll[NH], hl[NH], lh[NH], hh[NH];
         unpack_band<NH>(b[I][0], ll);
+#pragma unroll
+        for (int i = 0; i < NH; ++i) ll[i] += 128;                // uncentered domain (see fetch_row)
         unpack_band<NH>(b[I][1], hl);
         unpack_band<NH>(b[I][2], lh);
         unpack_band<NH>(b[I][3], hh);
