@@ -271,8 +271,15 @@ __global__ void __launch_bounds__(kStreamThreads) k_dwt_full_fwd(const __grid_co
     st.l3.n = 0;
     for (int r = P0; r < P1; r += 8) {                         // blocks of 8 rows
         uint2 q[8];
+        const int lr = r - (int)p.src_row0;                     // local row in the source window
+        if (col_ok && lr >= 0 && lr + 8 <= (int)p.src_rows && (uint64_t)(r + 7) * p.width + c.c0 + 8 <= p.n_bytes) {
+            const uint8_t* src = p.in + (uint64_t)lr * p.width + c.c0;   // whole block present
 #pragma unroll
-        for (int j = 0; j < 8; ++j) q[j] = fetch_row(p, r + j, c.c0, col_ok);
+            for (int j = 0; j < 8; ++j) q[j] = __ldg(reinterpret_cast<const uint2*>(src + (uint64_t)j * p.width));
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) q[j] = fetch_row(p, r + j, c.c0, col_ok);
+        }
         if (r + 8 < P1 && col_ok && (threadIdx.x & 15) == 0) {   // next block -> L2
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -350,16 +357,45 @@ __device__ __forceinline__ void unpack_band(uint2 q, int (&v)[NH]) {
     }
 }
 
+// every band row of the iteration inside the source window (and the lane's
+// chunk inside the matrix): the loads need no tests
 template <int L, int l>
-__device__ __forceinline__ void preload(InvPre& pre, const InvOut& o, const StreamCtx& c, int k0) {
+__device__ __forceinline__ bool window_ok(const StreamCtx& c, int k0) {
+    const int jb = (k0 << (L - l)) - ((1 << (L - l)) - 1);
+    const int sb0 = c.src0 >> l, sbn = c.src_rows >> l;
+    bool ok = jb >= sb0 && jb + (8 >> l) <= sb0 + sbn;
+    if constexpr (l > 1) ok = ok && window_ok<L, l - 1>(c, k0);
+    return ok;
+}
+
+template <int L, int l>
+__device__ __forceinline__ void preload(InvPre& pre, const InvOut& o, const StreamCtx& c, int k0, bool fast) {
     constexpr int NR = 8 >> l;
     const int jb = (k0 << (L - l)) - ((1 << (L - l)) - 1);
     auto& b = prow<l>(pre);
+    if (fast) {
+        const int sb0 = c.src0 >> l, sbn = c.src_rows >> l;
+        const int16_t* g0 = o.coef + (int64_t)(jb - sb0) * c.W + (c.c0 >> l);
+        const int64_t hr = (int64_t)sbn * c.W;
+        const int hc = c.W >> l;
 #pragma unroll
-    for (int t = 0; t < NR; ++t)
+        for (int t = 0; t < NR; ++t) {
 #pragma unroll
-        for (int band = (l == L ? 0 : 1); band < 4; ++band) b[t][band] = ld_raw<l>(o, c, jb + t, band >= 2, band & 1);
-    if constexpr (l > 1) preload<L, l - 1>(pre, o, c, k0);
+            for (int band = (l == L ? 0 : 1); band < 4; ++band) {
+                const int16_t* g = g0 + (int64_t)t * c.W + (band >= 2 ? hr : 0) + ((band & 1) ? hc : 0);
+                if constexpr (l == 1) b[t][band] = __ldg(reinterpret_cast<const uint2*>(g));
+                else if constexpr (l == 2) b[t][band] = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(g)), 0u);
+                else b[t][band] = make_uint2((uint32_t)(uint16_t)__ldg(g), 0u);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < NR; ++t)
+#pragma unroll
+            for (int band = (l == L ? 0 : 1); band < 4; ++band)
+                b[t][band] = ld_raw<l>(o, c, jb + t, band >= 2, band & 1);
+    }
+    if constexpr (l > 1) preload<L, l - 1>(pre, o, c, k0, fast);
 }
 
 template <int L, int l, int T>
@@ -518,7 +554,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_dwt_full_inv(const __grid_co
     st.bad = 0;
     InvPre pre;
     for (int k0 = P0 >> L; k0 < (P1 >> L); k0 += 8 >> L) {     // 8 output rows per iteration
-        preload<L, L>(pre, o, c, k0);
+        preload<L, L>(pre, o, c, k0, c.c0 >= 0 && c.c0 < c.W && window_ok<L, L>(c, k0));
         inv_top<L, 0>(st, pre, o, c);
     }
     inv_finish<L, L>(st, pre, o, c);
