@@ -246,8 +246,8 @@ __device__ __forceinline__ void fwd_rows(FwdState& st, const uint2 (&q)[8], int1
         int x[8];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            x[b] = (int)((q[J].x >> (8 * b)) & 0xff);             // uncentered: see fwd_emit
-            x[4 + b] = (int)((q[J].y >> (8 * b)) & 0xff);
+            x[b] = (int)__byte_perm(q[J].x, 0u, 0x4440u + b);     // zero-extended byte (uncentered: see fwd_emit)
+            x[4 + b] = (int)__byte_perm(q[J].y, 0u, 0x4440u + b);
         }
         fwd_push<L, 1, J & ((1 << L) - 1)>(st, x, coef, c);
         fwd_rows<L, J + 1>(st, q, coef, c);
@@ -573,14 +573,16 @@ __global__ void __launch_bounds__(kBlocksPerCta, 4) k_recover_full(const __grid_
 // ---------------------------------------------------------------- launchers
 
 // Launch shape: warps = column groups x row segments; segments of 256 rows,
-// halved (down to 32) until the grid holds enough warps to fill the SMs.
+// halved (down to 32) until the grid holds one full wave of warps (24 per
+// SM at ~80 registers): shorter segments re-read relatively more halo rows
+// (2H per segment).
 template <int L>
 static void stream_shape(const DwtParams& p, int& seg, int& ncg, int& nseg, unsigned& grid) {
     using F = FStream<L>;
     ncg = (int)((p.width / 8 + F::USE - 1) / F::USE);
     const uint64_t rows = std::min<uint64_t>(p.row0 + p.rows_out, p.rows) - p.row0;
     seg = 256;
-    while (seg > 32 && (uint64_t)ncg * ((rows + seg - 1) / seg) < 148ull * 48) seg /= 2;
+    while (seg > 32 && (uint64_t)ncg * ((rows + seg - 1) / seg) < 148ull * 24) seg /= 2;
     nseg = (int)((rows + seg - 1) / seg);
     grid = (unsigned)(((uint64_t)ncg * nseg + kStreamWarps - 1) / kStreamWarps);
 }
