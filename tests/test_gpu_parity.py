@@ -115,6 +115,23 @@ def test_cipher_parity(dev, orc, n):
             assert np.array_equal(back.cpu().numpy(), x)
 
 
+@pytest.mark.parametrize("mode", [se.MODE_BLOCK8, se.MODE_FULL])
+@pytest.mark.parametrize("flags", [0, se.FLAG_PUBLIC_PLAIN])
+def test_empty_input(dev, orc, mode, flags):
+    """The degenerate case n = 0: empty fragments, empty recovery, the clean
+    report {-1, 0}, as the oracle; no kernel launches."""
+    x = torch.empty(0, dtype=torch.uint8, device=dev)
+    se.launch_count(reset=True)
+    a, b, c = se.fragment_protect(x, 64, 2, KEY, IV, mode=mode, flags=flags)
+    assert (a.numel(), b.numel(), c.numel()) == tuple(len(s) for s in orc.protect(np.zeros(0, np.uint8), 64, 2,
+                                                                                  KEY, IV, mode=mode, flags=flags))
+    y, rep = se.fragment_recover(a, b, c, 0, 64, 2, KEY, IV, mode=mode, flags=flags)
+    torch.cuda.synchronize()
+    assert y.numel() == 0 and rep.tolist() == [-1, 0]
+    assert se.launch_count() == 0
+    assert se.cipher_encrypt(KEY, IV, x).numel() == 0
+
+
 def test_launch_evidence(dev):
     x = to_dev(synth.random_bytes(1 << 16, 1), dev)
     se.launch_count(reset=True)
