@@ -560,13 +560,16 @@ __global__ void __launch_bounds__(kStreamThreads) k_dwt_full_inv(const __grid_co
     inv_finish<L, L>(st, pre, o, c);
 }
 
+#ifndef SE_MIN_CTAS_FULL
+#define SE_MIN_CTAS_FULL 4
+#endif
 template <int L, bool MASK>
-__global__ void __launch_bounds__(kBlocksPerCta, 4) k_protect_full(const __grid_constant__ FusedParams p) {
+__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS_FULL) k_protect_full(const __grid_constant__ FusedParams p) {
     protect_cta<L, MASK, 1>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
-__global__ void __launch_bounds__(kBlocksPerCta, 4) k_recover_full(const __grid_constant__ FusedParams p) {
+__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS_FULL) k_recover_full(const __grid_constant__ FusedParams p) {
     recover_cta<L, MASK, 1>(p, blockIdx.x);
 }
 
