@@ -593,7 +593,9 @@ def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=8 << 
     frag_bytes = lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"]
     mapped = bool(flags & se.FLAG_HOST_MAPPED)
     how = ("SE_FLAG_HOST_MAPPED: the kernels read / write the pinned host buffers over PCIe, no staging"
-           if mapped else f"{chunk_bytes >> 10} KiB chunks on {n_streams} streams")
+           if mapped else (f"{chunk_bytes >> 10} KiB chunks" if chunk_bytes else
+                           f"library-default chunks ({min(16 << 20, max(4 << 20, n // 4)) >> 10} KiB)")
+           + f" on {n_streams} streams")
     return {"value": round(n / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n + frag_bytes,
             "d2h_bytes_per_step": frag_bytes + n, "ms_per_step": round(ms, 4),
             "path": f"fragment_protect_host + fragment_recover_host (C ABI, pinned host buffers, {how}), "
@@ -895,7 +897,7 @@ def main():
     ap.add_argument("--plain", action="store_true", help="PUBLIC_PLAIN measurement mode (C26)")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of sustained warm-up load")
     ap.add_argument("--e2e-steps", type=int, default=20)
-    ap.add_argument("--e2e-chunk-kib", type=int, default=4096, help="host-API chunk size (input KiB)")
+    ap.add_argument("--e2e-chunk-kib", type=int, default=0, help="host-API chunk size (input KiB; 0 = library default)")
     ap.add_argument("--e2e-streams", type=int, default=3, help="host-API CUDA streams")
     ap.add_argument("--e2e-mapped", type=int, default=0, help="1: zero-copy host API (SE_FLAG_HOST_MAPPED)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -150,7 +150,7 @@ int fragment_recover_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total
  * n_streams CUDA streams, overlapping H2D copy, kernel and D2H copy
  * (the paper's transfer/compute overlap).  Blocking: returns
  * after the last D2H completes.  chunk_bytes = input bytes per chunk
- * (rounded to whole 128-block groups; 0 = 32 MiB). */
+ * (rounded to whole 128-block groups; 0 = n/4 within [4 MiB, 16 MiB]). */
 int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
                           const void* h_in, void* h_a, void* h_b, void* h_c,
                           uint64_t chunk_bytes, uint32_t n_streams);

@@ -51,6 +51,14 @@ struct Chunk {
 #ifndef SE_HOST_RAMP
 #define SE_HOST_RAMP 0
 #endif
+// chunk_bytes == 0: a quarter of the input, within [4 MiB, 16 MiB] — small
+// files need >= 3-4 chunks to overlap at all, large ones lose ~15 % of the
+// PCIe rate to per-chunk costs below ~16 MiB (tools/e2e_probe.py: 256 MiB
+// protect 28.7 GB/s at 4 MiB, 34.9 at 16 MiB, 92 % of the D2H-bound model).
+static uint64_t auto_chunk(uint64_t n) {
+    return std::min<uint64_t>(16ull << 20, std::max<uint64_t>(4ull << 20, n / 4));
+}
+
 static std::vector<Chunk> make_chunks(const se_geom* g, const se_layout& lay, uint64_t chunk_bytes) {
     const uint64_t bpr = g->width / 8, block_rows = lay.rows / 8;
     const uint64_t ga = chunk_block_align(lay);
@@ -318,7 +326,7 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
         if (cudaStreamSynchronize(ctx.streams[0]) != cudaSuccess) st = SE_ECUDA;
         return st;
     }
-    if (chunk_bytes == 0) chunk_bytes = 32ull << 20;
+    if (chunk_bytes == 0) chunk_bytes = auto_chunk(g->n_bytes);
     if (n_streams == 0) n_streams = 3;
     // FULL mode transforms the whole matrix: one chunk
     const std::vector<Chunk> chunks = g->mode == SE_MODE_FULL
@@ -415,7 +423,7 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
         if (st == SE_OK && h_report) *h_report = ctx.hreps[0];
         return st;
     }
-    if (chunk_bytes == 0) chunk_bytes = 32ull << 20;
+    if (chunk_bytes == 0) chunk_bytes = auto_chunk(g->n_bytes);
     if (n_streams == 0) n_streams = 3;
     const std::vector<Chunk> chunks = g->mode == SE_MODE_FULL
         ? std::vector<Chunk>{Chunk{0, g->n_bytes, 0, lay.n_blocks}} : make_chunks(g, lay, chunk_bytes);
