@@ -35,6 +35,25 @@ __device__ __forceinline__ int isub(int a, int b, int m1) {       // a - b, m1 =
     return r;
 }
 
+// floor(v / 4) + c.  SE_LIFT_QHI=1: one IMAD.HI (v * 2^30 >> 32, signed) on
+// the FMA pipe instead of SHF on the ALU pipe (q30 = one << 30, opaque so
+// ptxas keeps the multiply) - measured slower (C2 masked protect / recover
+// 182.7 / 183.9 vs 184.7 / 187.5 GB/s, plain 576 vs 640: IMAD.HI's two FMA
+// issue slots and latency cost more than the ALU slot saved), so off.
+#ifndef SE_LIFT_QHI
+#define SE_LIFT_QHI 0
+#endif
+__device__ __forceinline__ int qfloor4(int v, int c, int q30) {
+#if SE_LIFT_QHI
+    int r;
+    asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(q30), "r"(c));
+    return r;
+#else
+    (void)q30;
+    return (v >> 2) + c;
+#endif
+}
+
 // ------------------------------------------------------------------ lifting
 // Forward 1-D lifting of n samples in place: output [s(0..n/2) | d(0..n/2)].
 // Samples are NOT centered: lifting commutes exactly with adding a constant
@@ -54,7 +73,7 @@ __device__ __forceinline__ void lift_fwd(int (&x)[N], uint32_t one, int m1) {
 #pragma unroll
     for (int k = 0; k < H; ++k) {
         const int dm1 = (k == 0) ? d[0] : d[k - 1];                   // d(-1) = d(0)
-        s[k] = iadd(x[2 * k], iadd(iadd(dm1, d[k], one), 2, one) >> 2, one);   // Eq. 5.2 (+)
+        s[k] = qfloor4(iadd(iadd(dm1, d[k], one), 2, one), x[2 * k], (int)(one << 30));   // Eq. 5.2 (+)
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) { x[k] = s[k]; x[H + k] = d[k]; }
@@ -68,7 +87,7 @@ __device__ __forceinline__ void lift_inv(int (&y)[N], uint32_t one, int m1) {
 #pragma unroll
     for (int k = 0; k < H; ++k) {
         const int dm1 = (k == 0) ? y[H] : y[H + k - 1];
-        x[2 * k] = isub(y[k], iadd(iadd(dm1, y[H + k], one), 2, one) >> 2, m1);
+        x[2 * k] = isub(y[k], qfloor4(iadd(iadd(dm1, y[H + k], one), 2, one), 0, (int)(one << 30)), m1);
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) {
