@@ -43,14 +43,31 @@ __device__ __forceinline__ int isub(int a, int b, int m1) {       // a - b, m1 =
 #ifndef SE_LIFT_QHI
 #define SE_LIFT_QHI 0
 #endif
+#ifndef SE_LIFT_LEA
+#define SE_LIFT_LEA 2      // measured (C2 masked p / r GB/s): 0 182.7 / 187.2, 1 185.1 / 187.1, 2 185.1 / 188.7
+#endif
 __device__ __forceinline__ int qfloor4(int v, int c, int q30) {
 #if SE_LIFT_QHI
     int r;
     asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(q30), "r"(c));
     return r;
+#elif SE_LIFT_LEA
+    (void)q30;
+    return (v >> 2) + c;                  // ptxas: one LEA.HI (shift and add) on the ALU pipe
 #else
     (void)q30;
     return (v >> 2) + c;
+#endif
+}
+
+// a + (b >> 1): SE_LIFT_LEA >= 2 lets ptxas fuse it into one LEA.HI (ALU)
+// instead of SHF (ALU) + IMAD (FMA)
+__device__ __forceinline__ int add_half(int a, int b, uint32_t one) {
+#if SE_LIFT_LEA >= 2
+    (void)one;
+    return a + (b >> 1);
+#else
+    return iadd(a, b >> 1, one);
 #endif
 }
 
@@ -73,7 +90,11 @@ __device__ __forceinline__ void lift_fwd(int (&x)[N], uint32_t one, int m1) {
 #pragma unroll
     for (int k = 0; k < H; ++k) {
         const int dm1 = (k == 0) ? d[0] : d[k - 1];                   // d(-1) = d(0)
+#if SE_LIFT_LEA || SE_LIFT_QHI
         s[k] = qfloor4(iadd(iadd(dm1, d[k], one), 2, one), x[2 * k], (int)(one << 30));   // Eq. 5.2 (+)
+#else
+        s[k] = iadd(x[2 * k], iadd(iadd(dm1, d[k], one), 2, one) >> 2, one);              // Eq. 5.2 (+)
+#endif
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) { x[k] = s[k]; x[H + k] = d[k]; }
@@ -91,7 +112,7 @@ __device__ __forceinline__ void lift_inv(int (&y)[N], uint32_t one, int m1) {
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) {
-        if (2 * k + 2 < N) x[2 * k + 1] = iadd(y[H + k], iadd(x[2 * k], x[2 * k + 2], one) >> 1, one);
+        if (2 * k + 2 < N) x[2 * k + 1] = add_half(y[H + k], iadd(x[2 * k], x[2 * k + 2], one), one);
         else x[2 * k + 1] = iadd(y[H + k], x[2 * k], one);
     }
 #pragma unroll
