@@ -15,14 +15,24 @@ constexpr int kCipherThreads = 256;
 #define SE_LANE_THREADS 1024
 #endif
 constexpr int kLaneThreads = SE_LANE_THREADS;       // CTA size of the lane-table cipher (one 64 KB table per CTA)
+// Keystream next to a fused kernel (grid-stride).  Wide: 256-thread CTAs, up
+// to 8 per SM.  Narrow (SE_KS_NARROW=1 honours CipherParams::narrow, set by
+// the masked protect): one 128-thread CTA per SM, so all 5 fused CTAs of
+// every SM start at once beside it.  Measured on C2 (three A/B rounds):
+// protect 186.3 vs 184.4 GB/s, but the recover that follows 186.0 vs 188.4 —
+// round trip 93.1 vs 93.2, so off.
+#ifndef SE_KS_NARROW
+#define SE_KS_NARROW 0
+#endif
+constexpr int kKsThreads = 256, kKsNarrowThreads = 128;
+constexpr int kKsNarrowCtasPerSm = 1;
 
 // p.in == nullptr: write the keystream itself (used by the fused kernels,
 // which then XOR it into the private fragment, see fused_cta.cuh).
 // LANE: the 64 KB lane-replicated table (standalone cipher), else the 5 KB
 // tables (keystream next to a running fused kernel).
-template <bool LANE>
-__global__ void __launch_bounds__(LANE ? kLaneThreads : kCipherThreads) k_cipher_ctr(const __grid_constant__ CipherParams p) {
-    constexpr int NT = LANE ? kLaneThreads : kCipherThreads;
+template <bool LANE, int NT>
+__global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ CipherParams p) {
     // a dependent kernel launched with programmatic stream serialization may
     // start now; it waits (griddepcontrol.wait) before reading our output
     asm volatile("griddepcontrol.launch_dependents;");
@@ -140,18 +150,22 @@ int launch_cipher_ctr(const CipherParams& p, void* stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t nblk = (p.n + 15) / 16;
     const bool lane = p.in != nullptr || p.lane_lut;
-    const int nt = lane ? kLaneThreads : kCipherThreads;
+    const bool narrow = SE_KS_NARROW && !lane && p.narrow;
+    const int nt = lane ? kLaneThreads : narrow ? kKsNarrowThreads : kKsThreads;
     const uint64_t want = (nblk + nt - 1) / nt;
     // lane table: 64 KB per CTA -> at most 3 CTAs per SM, and 2048 threads per SM
     const int lane_ctas = kCipherCtasPerSm < 2048 / kLaneThreads ? kCipherCtasPerSm : 2048 / kLaneThreads;
-    const uint64_t cap = (uint64_t)sms * (lane ? lane_ctas : kKeystreamCtasPerSm);
+    const uint64_t cap = (uint64_t)sms * (lane ? lane_ctas : narrow ? kKsNarrowCtasPerSm : kKeystreamCtasPerSm);
     const unsigned grid = (unsigned)(want < cap ? want : cap);
     if (grid == 0) return 0;
+    cudaStream_t s = (cudaStream_t)stream;
     if (lane) {
-        allow_lut<k_cipher_ctr<true>>();
-        k_cipher_ctr<true><<<grid, kLaneThreads, kAesLutBytes, (cudaStream_t)stream>>>(p);
+        allow_lut<k_cipher_ctr<true, kLaneThreads>>();
+        k_cipher_ctr<true, kLaneThreads><<<grid, kLaneThreads, kAesLutBytes, s>>>(p);
+    } else if (narrow) {
+        k_cipher_ctr<false, kKsNarrowThreads><<<grid, kKsNarrowThreads, 0, s>>>(p);
     } else {
-        k_cipher_ctr<false><<<grid, kCipherThreads, 0, (cudaStream_t)stream>>>(p);
+        k_cipher_ctr<false, kKsThreads><<<grid, kKsThreads, 0, s>>>(p);
     }
     note_launch();
     return (int)cudaGetLastError();

@@ -313,12 +313,13 @@ static DwtParams dwt_params(const se_geom* g, const se_layout& lay) {
 // (counter base p.ctr) written to `out`; the fused kernel that follows is
 // launched with programmatic stream serialization and XORs it in.
 static int launch_keystream(const FusedParams& p, uint8_t* out, uint64_t n, void* stream,
-                            se_report* init_report = nullptr) {
+                            se_report* init_report = nullptr, bool narrow = false) {
     CipherParams cp;
     memset(&cp, 0, sizeof cp);
     cp.in = nullptr;
     cp.out = out;
     cp.n = n;
+    cp.narrow = narrow;
     cp.report = init_report;
     memcpy(cp.ctr, p.ctr, sizeof cp.ctr);
     memcpy(cp.rk, p.rk, sizeof cp.rk);
@@ -357,7 +358,7 @@ int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
         if (!(SE_PROT_FUSED_AES && !mask) &&
-            launch_keystream(p, d_ks ? (uint8_t*)d_ks : p.a, lay.a_bytes, stream))
+            launch_keystream(p, d_ks ? (uint8_t*)d_ks : p.a, lay.a_bytes, stream, nullptr, mask))
             return SE_ECUDA;
         return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
     }

@@ -109,7 +109,7 @@ struct CipherParams {
     uint32_t ctr[4];          // IV + ctr_block_offset
     uint32_t rk[44];
     uint32_t lane_lut;        // keystream (in == nullptr) with the 64 KB lane table
-    uint32_t pad_;
+    uint32_t narrow;          // keystream: one 128-thread CTA per SM (k_cipher.cu)
     se_report* report;        // nullable: initialised to {-1, 0} by this kernel (the fused recover
                               // kernel that follows updates it only after griddepcontrol.wait)
 };
