@@ -103,14 +103,21 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
     __shared__ uint32_t s_job;
     using R = Rec<L>;
     const uint32_t x = blockIdx.x;
-    if (threadIdx.x == 0) {
-        uint32_t lo = 0, hi = bp.n_jobs - 1;          // largest j with cta_begin <= x
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) / 2;
-            if (bp.jobs[mid].cta_begin <= x) lo = mid;
-            else hi = mid - 1;
+    if (threadIdx.x < 32) {
+        // largest j with cta_begin <= x: 32-ary search by warp 0 (3 dependent
+        // loads for 10,000 jobs instead of 14 for a binary search)
+        const uint32_t lane = threadIdx.x;
+        uint32_t lo = 0, n = bp.n_jobs;               // answer in [lo, lo + n)
+        while (n > 1) {
+            const uint32_t step = (n + 31) / 32;
+            const uint32_t idx = lo + lane * step;
+            const bool le = lane * step < n && bp.jobs[idx].cta_begin <= x;
+            const uint32_t m = __ballot_sync(0xffffffffu, le);   // lanes 0..k set (sorted)
+            const uint32_t k = 31 - __clz(m);                    // lane 0 always set (cta_begin[lo] <= x)
+            lo += k * step;
+            n = min(step, n - k * step);
         }
-        s_job = lo;
+        if (lane == 0) s_job = lo;
     }
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(&bp.base);
