@@ -51,9 +51,21 @@ __device__ __forceinline__ float px(uint32_t w, int k) {
     return __int_as_float(__byte_perm(w, 0x4B000000u, 0x7540u | k)) - 8388736.0f;
 }
 
-// rint(clamp(v, 0, 255)) in the low byte of the result
+// rint(clamp(v, 0, 255)) in the low byte of the result (D3: round half to
+// even).  SE_DCT_F2I=1: one saturating conversion (cvt.rni.sat.u8.f32; the
+// clamp and the rounding commute for these bounds) instead of two FMNMX on the
+// ALU pipe - the level-2 kernels are ALU-bound by SHA-512.
+#ifndef SE_DCT_F2I
+#define SE_DCT_F2I 1
+#endif
 __device__ __forceinline__ uint32_t rnd_u8(float v) {
+#if SE_DCT_F2I
+    uint32_t r;
+    asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return r;
+#else
     return __float_as_uint(fminf(fmaxf(v, 0.0f), 255.0f) + 12582912.0f);
+#endif
 }
 
 __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
