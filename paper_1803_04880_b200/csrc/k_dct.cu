@@ -46,9 +46,17 @@ __device__ __forceinline__ constexpr float d2(int x) {
 }
 
 // byte `k` of word w, minus 128, as an exact float: PRMT the byte under the
-// exponent of 2^23, subtract 2^23 + 128.
+// exponent of 2^23, subtract 2^23 + 128 (ALU + FMA pipe) ...
 __device__ __forceinline__ float px(uint32_t w, int k) {
     return __int_as_float(__byte_perm(w, 0x4B000000u, 0x7540u | k)) - 8388736.0f;
+}
+// ... or I2F.U8 with a byte selector (conversion pipe, no ALU instruction):
+// faster in the DCT 8x8 transform (fwd 32.9 -> 31.0 us at 4800^2), slower in
+// the SE kernels (level 2: 119.3 -> 118.2 GB/s), so used there only.
+__device__ __forceinline__ float px_cvt(uint32_t w, int k) {
+    float f;
+    asm("cvt.rn.f32.u8 %0, %1;" : "=f"(f) : "h"((unsigned short)(unsigned char)(w >> (8 * k))));
+    return f - 128.0f;
 }
 
 // rint(clamp(v, 0, 255)) in the low byte of the result (D3: round half to
@@ -452,7 +460,7 @@ __device__ __forceinline__ void dct8_layer(const DctParams& p, const uint32_t (&
     for (int x = 0; x < 8; ++x) {                                       // rows
         float f[8];
 #pragma unroll
-        for (int y = 0; y < 8; ++y) f[y] = px(pw[2 * x + (y >> 2)], y & 3);
+        for (int y = 0; y < 8; ++y) f[y] = px_cvt(pw[2 * x + (y >> 2)], y & 3);
         dct8_1d(f, T[x]);
     }
 #pragma unroll
