@@ -14,6 +14,30 @@ namespace se {
 
 // Load the 8x8 block (br, bc) as raw byte values; zero fill past n (C18).
 // Centering (C8) is applied to LL_L only, after the transform (see lift_fwd).
+// The 4 bytes of w as ints.  SE_UNPACK 0: shifts and masks (ALU pipe);
+// 1: byte conversions with selectors (I2F.U8 + F2I, conversion pipe) to free
+// ALU slots in the SHA-bound masked kernels - measured slower (C2 masked
+// protect 182.7 vs 185.7 GB/s, plain 591 vs 638), so 0.
+#ifndef SE_UNPACK
+#define SE_UNPACK 0
+#endif
+__device__ __forceinline__ void unpack4(uint32_t w, int& b0, int& b1, int& b2, int& b3) {
+#if SE_UNPACK == 1
+    int* out[4] = {&b0, &b1, &b2, &b3};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float f;
+        asm("cvt.rn.f32.u8 %0, %1;" : "=f"(f) : "h"((unsigned short)(unsigned char)(w >> (8 * j))));
+        *out[j] = __float2int_rz(f);
+    }
+#else
+    b0 = (int)(w & 0xffu);
+    b1 = (int)((w >> 8) & 0xffu);
+    b2 = (int)((w >> 16) & 0xffu);
+    b3 = (int)(w >> 24);
+#endif
+}
+
 __device__ __forceinline__ void load_block(const uint8_t* __restrict__ in, uint64_t n, uint32_t W,
                                            uint64_t br, uint64_t bc, int (&v)[8][8]) {
     const uint64_t row0 = 8 * br * (uint64_t)W + 8 * bc;
@@ -21,11 +45,8 @@ __device__ __forceinline__ void load_block(const uint8_t* __restrict__ in, uint6
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint2 q = __ldg(reinterpret_cast<const uint2*>(in + row0 + (uint64_t)i * W));
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                v[i][j] = (int)((q.x >> (8 * j)) & 0xffu);
-                v[i][4 + j] = (int)((q.y >> (8 * j)) & 0xffu);
-            }
+            unpack4(q.x, v[i][0], v[i][1], v[i][2], v[i][3]);
+            unpack4(q.y, v[i][4], v[i][5], v[i][6], v[i][7]);
         }
     } else {
 #pragma unroll
