@@ -28,8 +28,10 @@ static uint64_t gcd64(uint64_t a, uint64_t b) {
 }
 
 // smallest block count g: g*a_bits % 128 == 0 and g*{b,c}_bits % 8 == 0
-static uint64_t chunk_block_align(const se_layout& lay) {
+// (and a multiple of min_blocks)
+static uint64_t chunk_block_align(const se_layout& lay, uint64_t min_blocks = 1) {
     uint64_t g = 128 / gcd64(128, lay.a_bits);
+    g = g / gcd64(g, min_blocks) * min_blocks;
     for (uint64_t bits : {(uint64_t)lay.b_bits, (uint64_t)lay.c_bits}) {
         if (!bits) continue;
         const uint64_t h = 8 / gcd64(8, bits);
@@ -59,9 +61,10 @@ static uint64_t auto_chunk(uint64_t n) {
     return std::min<uint64_t>(16ull << 20, std::max<uint64_t>(4ull << 20, n / 4));
 }
 
-static std::vector<Chunk> make_chunks(const se_geom* g, const se_layout& lay, uint64_t chunk_bytes) {
+static std::vector<Chunk> make_chunks(const se_geom* g, const se_layout& lay, uint64_t chunk_bytes,
+                                      uint64_t min_blocks = 1) {
     const uint64_t bpr = g->width / 8, block_rows = lay.rows / 8;
-    const uint64_t ga = chunk_block_align(lay);
+    const uint64_t ga = chunk_block_align(lay, min_blocks);
     const uint64_t unit = ga / gcd64(ga, bpr);                 // block-rows per alignment unit
     const uint64_t row_bytes = 8ull * g->width;
     uint64_t rows_per = std::max<uint64_t>(1, chunk_bytes / row_bytes);
@@ -293,6 +296,25 @@ static int mapped_ptr(const void* h, void** d) {
     return SE_OK;
 }
 
+// Hybrid staging (BLOCK8, page-locked host buffers): inputs go H2D by copy
+// engine, the fused kernel writes its outputs straight into the host buffers
+// over PCIe, so a chunk is one H2D copy and two kernels and the device-to-
+// host direction needs no copy-engine pass after the kernel.  Chunks are
+// whole 128-block CTA groups so every slice stays 16-byte aligned.
+// SE_HOST_HYBRID bit 0: protect (fragments leave as the CTAs' 128-bit slice
+// stores: C2 protect_host 510 -> 475 us, 256 MiB 7.69 -> 7.46 ms); bit 1:
+// recover (its 8-byte row stores over PCIe measured slower, 511 -> 541 us
+// and 7.44 -> 8.63 ms), so the default is 1.
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static bool hybrid_enabled(int op) {
+    static const int mask = [] {
+        const char* e = getenv("SE_HOST_HYBRID");
+        return e ? atoi(e) : 1;
+    }();
+    return (mask >> op) & 1;
+}
+
 }  // namespace se
 
 using namespace se;
@@ -328,9 +350,16 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
     }
     if (chunk_bytes == 0) chunk_bytes = auto_chunk(g->n_bytes);
     if (n_streams == 0) n_streams = 3;
+    // hybrid: fragments written by the kernels into the (mapped) host buffers
+    void* dmap[3] = {nullptr, nullptr, nullptr};
+    bool hybrid = hybrid_enabled(0) && g->mode == SE_MODE_BLOCK8 && pinned(h_a) && pinned(h_b) && pinned(h_c) &&
+                  aligned16(h_a) && aligned16(h_c) && (!h_b || aligned16(h_b)) && pinned(h_in);
+    if (hybrid && (mapped_ptr(h_a, &dmap[0]) || mapped_ptr(h_b, &dmap[1]) || mapped_ptr(h_c, &dmap[2])))
+        hybrid = false;
     // FULL mode transforms the whole matrix: one chunk
     const std::vector<Chunk> chunks = g->mode == SE_MODE_FULL
-        ? std::vector<Chunk>{Chunk{0, g->n_bytes, 0, lay.n_blocks}} : make_chunks(g, lay, chunk_bytes);
+        ? std::vector<Chunk>{Chunk{0, g->n_bytes, 0, lay.n_blocks}}
+        : make_chunks(g, lay, chunk_bytes, hybrid ? kBlocksPerCta : 1);
     int dev = 0;
     cudaGetDevice(&dev);
     HostCtx& ctx = host_ctx(dev);
@@ -348,14 +377,33 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
         cgs[k].n_bytes = c.byte1 - c.byte0;
         cgs[k].block_offset = g->block_offset + c.blk0;
         fragment_layout(&cgs[k], &cls[k]);
-        const uint64_t sizes[4] = {cgs[k].n_bytes, cls[k].a_bytes, cls[k].b_bytes, cls[k].c_bytes};
-        for (int i = 0; i < 4; ++i) {
+        // staged: input + three fragment slices; hybrid: input + keystream scratch
+        const uint64_t sizes[5] = {cgs[k].n_bytes, hybrid ? 0 : cls[k].a_bytes, hybrid ? 0 : cls[k].b_bytes,
+                                   hybrid ? 0 : cls[k].c_bytes, hybrid ? cls[k].a_bytes : 0};
+        for (int i = 0; i < 5; ++i) {
+            if (!sizes[i] && i) continue;
             if (sizes[i] + 16 > sl.cap[i]) cudaStreamSynchronize(ctx.streams[k % n_streams]);
             if (grow(sl.buf[i], sl.cap[i], sizes[i] + 16, ctx)) return SE_ECUDA;
         }
     }
     // pass 2: H2D -> keystream + fused kernel -> D2H per chunk, chunk k on stream k mod S
     auto issue = [&]() -> int {
+        if (hybrid) {
+            for (size_t k = 0; k < chunks.size(); ++k) {
+                const Chunk& c = chunks[k];
+                cudaStream_t s = ctx.streams[k % n_streams];
+                Slot& sl = ctx.slots[k % n_streams];
+                if (cudaMemcpyAsync(sl.buf[0], (const uint8_t*)h_in + c.byte0, cgs[k].n_bytes,
+                                    cudaMemcpyHostToDevice, s) != cudaSuccess)
+                    return SE_ECUDA;
+                uint8_t* d[3];
+                for (int i = 0; i < 3; ++i) d[i] = dmap[i] ? (uint8_t*)dmap[i] + c.blk0 * bits[i] / 8 : nullptr;
+                int st = protect_impl(&cgs[k], key, iv, sl.buf[0], d[0], cls[k].b_bytes ? d[1] : nullptr, d[2],
+                                      sl.buf[4], s);
+                if (st) return st;
+            }
+            return SE_OK;
+        }
         for (size_t k = 0; k < chunks.size(); ++k) {
             const Chunk& c = chunks[k];
             cudaStream_t s = ctx.streams[k % n_streams];
@@ -425,8 +473,14 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
     }
     if (chunk_bytes == 0) chunk_bytes = auto_chunk(g->n_bytes);
     if (n_streams == 0) n_streams = 3;
+    // hybrid: the recovered bytes written by the kernels into the (mapped) host buffer
+    void* dout = nullptr;
+    bool hybrid = hybrid_enabled(1) && g->mode == SE_MODE_BLOCK8 && pinned(h_out) && aligned16(h_out) &&
+                  pinned(h_a) && pinned(h_b) && pinned(h_c);
+    if (hybrid && mapped_ptr(h_out, &dout)) hybrid = false;
     const std::vector<Chunk> chunks = g->mode == SE_MODE_FULL
-        ? std::vector<Chunk>{Chunk{0, g->n_bytes, 0, lay.n_blocks}} : make_chunks(g, lay, chunk_bytes);
+        ? std::vector<Chunk>{Chunk{0, g->n_bytes, 0, lay.n_blocks}}
+        : make_chunks(g, lay, chunk_bytes, hybrid ? kBlocksPerCta : 1);
     int dev = 0;
     cudaGetDevice(&dev);
     HostCtx& ctx = host_ctx(dev);
@@ -477,11 +531,12 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
                     return SE_ECUDA;
             // report_ready = false: the chunk's report is initialised by its keystream kernel
             // (or memsets on the unmasked path) - no host-to-device copy per chunk
+            uint8_t* dst = hybrid ? (uint8_t*)dout + c.byte0 : (uint8_t*)sl.buf[0];
             int st = recover_impl(&cgs[k], key, iv, sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr, sl.buf[3],
-                                  sl.buf[0], ctx.reps + k, sl.buf[4], false, s);
+                                  dst, ctx.reps + k, sl.buf[4], false, s);
             if (st) return st;
-            if (cudaMemcpyAsync((uint8_t*)h_out + c.byte0, sl.buf[0], sizes[0], cudaMemcpyDeviceToHost, s) !=
-                    cudaSuccess ||
+            if ((!hybrid && cudaMemcpyAsync((uint8_t*)h_out + c.byte0, sl.buf[0], sizes[0], cudaMemcpyDeviceToHost,
+                                            s) != cudaSuccess) ||
                 cudaMemcpyAsync(&reps[k], ctx.reps + k, sizeof(se_report), cudaMemcpyDeviceToHost, s) != cudaSuccess)
                 return SE_ECUDA;
         }
