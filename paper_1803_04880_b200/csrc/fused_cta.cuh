@@ -415,6 +415,9 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
 // The keystream of the whole A stream sits in p.ks (k_cipher_ctr, launched
 // before with programmatic stream serialization); it is waited for and
 // applied after the SHA-512 unmask of C, which does not need A.
+#ifndef SE_REC_STAGE
+#define SE_REC_STAGE 0
+#endif
 template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta, bool SPEC = true>
 __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
@@ -472,6 +475,19 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
     }
     __syncthreads();                                                         // plain A ready
 
+    // SE_REC_STAGE: the CTA's bytes (8 rows x 8*BPC) go through shared memory
+    // and leave as 16-byte stores, one contiguous run per row, when the CTA's
+    // blocks lie in one block row, wholly inside n, on 16-byte aligned rows.
+    // Measured slower (C2 masked recover 183.5 vs 188.3 GB/s, plain 496 vs
+    // 530; host-mapped output still slower than staged copies), so off.
+#if SE_REC_STAGE
+    __shared__ __align__(16) uint32_t so[MODE == 0 ? 16 * BPC : 4];
+    const uint64_t sblk0 = cta * BPC, sbr0 = sblk0 / p.bpr, sbc0 = sblk0 - sbr0 * p.bpr;
+    const bool staged = MODE == 0 && sbc0 + BPC <= p.bpr && (p.width % 16) == 0 && (sbc0 % 2) == 0 &&
+                        8 * sbr0 * (uint64_t)p.width + 8 * sbc0 + 7ull * p.width + 8 * BPC <= p.n_bytes;
+#else
+    constexpr bool staged = false;
+#endif
     bool bad = false;
     if (valid) {
         smem_get_record<R::AW, R::ABITS>(sa, SA_W, (uint32_t)tid * R::ABITS, A);
@@ -495,11 +511,32 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
 #pragma unroll
                 for (int j = 0; j < 8; ++j) orv |= v[i][j];
             bad = (orv & ~0xff) != 0;      // any sample outside [0, 255]
+#if SE_REC_STAGE
+            if (staged) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint2 q;
+                    q.x = __byte_perm(__byte_perm(v[i][0], v[i][1], 0x0040), __byte_perm(v[i][2], v[i][3], 0x0040), 0x5410);
+                    q.y = __byte_perm(__byte_perm(v[i][4], v[i][5], 0x0040), __byte_perm(v[i][6], v[i][7], 0x0040), 0x5410);
+                    *reinterpret_cast<uint2*>(so + (i * 8 * BPC + 8 * tid) / 4) = q;
+                }
+            } else
+#endif
             store_block(p.out, p.n_bytes, p.width, br, bc, v);
         } else {
             footprint_full<L, true>(p, br, bc, v);
         }
     }
+#if SE_REC_STAGE
+    if (staged) {
+        __syncthreads();
+        for (int idx = tid; idx < 4 * BPC; idx += BPC) {
+            const int row = idx / (BPC / 2), c16 = idx % (BPC / 2);
+            uint8_t* dst = p.out + (8 * sbr0 + row) * (uint64_t)p.width + 8 * sbc0 + 16 * c16;
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(so + (row * 8 * BPC + 16 * c16) / 4);
+        }
+    }
+#endif
     if (MODE == 0 && p.report != nullptr) {
         if (bad) {
             atomicMin(&s_first, (unsigned long long)blk);
