@@ -385,6 +385,9 @@ def run_se(args):
                 "peak_gbs": peaks.get("hbm_gbs"), "frac": round(2 * hbm_bytes / (ms_step / 1e3) / 1e9 /
                                                                  peaks.get("hbm_gbs", 6551.7), 4)},
         "kernels_ms": {"protect": round(mp, 5), "recover": round(mr, 5)},
+        "step_ms_stats": {"mean": round(ms_step, 5),                       # median and best
+                          "median": round(statistics.median(p + r for p, r in zip(t_prot, t_rec)), 5),
+                          "best": round(min(p + r for p, r in zip(t_prot, t_rec)), 5), "rank": "0 (own steps)"},
         "protect_gbs": round(n / (mp / 1e3) / 1e9, 3),
         "recover_gbs": round(n / (mr / 1e3) / 1e9, 3),
         "comparator_aes128_ctr_gbs": None if aes_gbs is None else round(aes_gbs, 2),
