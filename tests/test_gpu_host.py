@@ -123,3 +123,26 @@ def test_host_mapped_needs_pinned(dev):
     x = torch.from_numpy(synth.random_bytes(4096, 1))              # pageable
     with pytest.raises(se.SEError):
         se.fragment_protect_host(x, 64, 2, KEY, IV, flags=se.FLAG_HOST_MAPPED)
+
+
+@pytest.mark.parametrize("offset", [0, 4])
+@pytest.mark.parametrize("W", [1032, 1024])
+def test_host_hybrid_staging(dev, orc, W, offset):
+    """Protect's hybrid staging (the fused kernel writes the fragments into the
+    page-locked host buffers) on chunks of whole 128-block groups — W = 1032
+    has 129 blocks per block row, so chunks span 128 block rows — and, with
+    the output views 4 bytes into their buffers (not 16-byte aligned), the
+    staged fallback: both byte-identical to the oracle."""
+    n, L = W * 8 * 300 + 77, 2
+    x = synth.random_bytes(n, W + offset)
+    lay = se.fragment_layout(n, W, L)
+    outs = []
+    for key in ("a_bytes", "b_bytes", "c_bytes"):
+        buf = torch.empty(lay[key] + 16, dtype=torch.uint8).pin_memory()
+        outs.append(buf[offset:offset + lay[key]])
+    a, b, c = se.fragment_protect_host(host(x), W, L, KEY, IV, out=tuple(outs), chunk_bytes=256 * 1024,
+                                       n_streams=3)
+    oa, ob, oc = orc.protect(x, W, L, KEY, IV)
+    assert np.array_equal(a.numpy(), oa) and np.array_equal(b.numpy(), ob) and np.array_equal(c.numpy(), oc)
+    back, rep = se.fragment_recover_host(a, b, c, n, W, L, KEY, IV, chunk_bytes=256 * 1024, n_streams=3)
+    assert np.array_equal(back.numpy(), x) and rep == (-1, 0)
