@@ -304,7 +304,8 @@ static int mapped_ptr(const void* h, void** d) {
 // SE_HOST_HYBRID bit 0: protect (fragments leave as the CTAs' 128-bit slice
 // stores: C2 protect_host 510 -> 475 us, 256 MiB 7.69 -> 7.46 ms); bit 1:
 // recover (its 8-byte row stores over PCIe measured slower, 511 -> 541 us
-// and 7.44 -> 8.63 ms), so the default is 1.
+// and 7.44 -> 8.63 ms); bit 2: recover reads its fragment slices from the host
+// buffers (zero-copy input; C2 e2e 12.9 -> 12.1 GB/s, slower).  Default 1.
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 static bool hybrid_enabled(int op) {
@@ -478,9 +479,14 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
     bool hybrid = hybrid_enabled(1) && g->mode == SE_MODE_BLOCK8 && pinned(h_out) && aligned16(h_out) &&
                   pinned(h_a) && pinned(h_b) && pinned(h_c);
     if (hybrid && mapped_ptr(h_out, &dout)) hybrid = false;
+    // zero-copy input: the fused kernels read the fragment slices from the (mapped) host buffers
+    void* din[3] = {nullptr, nullptr, nullptr};
+    bool zin = hybrid_enabled(2) && g->mode == SE_MODE_BLOCK8 && pinned(h_a) && pinned(h_b) && pinned(h_c) &&
+               aligned16(h_a) && aligned16(h_c) && (!h_b || aligned16(h_b));
+    if (zin && (mapped_ptr(h_a, &din[0]) || mapped_ptr(h_b, &din[1]) || mapped_ptr(h_c, &din[2]))) zin = false;
     const std::vector<Chunk> chunks = g->mode == SE_MODE_FULL
         ? std::vector<Chunk>{Chunk{0, g->n_bytes, 0, lay.n_blocks}}
-        : make_chunks(g, lay, chunk_bytes, hybrid ? kBlocksPerCta : 1);
+        : make_chunks(g, lay, chunk_bytes, (hybrid || zin) ? kBlocksPerCta : 1);
     int dev = 0;
     cudaGetDevice(&dev);
     HostCtx& ctx = host_ctx(dev);
@@ -525,14 +531,19 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
             Slot& sl = ctx.slots[k % n_streams];
             const se_layout& cl = cls[k];
             const uint64_t sizes[4] = {cgs[k].n_bytes, cl.a_bytes, cl.b_bytes, cl.c_bytes};
-            for (int i = 0; i < 3; ++i)
-                if (sizes[i + 1] && cudaMemcpyAsync(sl.buf[i + 1], hin[i] + c.blk0 * bits[i] / 8, sizes[i + 1],
-                                                    cudaMemcpyHostToDevice, s) != cudaSuccess)
+            const void* src[3] = {sl.buf[1], sl.buf[2], sl.buf[3]};
+            for (int i = 0; i < 3; ++i) {
+                if (zin) {
+                    src[i] = din[i] ? (const uint8_t*)din[i] + c.blk0 * bits[i] / 8 : nullptr;
+                } else if (sizes[i + 1] && cudaMemcpyAsync(sl.buf[i + 1], hin[i] + c.blk0 * bits[i] / 8,
+                                                           sizes[i + 1], cudaMemcpyHostToDevice, s) != cudaSuccess) {
                     return SE_ECUDA;
+                }
+            }
             // report_ready = false: the chunk's report is initialised by its keystream kernel
             // (or memsets on the unmasked path) - no host-to-device copy per chunk
             uint8_t* dst = hybrid ? (uint8_t*)dout + c.byte0 : (uint8_t*)sl.buf[0];
-            int st = recover_impl(&cgs[k], key, iv, sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr, sl.buf[3],
+            int st = recover_impl(&cgs[k], key, iv, src[0], cl.b_bytes ? src[1] : nullptr, src[2],
                                   dst, ctx.reps + k, sl.buf[4], false, s);
             if (st) return st;
             if ((!hybrid && cudaMemcpyAsync((uint8_t*)h_out + c.byte0, sl.buf[0], sizes[0], cudaMemcpyDeviceToHost,
