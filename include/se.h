@@ -130,7 +130,7 @@ typedef struct {
     uint32_t reserved0;
     uint8_t iv[16];
     uint64_t cta_begin;       /* set by fragment_batch_plan                   */
-    uint32_t derived[36];     /* set by fragment_batch_plan (library-private) */
+    uint32_t derived[132];    /* set by fragment_batch_plan (library-private) */
 } se_job;
 
 /* Returns the total number of CTAs of the launch (>= 0), or a negative

@@ -88,7 +88,7 @@ class Job(C.Structure):
     _fields_ = [("in_", C.c_void_p), ("out", C.c_void_p), ("a", C.c_void_p), ("b", C.c_void_p),
                 ("c", C.c_void_p), ("n_bytes", C.c_uint64), ("block_offset", C.c_uint64),
                 ("width", C.c_uint32), ("reserved0", C.c_uint32), ("iv", C.c_uint8 * 16),
-                ("cta_begin", C.c_uint64), ("derived", C.c_uint32 * 36)]
+                ("cta_begin", C.c_uint64), ("derived", C.c_uint32 * 132)]
 
 
 SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_batch_plan",

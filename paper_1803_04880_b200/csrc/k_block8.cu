@@ -30,6 +30,11 @@
 #ifndef SE_MIN_CTAS_BATCH
 #define SE_MIN_CTAS_BATCH 5
 #endif
+// batch kernels with the launch-constant SHA-512 schedule: its constants
+// depend on K || IV, so fragment_batch_plan derives them per file
+#ifndef SE_BATCH_SPEC
+#define SE_BATCH_SPEC 1
+#endif
 
 namespace se {
 
@@ -153,10 +158,15 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
     } else if (t == 60) {
         sp.ks = bp.ks ? bp.ks + job.cta_begin * 16ull * R::ABITS : nullptr;
     }
+    if (SE_BATCH_SPEC && t >= 64) {                  // this file's C-mask schedule constants
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(&dv.s512);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&sp.s512);
+        for (uint32_t i = t - 64; i < sizeof(SchedConst512) / 4; i += kBlocksPerCta - 64) dst[i] = src[i];
+    }
     __syncthreads();
     const uint64_t cta = x - job.cta_begin;
-    if (RECOVER) recover_cta<L, MASK, 0, kBlocksPerCta, false>(sp, cta);      // per-file IV: generic schedule
-    else protect_cta<L, MASK, 0, kBlocksPerCta, false>(sp, cta);
+    if (RECOVER) recover_cta<L, MASK, 0, kBlocksPerCta, SE_BATCH_SPEC != 0>(sp, cta);
+    else protect_cta<L, MASK, 0, kBlocksPerCta, SE_BATCH_SPEC != 0>(sp, cta);
 }
 
 __global__ void k_report_init(se_report* r, uint32_t n) {

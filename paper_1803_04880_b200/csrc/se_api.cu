@@ -653,6 +653,7 @@ int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels, cons
         memcpy(d.kiv, p.kiv, sizeof d.kiv);
         memcpy(d.mid256, p.mid256, sizeof d.mid256);
         memcpy(d.mid512, p.mid512, sizeof d.mid512);
+        d.s512 = p.s512;
         memset(job.derived, 0, sizeof job.derived);
         memcpy(job.derived, &d, sizeof d);
     }

@@ -89,6 +89,7 @@ struct JobDerived {
     uint32_t kiv[8];          // K || IV words
     uint32_t mid256[8];       // SHA-256 midstate over K||IV
     uint64_t mid512[8];       // SHA-512 midstate over K||IV
+    SchedConst512 s512;       // C-mask schedule constants of this file's K||IV (sha2_spec.cuh)
 };
 static_assert(sizeof(JobDerived) <= sizeof(((se_job*)0)->derived), "se_job.derived too small");
 

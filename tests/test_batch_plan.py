@@ -30,7 +30,7 @@ def make_jobs(sizes, widths, ivs, offsets=None):
 
 
 def test_job_struct_layout():
-    assert C.sizeof(se.Job) == 232
+    assert C.sizeof(se.Job) == 616
     assert se.Job.cta_begin.offset == 80 and se.Job.derived.offset == 88
 
 
