@@ -117,9 +117,10 @@ int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[1
  * the paper's chunks D_i are independent).  The caller fills one
  * se_job per file in HOST memory (pointers are device pointers; IV per file),
  * calls fragment_batch_plan (host, pure: validates every job, assigns each its
- * first CTA and derives the per-file counter base and SHA midstates into
- * `derived`), copies the array to device memory, then launches.  All jobs of
- * a batch share the key, levels and flags.  Mode is BLOCK8. */
+ * first CTA and derives the per-file counter base, SHA midstates and SHA-512
+ * schedule constants over K || IV into `derived`), copies the array (16-byte
+ * aligned) to device memory, then launches.  All jobs of a batch share the
+ * key, levels and flags.  Mode is BLOCK8. */
 typedef struct {
     const uint8_t* in;        /* protect: input bytes (device)                */
     uint8_t* out;             /* recover: output bytes (device)               */
