@@ -154,3 +154,25 @@ def test_full_stripe_corruption_report(dev, orc):
     with pytest.raises(se.SEError):
         se.fragment_recover_stripe(*ins, n, W, L, KEY, IV, st["row_begin"], st["row_end"],
                                    st["row_begin"], st["row_end"] - st["row_begin"])
+
+
+def _fuzz_cases(k=12, seed=2026):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(k):
+        W = 8 * int(rng.integers(1, 200))
+        rows = int(rng.integers(1, 90))
+        n = max(1, W * rows - int(rng.integers(0, W)))
+        out.append((n, W, int(rng.integers(1, 4))))
+    return out
+
+
+@pytest.mark.parametrize("n,W,L", _fuzz_cases())
+def test_full_streaming_fuzz(dev, orc, n, W, L):
+    """Seeded random shapes for the streaming FULL transform (column groups of
+    30 / 28 chunks, row segments with halos, ragged tails): coefficients
+    bit-exact and the round trip exact."""
+    x = synth.random_bytes(n, n ^ W)
+    coef = se.dwt_fwd(to_dev(x, dev), W, L, mode=FULL)
+    assert np.array_equal(coef.cpu().numpy().astype(np.int32), orc.dwt_fwd(x, W, L, orc.MODE_FULL))
+    assert np.array_equal(se.dwt_inv(coef, n, W, L, mode=FULL).cpu().numpy(), x)
