@@ -8,6 +8,7 @@ readings and citations; this file only marshals numpy arrays through ctypes.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import subprocess
@@ -51,39 +52,57 @@ def lib():
     global _lib
     if _lib is None:
         build()
-        L = C.CDLL(LIB_PATH)
-        u64, u32 = C.c_uint64, C.c_uint32
-        L.oracle_layout.argtypes = [u64, u32, u32, u32, _u64p]
-        L.oracle_lift_fwd_1d.argtypes = [_i32p, _i32p, C.c_int]
-        L.oracle_lift_inv_1d.argtypes = [_i32p, _i32p, C.c_int]
-        L.oracle_dwt_fwd.argtypes = [_u8p, u64, u32, u32, u32, _i32p]
-        L.oracle_dwt_inv.argtypes = [_i32p, u64, u32, u32, u32, _u8p]
-        L.oracle_dwt_inv.restype = C.c_int64
-        L.oracle_aes128_sbox.argtypes = [_u8p]
-        L.oracle_aes128_encrypt_block.argtypes = [_u8p, _u8p, _u8p]
-        L.oracle_aes128_ctr.argtypes = [_u8p, _u8p, u64, _u8p, _u8p, u64]
-        L.oracle_sha256.argtypes = [_u8p, u64, _u8p]
-        L.oracle_sha512.argtypes = [_u8p, u64, _u8p]
-        L.oracle_protect_range.argtypes = [u64, u32, u32, u32, u32, u64, _u8p, _u8p,
-                                           _u8p, _u8p, _u8p, _u8p, u64, u64]
-        L.oracle_recover_range.argtypes = [u64, u32, u32, u32, u32, u64, _u8p, _u8p,
-                                           _u8p, _u8p, _u8p, _u8p, _i64p, u64, u64]
-        L.oracle_dwt2_fwd_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
-        L.oracle_dwt2_inv_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
-        L.oracle_stats.argtypes = [_u8p, _u8p, u64, u32, _u64p, _u64p]
-        _f64p = C.POINTER(C.c_double)
-        L.oracle_dct_basis.argtypes = [_f64p]
-        L.oracle_dct8_fwd.argtypes = [_f64p, _f64p]
-        L.oracle_dct8_inv.argtypes = [_f64p, _f64p]
-        L.oracle_dct_layout.argtypes = [u32, u32, u32, _u64p]
-        L.oracle_dct_select.argtypes = [u32, u32, u32, _u8p, _f64p]
-        L.oracle_dct_image_fwd.argtypes = [u32, u32, u32, _u8p, _f64p]
-        L.oracle_dct_image_inv.argtypes = [u32, u32, u32, _f64p, _u8p]
-        L.oracle_dct_protect.argtypes = [u32, u32, u32, u32, u32, u64, _u8p, _u8p, _u8p, _u8p, _u8p, _f64p]
-        L.oracle_dct_recover.argtypes = [u32, u32, u32, u32, u32, u64, _u8p, _u8p, _u8p, _u8p, _u8p, _f64p]
-        L.oracle_record_fields.argtypes = [u32, u32, C.c_int, _i32p, _i32p, _i32p, _i32p, _i32p]
-        _lib = L
+        _lib = _load(LIB_PATH)
     return _lib
+
+
+@contextlib.contextmanager
+def library_override(path: str):
+    """Run this module's functions against another build of the oracle's C
+    sources (test infrastructure: tests/test_oracle_mutations.py builds
+    deliberately mutated copies and checks that the paper pins reject them)."""
+    global _lib
+    saved = lib()
+    _lib = _load(path)
+    try:
+        yield
+    finally:
+        _lib = saved
+
+
+def _load(path: str):
+    L = C.CDLL(path)
+    u64, u32 = C.c_uint64, C.c_uint32
+    L.oracle_layout.argtypes = [u64, u32, u32, u32, _u64p]
+    L.oracle_lift_fwd_1d.argtypes = [_i32p, _i32p, C.c_int]
+    L.oracle_lift_inv_1d.argtypes = [_i32p, _i32p, C.c_int]
+    L.oracle_dwt_fwd.argtypes = [_u8p, u64, u32, u32, u32, _i32p]
+    L.oracle_dwt_inv.argtypes = [_i32p, u64, u32, u32, u32, _u8p]
+    L.oracle_dwt_inv.restype = C.c_int64
+    L.oracle_aes128_sbox.argtypes = [_u8p]
+    L.oracle_aes128_encrypt_block.argtypes = [_u8p, _u8p, _u8p]
+    L.oracle_aes128_ctr.argtypes = [_u8p, _u8p, u64, _u8p, _u8p, u64]
+    L.oracle_sha256.argtypes = [_u8p, u64, _u8p]
+    L.oracle_sha512.argtypes = [_u8p, u64, _u8p]
+    L.oracle_protect_range.argtypes = [u64, u32, u32, u32, u32, u64, _u8p, _u8p,
+                                       _u8p, _u8p, _u8p, _u8p, u64, u64]
+    L.oracle_recover_range.argtypes = [u64, u32, u32, u32, u32, u64, _u8p, _u8p,
+                                       _u8p, _u8p, _u8p, _u8p, _i64p, u64, u64]
+    L.oracle_dwt2_fwd_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
+    L.oracle_dwt2_inv_region.argtypes = [_i32p, C.c_size_t, C.c_int, C.c_int, C.c_int]
+    L.oracle_stats.argtypes = [_u8p, _u8p, u64, u32, _u64p, _u64p]
+    _f64p = C.POINTER(C.c_double)
+    L.oracle_dct_basis.argtypes = [_f64p]
+    L.oracle_dct8_fwd.argtypes = [_f64p, _f64p]
+    L.oracle_dct8_inv.argtypes = [_f64p, _f64p]
+    L.oracle_dct_layout.argtypes = [u32, u32, u32, _u64p]
+    L.oracle_dct_select.argtypes = [u32, u32, u32, _u8p, _f64p]
+    L.oracle_dct_image_fwd.argtypes = [u32, u32, u32, _u8p, _f64p]
+    L.oracle_dct_image_inv.argtypes = [u32, u32, u32, _f64p, _u8p]
+    L.oracle_dct_protect.argtypes = [u32, u32, u32, u32, u32, u64, _u8p, _u8p, _u8p, _u8p, _u8p, _f64p]
+    L.oracle_dct_recover.argtypes = [u32, u32, u32, u32, u32, u64, _u8p, _u8p, _u8p, _u8p, _u8p, _f64p]
+    L.oracle_record_fields.argtypes = [u32, u32, C.c_int, _i32p, _i32p, _i32p, _i32p, _i32p]
+    return L
 
 
 def _p(a: np.ndarray, t):
