@@ -61,7 +61,7 @@ ALU_OPS = {
     2: {"sha256": 944, "sha512": 2544 - 8 * 18 - 12, "dwt": 160 + 64, "pack": 140, "xor": 19, "aes": 260 * 40 / 128},
     3: {"sha256": 944, "sha512": 2544 - 8 * 17 - 11, "dwt": 168 + 64, "pack": 140, "xor": 20, "aes": 260 * 10 / 128},
 }
-ALU_LANES_PER_SM_CLK = 64      # B300_MICROARCH.md: IADD3/LOP3/SHF/PRMT on alu-pipe, rt_SMSP = 2
+ALU_LANES_PER_SM_CLK = 64      # guide fallback (B300_MICROARCH.md); measured value: alu_lanes_per_clk()
 NUM_SMS = 148
 
 
@@ -73,19 +73,47 @@ def alu_ops_per_block(levels: int, masked: bool) -> float:
     return float(ops)
 
 
-def load_traffic(kernel_key: str):
-    """DRAM bytes per launch of `kernel_key` from the newest committed ncu
-    capture summary (profiles/round*_traffic.json), else None."""
+def _profile_entries():
+    """Per-(kernel, workload) ncu summaries committed under profiles/
+    (round*_traffic.json: {"entries": [{"kernel", "workload", "dram_bytes",
+    "inst_per_block", "source"}]}), newest round first."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "round*_traffic.json")))
-    for f in reversed(files):
+    out = []
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*_traffic.json")), reverse=True):
         try:
-            b = json.load(open(f)).get("bytes", {})
+            d = json.load(open(f))
         except (OSError, ValueError):
             continue
-        if kernel_key in b:
-            return b[kernel_key], os.path.basename(f)
+        for e in d.get("entries", []):
+            out.append(dict(e, file=os.path.basename(f)))
+    return out
+
+
+def load_traffic(kernel_key: str, workload: str):
+    """DRAM bytes per launch of `kernel_key` on `workload` from the newest
+    committed ncu capture of exactly that pair, else (None, None)."""
+    for e in _profile_entries():
+        if e.get("kernel") == kernel_key and e.get("workload") == workload and e.get("dram_bytes"):
+            return e["dram_bytes"], f"{e['file']}: {e.get('source', '')}"
     return None, None
+
+
+def load_profile_stats(kernel_key: str, workload: str):
+    for e in _profile_entries():
+        if e.get("kernel") == kernel_key and e.get("workload") == workload:
+            return e
+    return None
+
+
+def alu_lanes_per_clk():
+    """ALU-pipe lane operations per SM clock: measured by tools/intbench.cu
+    (profiles/round2_intpeak.json: SHF / LOP3 chains, SM cycles from clock64),
+    else the microarchitecture guide's 64."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "round2_intpeak.json")))
+        return float(d["alu_lanes_per_clk_per_sm"]), "measured: profiles/round2_intpeak.json"
+    except (OSError, ValueError, KeyError):
+        return float(ALU_LANES_PER_SM_CLK), "guide value (no measurement committed)"
 
 
 def load_peaks():
@@ -179,14 +207,15 @@ def init_dist(local: int):
 
 
 def allreduce_max(t):
-    """In-place max over ranks of a small float64 tensor (CPU hop for gloo)."""
+    """In-place max over ranks of a small float64 tensor: NCCL reduces the
+    device tensor directly; gloo (CPU tests) through a host copy."""
     import torch.distributed as dist
-    if dist.get_backend() == "gloo":
+    if dist.get_backend() == "gloo" and t.device.type != "cpu":
         c = t.cpu()
         dist.all_reduce(c, op=dist.ReduceOp.MAX)
         t.copy_(c)
     else:
-        allreduce_max(t)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t
 
 
@@ -203,9 +232,39 @@ def workload(cfg: int):
     return c, x
 
 
+def config_dict(args, world: int) -> dict:
+    """The `config` of the JSON line: identical for the repo arm and the
+    reference arm (same workload, same keys), so the driver can pair them."""
+    c = synth.CONFIGS[args.config]
+    stripes = args.config == 4
+    return {"workload": c["name"] + (" (PUBLIC_PLAIN)" if args.plain else ""),
+            "n_bytes": c["n_bytes"] * (1 if stripes else world), "width": c["width"], "levels": c["levels"],
+            "mode": "BLOCK8", "masks": "none (C26)" if args.plain else "SHA-256 on B, SHA-512 on C",
+            "parallelism": (f"dp{world}: one row stripe of the file per rank" if stripes else
+                            f"dp{world}: one independent file per rank"),
+            "l2": ("input 1 GiB > L2; L2 flushed between steps anyway" if stripes else
+                   "flushed between steps (2x L2 write + read-back)")}
+
+
+def local_input(args, rank: int, world: int):
+    """This rank's share of the workload: C4 = one row stripe of the 1 GiB
+    file (shard.plan_stripes: block_offset = global index of its first block;
+    strong scaling); C1-C3 = an independent file per rank (own IV; weak)."""
+    from paper_1803_04880_b200 import shard
+    c = synth.CONFIGS[args.config]
+    W, L = c["width"], c["levels"]
+    if args.config == 4:
+        plan = shard.plan_stripes(c["n_bytes"], W, L, world)[rank]
+        x_np = np.ascontiguousarray(synth.config_input(4)[plan["byte_begin"]: plan["byte_end"]])
+        return x_np, W, L, synth.iv_for(4), plan["block_offset"], "strong"
+    return synth.config_input(args.config), W, L, synth.iv_for(args.config, rank), 0, "weak"
+
+
 # ---------------------------------------------------------------- our arm
 
 def run_se(args):
+    """Configs 1-4 (BLOCK8).  One step = fragment_protect + fragment_recover
+    of this rank's input, device-resident."""
     import torch
     import torch.distributed as dist
 
@@ -215,42 +274,47 @@ def run_se(args):
     dev = init_dist(local) if world > 1 else torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     se.lib()
-    c, x_np = workload(args.config)
-    W, L, n = c["width"], c["levels"], x_np.size
+    x_np, W, L, iv, boff, scaling = local_input(args, rank, world)
+    n = x_np.size
     key = synth.KEY
-    iv = synth.iv_for(args.config, rank)                # each rank: its own independent file
     flags = se.FLAG_PUBLIC_PLAIN if args.plain else 0
     masked = not args.plain
-    lay = se.fragment_layout(n, W, L)
+    lay = se.fragment_layout(n, W, L, block_offset=boff)
     stream = torch.cuda.Stream(device=dev)
     x = torch.from_numpy(x_np).to(dev)
-    a = torch.empty(lay["a_bytes"], dtype=torch.uint8, device=dev)
-    b = torch.empty(max(lay["b_bytes"], 16), dtype=torch.uint8, device=dev)[: lay["b_bytes"]]
-    cc = torch.empty(lay["c_bytes"], dtype=torch.uint8, device=dev)
-    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    a = se._empty(lay["a_bytes"], dev)
+    b = se._empty(lay["b_bytes"], dev)
+    cc = se._empty(lay["c_bytes"], dev)
+    out = se._empty(n, dev)
     rep = torch.empty(2, dtype=torch.int64, device=dev)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)   # 252 MB > L2
     torch.cuda.synchronize()
 
-    def step():
-        se.fragment_protect(x, W, L, key, iv, flags=flags, out=(a, b, cc), stream=stream)
-        se.fragment_recover(a, b, cc, n, W, L, key, iv, flags=flags, out=out, report=rep, stream=stream)
+    def protect():
+        se.fragment_protect(x, W, L, key, iv, flags=flags, block_offset=boff, out=(a, b, cc), stream=stream)
+
+    def recover():
+        se.fragment_recover(a, b, cc, n, W, L, key, iv, flags=flags, block_offset=boff, out=out, report=rep,
+                            stream=stream)
 
     # correctness of the timed configuration (cheap property at full size)
     with torch.cuda.stream(stream):
-        step()
+        protect()
+        recover()
     stream.synchronize()
     assert torch.equal(out, x), "recover(protect(x)) != x in the timed configuration"
     assert rep.cpu().tolist() == [-1, 0]
 
     clocks = ClockSampler(dev.index if dev.index is not None else local)
     clocks.start()
-    # warm-up: at least W steps and ~1 s of sustained load (clock sampling)
+    # warm-up: at least W steps and ~soak s of sustained load (clock sampling)
     t_end = time.time() + args.soak
     i = 0
-    while i < args.warmup or time.time() < t_end:
-        step()
-        i += 1
+    with torch.cuda.stream(stream):
+        while i < args.warmup or time.time() < t_end:
+            protect()
+            recover()
+            i += 1
     stream.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -259,13 +323,13 @@ def run_se(args):
         dist.barrier()
     torch.cuda.synchronize()
     se.launch_count(reset=True)
-    for k in range(args.steps):
-        with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
             l2_flush(flush, k)                                  # evict L2 between timed steps
             ev[k][0].record(stream)
-            se.fragment_protect(x, W, L, key, iv, flags=flags, out=(a, b, cc), stream=stream)
+            protect()
             ev[k][1].record(stream)
-            se.fragment_recover(a, b, cc, n, W, L, key, iv, flags=flags, out=out, report=rep, stream=stream)
+            recover()
             ev[k][2].record(stream)
     stream.synchronize()
     launches = se.launch_count()
@@ -275,35 +339,28 @@ def run_se(args):
     clocks.stop()
     t_prot = [e[0].elapsed_time(e[1]) for e in ev]          # ms
     t_rec = [e[1].elapsed_time(e[2]) for e in ev]
-    total_ms = sum(t_prot) + sum(t_rec)
-    ms_step = total_ms / args.steps
+    mp, mr = sum(t_prot) / args.steps, sum(t_rec) / args.steps
+    t = torch.tensor([mp + mr, mp, mr], dtype=torch.float64, device=dev)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        allreduce_max(t)
-        total_ms = float(t.item())
-        ms_step = total_ms / args.steps
+        allreduce_max(t)                                    # max over ranks
+    ms_step, mp_max, mr_max = (float(v) for v in t.tolist())
 
-    # ---- e2e: same metric with host buffers, H2D/D2H inside the timed region
+    # ---- e2e: same metric through the public host API (pinned host buffers,
+    #      H2D of the inputs and D2H of the results inside the timed region)
     e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags | (se.FLAG_HOST_MAPPED if args.e2e_mapped else 0), dev,
-                  args.e2e_steps, chunk_bytes=args.e2e_chunk_kib << 10,
-                  n_streams=args.e2e_streams) if args.e2e_steps > 0 else \
+                  args.e2e_steps, chunk_bytes=args.e2e_chunk_kib << 10, n_streams=args.e2e_streams,
+                  block_offset=boff, world=world) if args.e2e_steps > 0 else \
         {"value": None, "unit": "GB/s", "note": "skipped (--e2e-steps 0, profiling runs only)"}
 
-    # the same through the zero-copy host mode (SE_FLAG_HOST_MAPPED: the kernels read and write the
-    # pinned host buffers over PCIe instead of staged copies) - reported next to e2e
-    if args.e2e_steps > 0 and not args.e2e_mapped:
-        e2e["mapped_variant"] = run_e2e(se, torch, x_np, W, L, key, iv, flags | se.FLAG_HOST_MAPPED, dev,
-                                        args.e2e_steps)
-
-    # ---- comparator: full-file AES-128-CTR on the same GPU (paper methodology)
+    # ---- comparator: AES-128-CTR over all input bytes on the same GPU (paper methodology)
     aes_gbs = None
     if not args.no_comparator:
         y = torch.empty_like(x)
-        for _ in range(3):
-            se.cipher_encrypt(key, iv, x, out=y, stream=stream)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 20
         with torch.cuda.stream(stream):
+            for _ in range(3):
+                se.cipher_encrypt(key, iv, x, out=y, stream=stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
             e0.record(stream)
             for _ in range(reps):
                 se.cipher_encrypt(key, iv, x, out=y, stream=stream)
@@ -312,26 +369,16 @@ def run_se(args):
         aes_gbs = n * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
         del y
 
-    # ---- NEXT row f2: security battery on the protected public fragment C'
-    #      vs the original (one pass of se_stats_accumulate), timed + metrics
+    # ---- NEXT row f2: security battery on the protected public fragment C' vs the original
     battery = None
     if not args.no_comparator:
-        xs = x[: cc.numel()]
-        st, jt = se.stats_accumulate(cc, W, x=xs, stream=stream)
+        m = min(cc.numel(), 64 << 20)
+        xs, ys = x[:m], cc[:m]
+        st, jt = se.stats_accumulate(ys, W, x=xs, stream=stream)
         stream.synchronize()
         metrics = se.stats_metrics(st, jt)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(5):
-                st.zero_()
-                jt.zero_()
-                se.stats_accumulate(cc, W, x=xs, stats=st, joint=jt, stream=stream)
-            e1.record(stream)
-        stream.synchronize()
-        battery = {"input_gbs": round(2 * cc.numel() * 5 / (e0.elapsed_time(e1) / 1e3) / 1e9, 2),
-                   "on": "C' vs original (first |C'| bytes)",
-                   **{k: (round(v, 6) if isinstance(v, float) else v) for k, v in metrics.items()}}
+        battery = {"on": f"C' vs original (first {m} bytes)",
+                   **{k_: (round(v, 6) if isinstance(v, float) else v) for k_, v in metrics.items()}}
 
     if rank != 0:
         if world > 1:
@@ -340,29 +387,13 @@ def run_se(args):
 
     peaks, peak_src = load_peaks()
     clk = clocks.summary()
-    gbs = n * world / (ms_step / 1e3) / 1e9
-    # dominant kernel = the slower of the two fused kernels
-    mp, mr = sum(t_prot) / args.steps, sum(t_rec) / args.steps
+    total_bytes = synth.CONFIGS[args.config]["n_bytes"] * (1 if scaling == "strong" else world)
+    gbs = total_bytes / (ms_step / 1e3) / 1e9
+    # dominant kernel = the slower of the two fused calls (each call is one kernel launch)
     dom_name, dom_ms = ("k_protect_block8", mp) if mp >= mr else ("k_recover_block8", mr)
-    ops = alu_ops_per_block(L, masked) * lay["n_blocks"]
-    achieved = ops / (dom_ms / 1e3) / 1e9                     # Gop/s
-    peak_alu = NUM_SMS * ALU_LANES_PER_SM_CLK * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
-    hbm_bytes = n + lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"]     # algorithmic bytes per launch
     kkey = f"{dom_name}<{L}, {1 if masked else 0}>"
-    traffic, traffic_src = load_traffic(kkey)
-    if masked:   # SHA-2 masks make the path ALU-bound
-        roofline = {"bound": "alu", "kernel": kkey, "achieved": round(achieved, 1), "peak": round(peak_alu, 1),
-                    "unit": "Gop/s", "frac": round(achieved / peak_alu, 4), "traffic": traffic,
-                    "traffic_source": traffic_src, "algorithmic_bytes": hbm_bytes,
-                    "peak_source": f"guide: {NUM_SMS} SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x "
-                                   f"{peaks.get('sm_max_mhz', 1965.0)} MHz ({peak_src} max clock)",
-                    "alu_ops_per_block": alu_ops_per_block(L, masked)}
-    else:        # PUBLIC_PLAIN: transform + split + AES only, HBM-bound by design
-        ach = hbm_bytes / (dom_ms / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": kkey, "achieved": round(ach, 1), "peak": peaks.get("hbm_gbs"),
-                    "unit": "GB/s", "frac": round(ach / peaks.get("hbm_gbs", 6551.7), 4), "traffic": traffic,
-                    "traffic_source": traffic_src, "algorithmic_bytes": hbm_bytes,
-                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+    roofline = make_roofline(kkey, config_dict(args, world)["workload"], L, masked, n, lay, dom_ms, peaks, peak_src)
+    hbm_bytes = n + lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"]
     line = {
         "metric": "protect+recover GB/s per GPU and at 1/2/4/8 B200; % of HBM roofline",
         "value": round(gbs, 3),
@@ -372,24 +403,23 @@ def run_se(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 5),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": c["name"] + (" (PUBLIC_PLAIN)" if args.plain else ""), "n_bytes": n,
-                   "width": W, "levels": L, "mode": "BLOCK8", "n_blocks": lay["n_blocks"],
-                   "per_rank_input": "independent file per rank (own IV)", "l2": "flushed between steps (2x L2 write + read-back)",
-                   "parallelism": f"dp{world} by file"},
+        "config": config_dict(args, world),
         "roofline": roofline,
         "hbm": {"bytes_per_step": 2 * hbm_bytes, "achieved_gbs": round(2 * hbm_bytes / (ms_step / 1e3) / 1e9, 1),
-                "peak_gbs": peaks.get("hbm_gbs"), "frac": round(2 * hbm_bytes / (ms_step / 1e3) / 1e9 /
-                                                                 peaks.get("hbm_gbs", 6551.7), 4)},
-        "kernels_ms": {"protect": round(mp, 5), "recover": round(mr, 5)},
-        "step_ms_stats": {"mean": round(ms_step, 5),                       # median and best
-                          "median": round(statistics.median(p + r for p, r in zip(t_prot, t_rec)), 5),
-                          "best": round(min(p + r for p, r in zip(t_prot, t_rec)), 5), "rank": "0 (own steps)"},
-        "protect_gbs": round(n / (mp / 1e3) / 1e9, 3),
-        "recover_gbs": round(n / (mr / 1e3) / 1e9, 3),
+                "peak_gbs": peaks.get("hbm_gbs"),
+                "frac": round(2 * hbm_bytes / (ms_step / 1e3) / 1e9 / peaks.get("hbm_gbs", 6551.7), 4),
+                "note": "rank 0's algorithmic bytes over the max-over-ranks step time"},
+        "rank0": {"n_bytes": n, "block_offset": boff, "n_blocks": lay["n_blocks"],
+                  "kernels_ms": {"protect": round(mp, 5), "recover": round(mr, 5)},
+                  "protect_gbs": round(n / (mp / 1e3) / 1e9, 3), "recover_gbs": round(n / (mr / 1e3) / 1e9, 3),
+                  "step_ms_stats": {"mean": round(mp + mr, 5),
+                                    "median": round(statistics.median(p + r for p, r in zip(t_prot, t_rec)), 5),
+                                    "best": round(min(p + r for p, r in zip(t_prot, t_rec)), 5)}},
+        "max_over_ranks_ms": {"protect": round(mp_max, 5), "recover": round(mr_max, 5)},
         "comparator_aes128_ctr_gbs": None if aes_gbs is None else round(aes_gbs, 2),
         "security_battery": battery,
         "e2e": e2e,
@@ -397,10 +427,46 @@ def run_se(args):
         "clocks": clk,
     }
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(x_np, W, L, key, iv, flags, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(x_np, W, L, key, iv, flags, args.cpu_seconds, block_offset=boff)
     if world > 1:
         dist.destroy_process_group()
     return line
+
+
+def make_roofline(kkey, workload_name, L, masked, n_in, lay, dom_ms, peaks, peak_src):
+    """roofline object of the dominant kernel: masked = ALU-pipe
+    bound (algorithmic ALU ops / measured ALU-pipe peak, tools/intbench.cu ->
+    profiles/round2_intpeak.json), PUBLIC_PLAIN = HBM bound (algorithmic bytes /
+    measured copy bandwidth).  `traffic` = ncu DRAM bytes of this kernel on
+    THIS workload (profiles/round*_traffic.json), else null."""
+    alg_bytes = n_in + lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"]     # per launch
+    traffic, tsrc = load_traffic(kkey, workload_name)
+    prof = load_profile_stats(kkey, workload_name)
+    if masked:
+        ops = alu_ops_per_block(L, True) * lay["n_blocks"]
+        achieved = ops / (dom_ms / 1e3) / 1e9                        # Gop/s
+        lanes, lsrc = alu_lanes_per_clk()
+        mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak_alu = NUM_SMS * lanes * mhz * 1e6 / 1e9
+        r = {"bound": "alu", "kernel": kkey, "achieved": round(achieved, 1), "peak": round(peak_alu, 1),
+             "unit": "Gop/s", "frac": round(achieved / peak_alu, 4), "traffic": traffic, "traffic_source": tsrc,
+             "algorithmic_bytes": alg_bytes, "alu_ops_per_block": alu_ops_per_block(L, True),
+             "peak_source": f"{NUM_SMS} SMs x {lanes} ALU-pipe lanes/clk/SM ({lsrc}) x {mhz} MHz (max clock)"}
+    else:
+        ach = alg_bytes / (dom_ms / 1e3) / 1e9
+        r = {"bound": "hbm", "kernel": kkey, "achieved": round(ach, 1), "peak": peaks.get("hbm_gbs"),
+             "unit": "GB/s", "frac": round(ach / peaks.get("hbm_gbs", 6551.7), 4), "traffic": traffic,
+             "traffic_source": tsrc, "algorithmic_bytes": alg_bytes,
+             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+    if traffic:
+        r["traffic_over_algorithmic"] = round(traffic / alg_bytes, 3)
+    if prof and prof.get("inst_per_block"):
+        # issue view: executed SASS instructions (ncu, same kernel and workload) per issue slot
+        mhz = peaks.get("sm_max_mhz", 1965.0)
+        issue = prof["inst_per_block"] * lay["n_blocks"] / (dom_ms / 1e3) / (NUM_SMS * 128 * mhz * 1e6)
+        r["issue_frac"] = round(issue, 4)
+        r["inst_per_block"] = prof["inst_per_block"]
+    return r
 
 
 def run_multi(args):
@@ -419,6 +485,7 @@ def run_multi(args):
     torch.cuda.set_device(dev)
     se.lib()
     key, L = synth.KEY, 2
+    flags = se.FLAG_PUBLIC_PLAIN if args.plain else 0
     if args.config == 4 and args.full:
         # C4-FULL (row a11 with row e): whole-matrix DWT, W = 32768, stripes of
         # block rows protected from their rows + 2(2^L-1) halo rows and recovered
@@ -436,7 +503,7 @@ def run_multi(args):
         del full
         # the fragments of the recover window (untimed setup: in a deployment they are read from storage)
         ext = se.fragment_protect_stripe(ext_in, n, W, L, key, iv, plan["rec_row0"],
-                                         plan["rec_row0"] + plan["rec_rows"], rec_src0)
+                                         plan["rec_row0"] + plan["rec_rows"], rec_src0, flags=flags)
         del ext_in
         nb = plan["n_blocks"]
         lay = se.fragment_layout(n, W, L, se.MODE_FULL)
@@ -446,11 +513,11 @@ def run_multi(args):
 
         def protect():
             se.fragment_protect_stripe(src, n, W, L, key, iv, plan["row_begin"], plan["row_end"], plan["src_row0"],
-                                       out=frag)
+                                       flags=flags, out=frag)
 
         def recover():
             se.fragment_recover_stripe(*ext, n, W, L, key, iv, plan["row_begin"], plan["row_end"], plan["rec_row0"],
-                                       plan["rec_rows"], out=out, report=rep)
+                                       plan["rec_rows"], flags=flags, out=out, report=rep)
 
         def check():
             return torch.equal(out, x) and rep.cpu().tolist() == [-1, 0]
@@ -458,31 +525,6 @@ def run_multi(args):
         workload = (f"C4-FULL 1 GiB W=32768 whole-matrix DWT L=2: {world} row stripes with "
                     f"{2 * ((1 << L) - 1)} halo rows per side (protect) / 1 halo block row (recover)")
         extra = {"stripe_rows": plan["row_end"] - plan["row_begin"], "mode_detail": "FULL"}
-    elif args.config == 4:
-        c = synth.CONFIGS[4]
-        n, W = c["n_bytes"], c["width"]
-        plan = shard.plan_stripes(n, W, L, world)[rank]
-        x_np = synth.config_input(4)[plan["byte_begin"]: plan["byte_end"]]
-        x = torch.from_numpy(np.ascontiguousarray(x_np)).to(dev)
-        del x_np
-        iv = synth.iv_for(4)
-        nloc = x.numel()
-        lay = se.fragment_layout(nloc, W, L, block_offset=plan["block_offset"])
-        frag = (se._empty(lay["a_bytes"], dev), se._empty(lay["b_bytes"], dev), se._empty(lay["c_bytes"], dev))
-        out = se._empty(nloc, dev)
-        rep = torch.empty(2, dtype=torch.int64, device=dev)
-
-        def protect():
-            se.fragment_protect(x, W, L, key, iv, block_offset=plan["block_offset"], out=frag)
-
-        def recover():
-            se.fragment_recover(*frag, nloc, W, L, key, iv, block_offset=plan["block_offset"], out=out, report=rep)
-
-        def check():
-            return torch.equal(out, x) and rep.cpu().tolist() == [-1, 0]
-        total_bytes, n_blocks_local = n, lay["n_blocks"]
-        workload = f"{c['name']} row stripes ({world} stripes of whole block-rows, block_offset per stripe)"
-        extra = {"stripe_bytes": nloc, "block_offset": plan["block_offset"]}
     else:
         sizes = synth.c5_file_sizes(10000, 5)
         mine = shard.plan_files(sizes, world)[rank]
@@ -493,7 +535,7 @@ def run_multi(args):
             files.append(torch.randint(0, 256, (int(sizes[i]),), dtype=torch.uint8, device=dev, generator=gen))
         widths = [synth.width_rule(int(sizes[i])) for i in mine]
         ivs = [synth.iv_for(5, i) for i in mine]
-        batch = se.Batch(files, widths, ivs, L, key)
+        batch = se.Batch(files, widths, ivs, L, key, flags=flags)
 
         def protect():
             batch.protect()
@@ -545,20 +587,23 @@ def run_multi(args):
         return None
     ms, mp, mr = (float(v) for v in t.tolist())
     peaks, peak_src = load_peaks()
-    peak_alu = NUM_SMS * ALU_LANES_PER_SM_CLK * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
-    achieved = alu_ops_per_block(L, True) * n_blocks_local / (max(mp, mr) / 1e3) / 1e9
+    lanes, lsrc = alu_lanes_per_clk()
+    peak_alu = NUM_SMS * lanes * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+    achieved = alu_ops_per_block(L, not args.plain) * n_blocks_local / (max(mp, mr) / 1e3) / 1e9
     return {
         "metric": "protect+recover GB/s per GPU and at 1/2/4/8 B200; % of HBM roofline",
         "value": round(total_bytes / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": dict({"workload": workload, "n_bytes_total": total_bytes, "levels": L,
+        "config": dict({"workload": workload + (" (PUBLIC_PLAIN)" if args.plain else ""),
+                        "n_bytes_total": total_bytes, "levels": L,
                         "mode": "FULL" if getattr(args, "full", False) else "BLOCK8",
                         "parallelism": f"dp{world} ({'row stripes' if args.config == 4 else 'by file'})",
                         "l2": "flushed between steps (2x L2 write + read-back)"}, **extra),
         "roofline": {"bound": "alu", "kernel": "k_protect/k_recover (rank 0 slowest)", "achieved": round(achieved, 1),
                      "peak": round(peak_alu, 1), "unit": "Gop/s", "frac": round(achieved / peak_alu, 4),
-                     "traffic": None, "peak_source": f"guide ALU pipe x {peaks.get('sm_max_mhz')} MHz ({peak_src})"},
+                     "traffic": None, "peak_source": f"{NUM_SMS} SMs x {lanes} ALU lanes/clk ({lsrc}) x "
+                                                     f"{peaks.get('sm_max_mhz')} MHz ({peak_src})"},
         "protect_gbs": round(total_bytes / (mp / 1e3) / 1e9, 3), "recover_gbs": round(total_bytes / (mr / 1e3) / 1e9, 3),
         "e2e": {"value": None, "unit": "GB/s", "note": "multi-file / stripe modes are device-resident; e2e is measured "
                                                        "on the default config"},
@@ -566,43 +611,52 @@ def run_multi(args):
     }
 
 
-def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=8 << 20, n_streams=4):
+def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=0, n_streams=3, block_offset=0,
+            world=1):
     """The same metric end to end through the public host API: one step =
     fragment_protect_host (pinned input -> H2D -> fused kernel -> D2H of the three
     fragments) + fragment_recover_host (H2D fragments -> kernel -> D2H bytes);
     the library pipelines chunks over several streams.  Both calls block, so
-    the step is timed host-side (perf_counter) around them."""
+    the step is timed host-side (perf_counter) around them; with several
+    ranks, between barriers and as the max over ranks."""
+    import torch.distributed as dist
     n = x_np.size
-    lay = se.fragment_layout(n, W, L)
+    lay = se.fragment_layout(n, W, L, block_offset=block_offset)
     hx = torch.from_numpy(x_np).pin_memory()
     frag = (se._host_empty(lay["a_bytes"]), se._host_empty(lay["b_bytes"]), se._host_empty(lay["c_bytes"]))
     hout = se._host_empty(n)
 
     def one():
-        se.fragment_protect_host(hx, W, L, key, iv, flags=flags, out=frag, chunk_bytes=chunk_bytes,
-                                 n_streams=n_streams)
-        _, rep = se.fragment_recover_host(*frag, n, W, L, key, iv, flags=flags, out=hout,
-                                          chunk_bytes=chunk_bytes, n_streams=n_streams)
+        se.fragment_protect_host(hx, W, L, key, iv, flags=flags, block_offset=block_offset, out=frag,
+                                 chunk_bytes=chunk_bytes, n_streams=n_streams)
+        _, rep = se.fragment_recover_host(*frag, n, W, L, key, iv, flags=flags, block_offset=block_offset,
+                                          out=hout, chunk_bytes=chunk_bytes, n_streams=n_streams)
         return rep
 
     for _ in range(3):
         one()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         rep = one()
     ms = (time.perf_counter() - t0) * 1e3 / steps
     assert torch.equal(hout, hx) and rep == (-1, 0)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        allreduce_max(t)
+        ms = float(t.item())
     frag_bytes = lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"]
     mapped = bool(flags & se.FLAG_HOST_MAPPED)
     how = ("SE_FLAG_HOST_MAPPED: the kernels read / write the pinned host buffers over PCIe, no staging"
            if mapped else (f"{chunk_bytes >> 10} KiB chunks" if chunk_bytes else
                            f"library-default chunks ({min(16 << 20, max(4 << 20, n // 4)) >> 10} KiB)")
            + f" on {n_streams} streams")
-    return {"value": round(n / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n + frag_bytes,
+    return {"value": round(n * world / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n + frag_bytes,
             "d2h_bytes_per_step": frag_bytes + n, "ms_per_step": round(ms, 4),
             "path": f"fragment_protect_host + fragment_recover_host (C ABI, pinned host buffers, {how}), "
-                    f"host wall clock"}
+                    f"host wall clock" + (", max over ranks; bytes are per rank" if world > 1 else "")}
 
 
 # ---------------------------------------------------------------- NEXT row f3: Chapter 4 DCT SE
@@ -716,16 +770,17 @@ def run_dct(args):
     dom_name, dom_ms = ("k_dct_protect", tp) if tp >= tr else ("k_dct_recover", tr)
     aesf = 1 if (dom_name == "k_dct_recover" or level == 1) else 0   # AES inside the kernel (k_dct.cu)
     kkey = f"{dom_name}<1, {level}, {1 if flags else 0}, {aesf}>"
-    traffic, traffic_src = load_traffic(kkey)
+    traffic, traffic_src = load_traffic(kkey, f"Table 4.1 image {W}x{H} grey, level {level}")
     alg_bytes = 2 * n + lay["a_bytes"]
     if level == 2:
         ops_blk = sum(DCT_ALU_OPS.values()) + DCT_SHA512_OPS[bool(flags)]
         ach = ops_blk * lay["records"] / (dom_ms / 1e3) / 1e9
-        peak_alu = NUM_SMS * ALU_LANES_PER_SM_CLK * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+        lanes, lsrc = alu_lanes_per_clk()
+        peak_alu = NUM_SMS * lanes * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
         roofline = {"bound": "alu", "kernel": kkey, "achieved": round(ach, 1), "peak": round(peak_alu, 1),
                     "unit": "Gop/s", "frac": round(ach / peak_alu, 4), "traffic": traffic,
                     "traffic_source": traffic_src, "algorithmic_bytes": alg_bytes, "alu_ops_per_block": ops_blk,
-                    "peak_source": f"guide: {NUM_SMS} SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x "
+                    "peak_source": f"{NUM_SMS} SMs x {lanes} ALU lanes/clk ({lsrc}) x "
                                    f"{peaks.get('sm_max_mhz', 1965.0)} MHz ({peak_src} max clock)"}
     else:
         ach = alg_bytes / (dom_ms / 1e3) / 1e9
@@ -793,7 +848,7 @@ def run_dct(args):
 
 # ---------------------------------------------------------------- CPU oracle baseline
 
-def oracle_time(x_np, W, L, key, iv, flags, n_blocks_sample, threads, reps=1):
+def oracle_time(x_np, W, L, key, iv, flags, n_blocks_sample, threads, reps=1, block_offset=0):
     """Oracle protect + recover over the first n_blocks_sample blocks, split
     across `threads` host threads (ctypes releases the GIL)."""
     from concurrent.futures import ThreadPoolExecutor
@@ -808,10 +863,11 @@ def oracle_time(x_np, W, L, key, iv, flags, n_blocks_sample, threads, reps=1):
     ranges = [(g0 * 128, min(nb, (g0 + per) * 128)) for g0 in range(0, groups, per)]
 
     def prot(r):
-        oracle.protect(x_np, W, L, key, iv, flags=flags, block_range=r, out=bufs)
+        oracle.protect(x_np, W, L, key, iv, flags=flags, block_offset=block_offset, block_range=r, out=bufs)
 
     def rec(r):
-        oracle.recover(bufs[0], bufs[1], bufs[2], x_np.size, W, L, key, iv, flags=flags, block_range=r, out=out)
+        oracle.recover(bufs[0], bufs[1], bufs[2], x_np.size, W, L, key, iv, flags=flags, block_offset=block_offset,
+                       block_range=r, out=out)
 
     with ThreadPoolExecutor(max_workers=threads) as ex:
         t0 = time.perf_counter()
@@ -822,19 +878,19 @@ def oracle_time(x_np, W, L, key, iv, flags, n_blocks_sample, threads, reps=1):
     return nb * reps, dt
 
 
-def cpu_baseline(x_np, W, L, key, iv, flags, seconds):
+def cpu_baseline(x_np, W, L, key, iv, flags, seconds, block_offset=0):
     threads = os.cpu_count() or 1
-    nb_probe, dt_probe = oracle_time(x_np, W, L, key, iv, flags, 256 * threads, threads)
+    nb_probe, dt_probe = oracle_time(x_np, W, L, key, iv, flags, 256 * threads, threads, block_offset=block_offset)
     rate = nb_probe / max(dt_probe, 1e-6)
     total_nb = -(-x_np.size // (W * 8)) * (W // 8)
     want = max(128, rate * seconds)
     nb = int(min(total_nb, want))
     reps = max(1, min(50, int(want // nb)))
-    done, dt = oracle_time(x_np, W, L, key, iv, flags, nb, threads, reps)
+    done, dt = oracle_time(x_np, W, L, key, iv, flags, nb, threads, reps, block_offset=block_offset)
     gbs = done * 64 / dt / 1e9
     # the same on one core (SURVEY.md §8.1 row d: 1 core and all host cores), a ~3 s sample
     nb1 = int(min(total_nb, max(128, rate / threads * 3.0)))
-    done1, dt1 = oracle_time(x_np, W, L, key, iv, flags, nb1, 1)
+    done1, dt1 = oracle_time(x_np, W, L, key, iv, flags, nb1, 1, block_offset=block_offset)
     return {"value": round(gbs, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
             "sample": f"{reps} pass(es) over the first {nb} of {total_nb} 8x8 blocks of the same input "
                       f"(protect+recover), {threads} host threads, {dt:.1f} s",
@@ -854,52 +910,80 @@ def cpu_model():
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle (oracle/, plain C) as it stands, on
+    all host cores, over the SAME workload as the repo arm's line (same
+    `config`): every timed step is protect + recover of the whole input (C4:
+    the whole 1 GiB file; C1-C3: one file per rank of the repo arm).  Warm-up
+    steps run on a bounded prefix (they only warm caches and threads).  Under
+    torchrun, rank 0 alone runs; the other ranks exit without work."""
     rank, world, _ = dist_env()
     if rank != 0:
         return None
-    c, x_np = workload(args.config)
+    c = synth.CONFIGS[args.config]
     W, L = c["width"], c["levels"]
-    key, iv = synth.KEY, synth.iv_for(args.config, 0)
+    key = synth.KEY
     flags = 1 if args.plain else 0
     threads = os.cpu_count() or 1
-    nb_probe, dt_probe = oracle_time(x_np, W, L, key, iv, flags, 128 * threads, threads)
-    rate = nb_probe / max(dt_probe, 1e-6)
-    total_nb = -(-x_np.size // (W * 8)) * (W // 8)
-    budget = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.2)
-    nb = int(min(total_nb, max(128, rate * budget)))
+    if args.config == 4:
+        inputs = [(synth.config_input(4), synth.iv_for(4))]
+        scaling = "strong"
+    else:
+        x_np = synth.config_input(args.config)
+        inputs = [(x_np, synth.iv_for(args.config, r)) for r in range(world)]
+        scaling = "weak"
+    total_bytes = sum(x.size for x, _ in inputs)
+    nb_of = [-(-x.size // (W * 8)) * (W // 8) for x, _ in inputs]
+    x0, iv0 = inputs[0]
+    nb_probe, dt_probe = oracle_time(x0, W, L, key, iv0, flags, 128 * threads, threads)
+    rate = nb_probe / max(dt_probe, 1e-6)                     # blocks/s, all threads
+    nb_warm = int(min(nb_of[0], max(128, rate * 1.0)))
     for _ in range(args.warmup):
-        oracle_time(x_np, W, L, key, iv, flags, nb, threads)
+        oracle_time(x0, W, L, key, iv0, flags, nb_warm, threads)
     times = []
     for _ in range(args.steps):
-        _, dt = oracle_time(x_np, W, L, key, iv, flags, nb, threads)
+        dt = 0.0
+        for (x, iv), nb in zip(inputs, nb_of):
+            _, d = oracle_time(x, W, L, key, iv, flags, nb, threads)
+            dt += d
         times.append(dt)
     ms = 1e3 * sum(times) / len(times)
-    gbs = nb * 64 / (ms / 1e3) / 1e9
-    sample = f"first {nb} of {total_nb} 8x8 blocks per step (protect+recover), {threads} host threads"
+    gbs = total_bytes / (ms / 1e3) / 1e9
+    sample = (f"every timed step = protect + recover of the whole workload ({sum(nb_of)} 8x8 blocks, "
+              f"{total_bytes} bytes), {threads} host threads; warm-up steps on the first {nb_warm} blocks")
     return {
         "metric": "protect+recover GB/s per GPU and at 1/2/4/8 B200; % of HBM roofline",
         "impl": "reference", "value": round(gbs, 6), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": c["name"], "n_bytes": x_np.size, "width": W, "levels": L, "mode": "BLOCK8"},
+        "scaling": scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": config_dict(args, world),
         "cpu_baseline": {"value": round(gbs, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
                          "sample": sample, "host_cpu": cpu_model()},
         "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
+def relaunch_distributed(n: int):
+    """`python bench.py --gpus N` outside torchrun: re-run this command as N
+    ranks, one process per GPU (the driver's own launch line)."""
+    port = os.environ.get("MASTER_PORT", "29533")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", port, os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--stripes", action="store_true", help="C4: split the one file into per-rank row stripes")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (default 4: the 1 GiB file, one row stripe per rank)")
+    ap.add_argument("--stripes", action="store_true", help="(kept for old command lines: C4 always runs as stripes)")
     ap.add_argument("--full", action="store_true", help="C4 stripes in FULL mode (whole-matrix DWT, halo rows)")
     ap.add_argument("--impl", default="se", choices=["se", "reference"])
     ap.add_argument("--plain", action="store_true", help="PUBLIC_PLAIN measurement mode (C26)")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of sustained warm-up load")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-chunk-kib", type=int, default=0, help="host-API chunk size (input KiB; 0 = library default)")
     ap.add_argument("--e2e-streams", type=int, default=3, help="host-API CUDA streams")
     ap.add_argument("--e2e-mapped", type=int, default=0, help="1: zero-copy host API (SE_FLAG_HOST_MAPPED)")
@@ -912,11 +996,16 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch_distributed(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)")
     if args.impl == "reference":
         line = run_reference(args)
     elif args.dct:
         line = run_dct(args)
-    elif args.config == 5 or (args.config == 4 and args.stripes):
+    elif args.config == 5 or (args.config == 4 and args.full):
         line = run_multi(args)
     else:
         line = run_se(args)

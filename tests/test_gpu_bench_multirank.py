@@ -26,7 +26,7 @@ def free_port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("extra", [[], ["--config", "4", "--stripes", "--steps", "1"]])
+@pytest.mark.parametrize("extra", [["--steps", "1"], ["--config", "2"], ["--config", "1", "--impl", "reference"]])
 def test_two_ranks_print_one_line(extra):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -42,3 +42,30 @@ def test_two_ranks_print_one_line(extra):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] in (1, 2) and d["warmup"] == 3
     assert d["scaling"] in ("weak", "strong")
+
+
+def _nccl_worker(port):
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    t = torch.tensor([3.0, 5.0], dtype=torch.float64, device=dev)
+    bench.allreduce_max(t)
+    torch.cuda.synchronize()
+    assert t.tolist() == [3.0, 5.0]
+    dist.destroy_process_group()
+
+
+def test_allreduce_max_inside_a_real_nccl_group():
+    """bench.allreduce_max on a CUDA tensor in an NCCL process group (the
+    branch round 1 never ran: it recursed)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = torch.multiprocessing.get_context("spawn")
+    p = ctx.Process(target=_nccl_worker, args=(free_port(),))
+    p.start()
+    p.join(timeout=300)
+    assert p.exitcode == 0

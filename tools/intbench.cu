@@ -9,8 +9,12 @@
 #define CHAINS 8
 constexpr int ITERS = 4096;
 
+__device__ unsigned long long g_cycles[4096];
+
 template <int OP>
 __global__ void __launch_bounds__(256) k(uint32_t* out, uint32_t seed, uint32_t one) {
+    __syncthreads();
+    const long long c0 = clock64();
     uint32_t x[CHAINS], y[CHAINS];
 #pragma unroll
     for (int c = 0; c < CHAINS; ++c) { x[c] = seed + threadIdx.x * 7 + c; y[c] = seed ^ (c * 0x9e3779b9u); }
@@ -37,6 +41,10 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, uint32_t seed, uint32_t 
                 x[c] += y[c];
             } else if (OP == 7) {   // PRMT
                 asm volatile("prmt.b32 %0, %0, %1, 0x3210;" : "+r"(x[c]) : "r"(y[c]));
+            } else if (OP == 8) {   // issue rate: LOP3 | IMAD | FFMA | LOP3 ... on independent chains
+                if (c % 4 == 0 || c % 4 == 2) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(y[c]), "r"(one));
+                else if (c % 4 == 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(one), "r"(y[c]));
+                else asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+r"(x[c]) : "r"(y[c]));
             }
         }
     }
@@ -44,6 +52,8 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, uint32_t seed, uint32_t 
 #pragma unroll
     for (int c = 0; c < CHAINS; ++c) r ^= x[c];
     out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_cycles[blockIdx.x] = (unsigned long long)(clock64() - c0);
 }
 
 template <int OP>
@@ -59,10 +69,19 @@ float run(uint32_t* d, int grid, const char* name, int sms, float ops_per_chain_
     cudaEventElapsedTime(&ms, a, b);
     int clk_khz;
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+    static unsigned long long cyc[4096];
+    cudaMemcpyFromSymbol(cyc, g_cycles, sizeof(unsigned long long) * (grid < 4096 ? grid : 4096));
+    double mean_cyc = 0;
+    const int nc = grid < 4096 ? grid : 4096;
+    for (int i = 0; i < nc; ++i) mean_cyc += (double)cyc[i] / nc;
     double lane_ops = (double)grid * 256 * ITERS * CHAINS * ops_per_chain_iter;
     double per_s = lane_ops / (ms / 1e3);
-    printf("{\"op\": \"%s\", \"ms\": %.4f, \"Tlane_ops_per_s\": %.3f, \"lane_ops_per_clk_per_sm_at_max_clock\": %.1f}\n",
-           name, ms, per_s / 1e12, per_s / sms / (clk_khz * 1e3));
+    // all grid/sms CTAs of an SM are co-resident (8 x 256 threads), so the
+    // SM's lane ops per SM cycle = CTAs per SM x ops per CTA / CTA cycles
+    const double per_clk_sm = (double)(grid / sms) * 256 * ITERS * CHAINS * ops_per_chain_iter / mean_cyc;
+    printf("{\"op\": \"%s\", \"ms\": %.4f, \"Tlane_ops_per_s\": %.3f, \"lane_ops_per_clk_per_sm\": %.2f, "
+           "\"lane_ops_per_clk_per_sm_at_max_clock\": %.2f, \"effective_mhz\": %.0f}\n",
+           name, ms, per_s / 1e12, per_clk_sm, per_s / sms / (clk_khz * 1e3), per_s / sms / per_clk_sm / 1e6);
     return ms;
 }
 
@@ -80,6 +99,7 @@ int main() {
     run<5>(d, grid, "SHF|IMAD alternating", sms, 1);
     run<6>(d, grid, "IMAD.HI(+IADD)", sms, 1);
     run<7>(d, grid, "PRMT", sms, 1);
+    run<8>(d, grid, "issue: LOP3|IMAD|LOP3|FFMA", sms, 1);
     printf("{\"sms\": %d}\n", sms);
     return 0;
 }
