@@ -31,7 +31,8 @@
  *              framing (C15): M_B = K||IV||be64(b)||A_b, M_C = K||IV||be64(b)||B'_b.
  *   Device ptrs  caller-owned device memory (e.g. torch tensors), 16-byte
  *              aligned (else SE_EALIGN), valid until the stream reaches the
- *              work.  No call allocates device memory on the hot path.
+ *              work.  No device-resident call allocates device memory or
+ *              synchronises; FULL mode takes a caller workspace (below).
  *   stream     a cudaStream_t passed as void* (NULL = legacy default stream).
  *              Calls are asynchronous on it; all run on the current device.
  *   Errors     return se_status; nothing is printed.  Launch failures are
@@ -101,16 +102,42 @@ int fragment_layout(const se_geom* g, se_layout* out);
 /* ---- protect: rows a1-a9 in one kernel -----------------------------------
  * d_in: n_bytes input bytes (device).  d_a, d_b, d_c: device buffers of
  * a_bytes, b_bytes, c_bytes (d_b may be NULL when b_bytes == 0).  Writes the
- * protected streams A', B', C'.  n_bytes == 0 is a no-op. */
+ * protected streams A', B', C'.  n_bytes == 0 is a no-op.  One kernel launch
+ * (BLOCK8); AES-128-CTR of A runs inside it (no scratch).  At most 2^32
+ * 8x8 blocks (256 GiB) per call, else SE_EINVAL.  FULL mode needs a
+ * workspace: use fragment_protect_ws (fragment_protect returns SE_EINVAL). */
 int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
                      const void* d_in, void* d_a, void* d_b, void* d_c, void* stream);
 
 /* ---- recover: row a10 -----------------------------------------------------
  * Inverse of fragment_protect; writes exactly n_bytes bytes to d_out.
- * d_report (nullable, device) receives the corruption report. */
+ * d_report (nullable, device) receives the corruption report (set to
+ * {-1, 0} by the call, then updated by the kernel).  FULL mode: use
+ * fragment_recover_ws. */
 int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
                      const void* d_a, const void* d_b, const void* d_c, void* d_out,
                      se_report* d_report, void* stream);
+
+/* ---- caller-owned workspace (FULL mode, row a11) ---------------------------
+ * No call allocates device memory.  FULL mode keeps the R x W int16 Mallat
+ * coefficients of the matrix (stripe calls: of the stripe's row window)
+ * between its transform and footprint kernels in a workspace the caller
+ * provides: fragment_workspace_size returns its size in *bytes (0 in BLOCK8
+ * mode; st = NULL for the whole-file calls, else the stripe the
+ * fragment_*_stripe call will get).  The _ws calls are fragment_protect /
+ * fragment_recover plus that workspace (16-byte aligned device memory, at
+ * least the queried size, else SE_EINVAL / SE_EALIGN; it may be reused as
+ * soon as the stream has passed the call). */
+typedef struct {
+    uint64_t row_begin, row_end, src_row0, src_rows;
+} se_stripe;
+int fragment_workspace_size(const se_geom* g, const se_stripe* st, uint64_t* bytes);
+int fragment_protect_ws(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
+                        const void* d_in, void* d_a, void* d_b, void* d_c,
+                        void* d_ws, uint64_t ws_bytes, void* stream);
+int fragment_recover_ws(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
+                        const void* d_a, const void* d_b, const void* d_c, void* d_out,
+                        se_report* d_report, void* d_ws, uint64_t ws_bytes, void* stream);
 
 /* ---- batched protect / recover (many independent files, one launch) -----
  * "batch of 10,000 mixed-size files ... sharded by file" (BASELINE.json C5;
@@ -179,16 +206,14 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
  * Outputs: protect writes the stripe's blocks' records (stream slices at
  * byte offset first_block * bits / 8 of the whole-file streams); recover
  * writes the stripe's bytes (row_begin * W onwards, clipped at n_bytes) and
- * reports bad blocks with stripe-local indices.  SE_EINVAL on a bad window. */
-typedef struct {
-    uint64_t row_begin, row_end, src_row0, src_rows;
-} se_stripe;
-
+ * reports bad blocks with stripe-local indices.  SE_EINVAL on a bad window.
+ * d_ws / ws_bytes: the workspace of fragment_workspace_size(g, s, ...). */
 int fragment_protect_stripe(const se_geom* g, const se_stripe* s, const uint8_t key[16], const uint8_t iv[16],
-                            const void* d_in, void* d_a, void* d_b, void* d_c, void* stream);
+                            const void* d_in, void* d_a, void* d_b, void* d_c, void* d_ws, uint64_t ws_bytes,
+                            void* stream);
 int fragment_recover_stripe(const se_geom* g, const se_stripe* s, const uint8_t key[16], const uint8_t iv[16],
                             const void* d_a, const void* d_b, const void* d_c, void* d_out,
-                            se_report* d_report, void* stream);
+                            se_report* d_report, void* d_ws, uint64_t ws_bytes, void* stream);
 
 /* ---- transform only: rows a1-a4 / a11 ------------------------------------
  * d_coef: R x W int16 (R = layout.rows).  BLOCK8: block (br, bc) coefficient

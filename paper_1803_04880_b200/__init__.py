@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libse.so")
 CSRC = os.path.join(_HERE, "csrc")
-SOURCES = ["se_api.cu", "k_block8.cu", "k_full.cu", "k_cipher.cu", "k_stats.cu", "se_host.cu",
+SOURCES = ["se_api.cu", "k_block8.cu", "k_tile.cu", "k_full.cu", "k_cipher.cu", "k_stats.cu", "se_host.cu",
            "k_dct.cu", "se_dct_api.cu", "se_container.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
@@ -98,7 +98,8 @@ SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_
            "dct_layout", "dct_protect", "dct_recover", "dct_select", "dct8_forward", "dct8_inverse",
            "se_container_streams", "se_container_size", "se_container_pack", "se_container_open",
            "se_disperse_plan", "se_storage_footprint", "se_sha256",
-           "fragment_protect_stripe", "fragment_recover_stripe"]
+           "fragment_protect_stripe", "fragment_recover_stripe", "fragment_workspace_size",
+           "fragment_protect_ws", "fragment_recover_ws"]
 
 
 class Stripe(C.Structure):
@@ -168,8 +169,11 @@ def lib():
         L.se_sha256.argtypes = [vp, C.c_uint64, vp]
         L.se_sha256.restype = None
         sp = C.POINTER(Stripe)
-        L.fragment_protect_stripe.argtypes = [gp, sp, u8p, u8p, vp, vp, vp, vp, vp]
-        L.fragment_recover_stripe.argtypes = [gp, sp, u8p, u8p, vp, vp, vp, vp, vp, vp]
+        L.fragment_protect_stripe.argtypes = [gp, sp, u8p, u8p, vp, vp, vp, vp, vp, C.c_uint64, vp]
+        L.fragment_recover_stripe.argtypes = [gp, sp, u8p, u8p, vp, vp, vp, vp, vp, vp, C.c_uint64, vp]
+        L.fragment_workspace_size.argtypes = [gp, sp, C.POINTER(C.c_uint64)]
+        L.fragment_protect_ws.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp, C.c_uint64, vp]
+        L.fragment_recover_ws.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp, vp, C.c_uint64, vp]
         L.se_strerror.argtypes = [C.c_int]
         L.se_strerror.restype = C.c_char_p
         L.se_launch_count.argtypes = [C.c_int]
@@ -225,34 +229,74 @@ def _empty(n, device):
         torch.empty(16, dtype=torch.uint8, device=device)[:0]
 
 
+def fragment_workspace_size(n_bytes: int, width: int, levels: int, mode: int = MODE_BLOCK8, stripe=None) -> int:
+    """Device workspace bytes a FULL-mode call needs (0 in BLOCK8); stripe =
+    (row_begin, row_end, src_row0, src_rows) for the stripe calls."""
+    g = _geom(n_bytes, width, levels, mode)
+    st = Stripe(*[int(v) for v in stripe]) if stripe is not None else None
+    out = C.c_uint64()
+    _check(lib().fragment_workspace_size(C.byref(g), C.byref(st) if st is not None else None, C.byref(out)),
+           "fragment_workspace_size")
+    return int(out.value)
+
+
+def _workspace(nbytes: int, device, stream):
+    """A caller-side workspace tensor (torch's caching allocator; kept alive
+    for the stream's use of it with record_stream)."""
+    import torch
+    if nbytes == 0:
+        return None
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    if stream is not None and hasattr(stream, "cuda_stream"):
+        ws.record_stream(stream)
+    return ws
+
+
 def fragment_protect(x, width: int, levels: int, key, iv, mode: int = MODE_BLOCK8, flags: int = 0,
-                     block_offset: int = 0, out=None, stream=None):
-    """x: 1-D uint8 CUDA tensor (n bytes).  Returns device tensors (A', B', C')."""
+                     block_offset: int = 0, out=None, stream=None, workspace=None):
+    """x: 1-D uint8 CUDA tensor (n bytes).  Returns device tensors (A', B', C').
+    FULL mode uses `workspace` (a uint8 CUDA tensor of fragment_workspace_size
+    bytes) or allocates one through torch."""
     lay = fragment_layout(x.numel(), width, levels, mode, flags, block_offset)
     a, b, c = out if out is not None else (_empty(lay["a_bytes"], x.device), _empty(lay["b_bytes"], x.device),
                                            _empty(lay["c_bytes"], x.device))
     g = _geom(x.numel(), width, levels, mode, flags, block_offset)
+    if mode == MODE_FULL:
+        ws = workspace if workspace is not None else \
+            _workspace(fragment_workspace_size(x.numel(), width, levels, mode), x.device, stream)
+        _check(lib().fragment_protect_ws(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(x), _ptr(a),
+                                         _ptr(b) if b.numel() else None, _ptr(c), _ptr(ws),
+                                         ws.numel() if ws is not None else 0, _stream(stream)), "fragment_protect_ws")
+        return a, b, c
     _check(lib().fragment_protect(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(x), _ptr(a),
                                   _ptr(b) if b.numel() else None, _ptr(c), _stream(stream)), "fragment_protect")
     return a, b, c
 
 
 def fragment_recover(a, b, c, n_bytes: int, width: int, levels: int, key, iv, mode: int = MODE_BLOCK8,
-                     flags: int = 0, block_offset: int = 0, out=None, report=None, stream=None):
+                     flags: int = 0, block_offset: int = 0, out=None, report=None, stream=None, workspace=None):
     """Returns (bytes tensor, report tensor int64[2] = [first_bad_block, bad_blocks])."""
     import torch
     dev = a.device
     o = out if out is not None else _empty(n_bytes, dev)
     rep = report if report is not None else torch.empty(2, dtype=torch.int64, device=dev)
     g = _geom(n_bytes, width, levels, mode, flags, block_offset)
-    _check(lib().fragment_recover(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(a),
-                                  _ptr(b) if b is not None and b.numel() else None, _ptr(c), _ptr(o),
-                                  _ptr(rep), _stream(stream)), "fragment_recover")
+    bb = _ptr(b) if b is not None and b.numel() else None
+    if mode == MODE_FULL:
+        ws = workspace if workspace is not None else \
+            _workspace(fragment_workspace_size(n_bytes, width, levels, mode), dev, stream)
+        _check(lib().fragment_recover_ws(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(a), bb, _ptr(c),
+                                         _ptr(o), _ptr(rep), _ptr(ws), ws.numel() if ws is not None else 0,
+                                         _stream(stream)), "fragment_recover_ws")
+        return o, rep
+    _check(lib().fragment_recover(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(a), bb, _ptr(c),
+                                  _ptr(o), _ptr(rep), _stream(stream)), "fragment_recover")
     return o, rep
 
 
 def fragment_protect_stripe(src, n_bytes: int, width: int, levels: int, key, iv, row_begin: int, row_end: int,
-                            src_row0: int, flags: int = 0, block_offset: int = 0, out=None, stream=None):
+                            src_row0: int, flags: int = 0, block_offset: int = 0, out=None, stream=None,
+                            workspace=None):
     """FULL-mode stripe: `src` = input bytes of rows [src_row0, ...) (the stripe
     plus halo rows).  Returns the stripe's (A', B', C') slices (device)."""
     lay = fragment_layout(n_bytes, width, levels, MODE_FULL, flags, block_offset)
@@ -262,16 +306,19 @@ def fragment_protect_stripe(src, n_bytes: int, width: int, levels: int, key, iv,
     src_rows = -(-src.numel() // width)
     st = Stripe(int(row_begin), int(row_end), int(src_row0), int(min(src_rows, lay["rows"] - src_row0)))
     g = _geom(n_bytes, width, levels, MODE_FULL, flags, block_offset)
+    ws = workspace if workspace is not None else _workspace(
+        fragment_workspace_size(n_bytes, width, levels, MODE_FULL, (st.row_begin, st.row_end, st.src_row0,
+                                                                    st.src_rows)), src.device, stream)
     _check(lib().fragment_protect_stripe(C.byref(g), C.byref(st), _bytes16(key, "key"), _bytes16(iv, "iv"),
                                          _ptr(src), _ptr(a), _ptr(b) if b.numel() else None, _ptr(c),
-                                         _stream(stream)),
+                                         _ptr(ws), ws.numel(), _stream(stream)),
            "fragment_protect_stripe")
     return a, b, c
 
 
 def fragment_recover_stripe(a, b, c, n_bytes: int, width: int, levels: int, key, iv, row_begin: int, row_end: int,
                             src_row0: int, src_rows: int, flags: int = 0, block_offset: int = 0, out=None,
-                            report=None, stream=None):
+                            report=None, stream=None, workspace=None):
     """FULL-mode stripe recovery from the fragments of block rows [src_row0/8,
     (src_row0+src_rows)/8).  Returns (stripe bytes, report[2])."""
     import torch
@@ -281,9 +328,12 @@ def fragment_recover_stripe(a, b, c, n_bytes: int, width: int, levels: int, key,
     rep = report if report is not None else torch.empty(2, dtype=torch.int64, device=dev)
     st = Stripe(int(row_begin), int(row_end), int(src_row0), int(src_rows))
     g = _geom(n_bytes, width, levels, MODE_FULL, flags, block_offset)
+    ws = workspace if workspace is not None else _workspace(
+        fragment_workspace_size(n_bytes, width, levels, MODE_FULL, (row_begin, row_end, src_row0, src_rows)),
+        dev, stream)
     _check(lib().fragment_recover_stripe(C.byref(g), C.byref(st), _bytes16(key, "key"), _bytes16(iv, "iv"),
                                          _ptr(a), _ptr(b) if b is not None and b.numel() else None, _ptr(c),
-                                         _ptr(o), _ptr(rep), _stream(stream)),
+                                         _ptr(o), _ptr(rep), _ptr(ws), ws.numel(), _stream(stream)),
            "fragment_recover_stripe")
     return o, rep
 

@@ -332,13 +332,17 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
 
     const int tid = threadIdx.x;
     const uint64_t blk = cta * BPC + tid;
+    __shared__ AesSmem aes;
+    aes_load_tables(aes, tid, BPC);                       // constant tables: before the grid dependency
     for (int i = tid; i < SA_W; i += BPC) sa[i] = 0;
     for (int i = tid; i < SB_W; i += BPC) sb[i] = 0;
+    // programmatic dependent launch: inputs (and FULL-mode coefficients) are
+    // written by earlier work on the stream
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
 
     if (blk < p.n_blocks) {
-        const uint32_t b32 = (uint32_t)blk;                 // < 2^32 blocks per call (256 GiB)
-        const uint64_t br = b32 / p.bpr, bc = b32 - (uint32_t)br * p.bpr;
+        const uint64_t br = blk / p.bpr, bc = blk - br * p.bpr;
         int v[8][8];
         if constexpr (MODE == 0) {
             load_block(p.in, p.n_bytes, p.width, br, bc, v);
@@ -378,11 +382,8 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
     // row a9: 128-bit coalesced stores of the CTA's slice of each stream;
     // A' = A ^ keystream on the way out (row a6, XOR half)
     const uint64_t a0 = cta * (BPC / 8ull) * R::ABITS, c0 = cta * (BPC / 8ull) * R::CBITS;
-    if constexpr (!MASK && SE_PROT_FUSED_AES) {
-        // unmasked protect: encrypt the CTA's A slice (whole AES counter blocks) here
-        __shared__ AesSmem aes;
-        aes_load_tables(aes, tid, BPC);
-        __syncthreads();
+    {
+        // row a6: encrypt the CTA's A slice (whole AES counter blocks) on the way out
         const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
         const uint32_t nblk = (uint32_t)((alen + 15) / 16);
         for (uint32_t j = tid; j < nblk; j += BPC) {
@@ -394,11 +395,6 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
         }
         __syncthreads();
         copy_s2g<BPC>(p.a + a0, sa, alen, tid);
-    } else {
-        asm volatile("griddepcontrol.wait;" ::: "memory");          // keystream kernel complete
-        const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
-        if (p.ks) copy_s2g_xor<BPC>(p.a + a0, sa, p.ks + a0, alen, tid);   // keystream in device scratch
-        else copy_s2g_xor_global<BPC>(p.a + a0, sa, alen, tid);           // keystream already in A'
     }
     if (R::BBITS) {
         const uint64_t b0 = cta * (BPC / 8ull) * R::BBITS;
@@ -436,7 +432,10 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
     const uint64_t blk = cta * BPC + tid;
     const uint64_t a0 = cta * (BPC / 8ull) * R::ABITS, c0 = cta * (BPC / 8ull) * R::CBITS;
     const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
+    __shared__ AesSmem aes;
+    aes_load_tables(aes, tid, BPC);                       // constant tables: before the grid dependency
     if (tid == 0) { s_first = ~0ull; s_bad = 0; }
+    asm volatile("griddepcontrol.wait;" ::: "memory");    // fragments / report written by earlier work
     copy_g2s<BPC>(sa, p.a + a0, alen, SA_W * 4, tid);
     if (R::BBITS) {
         const uint64_t b0 = cta * (BPC / 8ull) * R::BBITS;
@@ -455,12 +454,8 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         smem_get_record<R::CW, R::CBITS>(sc, SC_W, (uint32_t)tid * R::CBITS, C);
         if (MASK && R::BBITS) mask_c<R::BW, R::BBYTES, SPEC>(p, gb, B, C);    // C from B'
     }
-    if constexpr (!MASK && SE_REC_FUSED_AES) {
-        // unmasked (latency-bound) recovery: decrypt the CTA's A slice - whole
-        // AES counter blocks - here instead of waiting for a keystream kernel
-        __shared__ AesSmem aes;
-        aes_load_tables(aes, tid, BPC);
-        __syncthreads();
+    {
+        // row a6: decrypt the CTA's A slice (whole AES counter blocks) in shared memory
         const uint32_t nblk = (uint32_t)((alen + 15) / 16);
         for (uint32_t j = tid; j < nblk; j += BPC) {
             uint32_t x[4];
@@ -469,9 +464,6 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
 #pragma unroll
             for (int k = 0; k < 4; ++k) sa[4 * j + k] ^= bswap32(x[k]);
         }
-    } else {
-        asm volatile("griddepcontrol.wait;" ::: "memory");                  // keystream kernel complete
-        xor_g2s<BPC>(sa, p.ks + a0, alen, tid);                                   // A' -> A
     }
     __syncthreads();                                                         // plain A ready
 

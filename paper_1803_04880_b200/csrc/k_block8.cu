@@ -108,6 +108,7 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
     __shared__ uint32_t s_job;
     using R = Rec<L>;
     const uint32_t x = blockIdx.x;
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // job table / report init written by earlier work
     if (threadIdx.x < 32) {
         // largest j with cta_begin <= x: 32-ary search by warp 0 (3 dependent
         // loads for 10,000 jobs instead of 14 for a binary search)
@@ -155,8 +156,6 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
         sp.mid256[t - 44] = dv.mid256[t - 44];
     } else if (t >= 52 && t < 60) {
         sp.mid512[t - 52] = dv.mid512[t - 52];
-    } else if (t == 60) {
-        sp.ks = bp.ks ? bp.ks + job.cta_begin * 16ull * R::ABITS : nullptr;
     }
     if (SE_BATCH_SPEC && t >= 64) {                  // this file's C-mask schedule constants
         const uint32_t* src = reinterpret_cast<const uint32_t*>(&dv.s512);

@@ -590,8 +590,7 @@ void launch_level(const DctParams& p, uint32_t level, bool keyed, int op, unsign
 // slots to spare (level 1, and recovery, which also skips the keystream
 // scratch), not in the ALU-bound level-2 protect (100.4 vs 97.3 us).
 bool dct_fused_aes(int op, uint32_t level) {
-    if (!SE_DCT_FUSED_AES) return false;
-    return op == 1 || level == 1;
+    return op == 1 || (SE_DCT_FUSED_AES && level == 1);    // recovery: always in-kernel (no scratch)
 }
 
 int launch_dct(const DctParams& p, uint32_t channels, uint32_t level, bool keyed, int op, void* stream) {

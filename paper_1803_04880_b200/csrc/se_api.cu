@@ -4,13 +4,12 @@
 // for every block once on the host — AES-128 key schedule (FIPS-197 §5.2),
 // the CTR start counter (C13), and the SHA-256 / SHA-512 midstates over the
 // constant message prefix K||IV (C15) — and launches the fused kernels on the
-// caller's stream.  No device allocation, no synchronisation on the hot path.
+// caller's stream.  No device allocation, no synchronisation on the hot path:
+// FULL mode takes a caller-owned workspace (fragment_workspace_size).
 #include <cuda_runtime.h>
 #include <string.h>
 
 #include <algorithm>
-#include <map>
-#include <mutex>
 
 #include "se_internal.h"
 #include "../../include/se_container.h"
@@ -197,54 +196,6 @@ static void fill_fused(FusedParams& p, const se_geom* g, const se_layout& lay, c
     fill_sched(p, lay);
 }
 
-// Keep the stream-ordered pool's memory across calls (default release
-// threshold 0 would hand it back to the OS at every synchronisation).
-void keep_pool() {
-    static thread_local int done_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (done_dev == dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done_dev = dev;
-}
-
-// Keystream scratch for recovery, cached per (device, stream): calls on one
-// stream are ordered, so they can share a buffer (grown with cudaFreeAsync /
-// cudaMallocAsync on that stream); the stream id (cudaStreamGetId) is never
-// reused, unlike the handle.  Bounded: past 64 streams the cache is flushed
-// after a device synchronisation.
-void* ks_scratch(cudaStream_t s, size_t bytes) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    unsigned long long sid = 0;
-    if (cudaStreamGetId(s, &sid) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    static std::mutex m;
-    static std::map<std::pair<int, unsigned long long>, std::pair<void*, size_t>> cache;
-    std::lock_guard<std::mutex> lock(m);
-    if (cache.size() > 64) {
-        cudaDeviceSynchronize();
-        for (auto& kv : cache) cudaFree(kv.second.first);
-        cache.clear();
-    }
-    auto& e = cache[{dev, sid}];
-    if (e.second < bytes) {
-        if (e.first) cudaFreeAsync(e.first, s);
-        keep_pool();
-        e = {nullptr, 0};
-        void* p = nullptr;
-        if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
-        e = {p, bytes};
-    }
-    return e.first;
-}
-
 }  // namespace se
 
 using namespace se;
@@ -292,6 +243,7 @@ static int fused_checks(const se_geom* g, const uint8_t* key, const uint8_t* iv,
     int rc = fragment_layout(g, &lay);
     if (rc) return rc;
     if (!key || !iv) return SE_EINVAL;
+    if (lay.n_blocks > kMaxBlocks) return SE_EINVAL;          // 2^32 blocks (256 GiB) per call
     if ((g->block_offset * lay.a_bits) % 128) return SE_EINVAL;
     // FULL mode transforms the whole matrix: a stripe would need its
     // neighbours' halo rows, which this entry point does not take.
@@ -309,41 +261,28 @@ static DwtParams dwt_params(const se_geom* g, const se_layout& lay) {
 }
 
 
-// Row a6, keystream half: AES-128-CTR keystream of the whole A stream
-// (counter base p.ctr) written to `out`; the fused kernel that follows is
-// launched with programmatic stream serialization and XORs it in.
-static int launch_keystream(const FusedParams& p, uint8_t* out, uint64_t n, void* stream,
-                            se_report* init_report = nullptr, bool narrow = false) {
-    CipherParams cp;
-    memset(&cp, 0, sizeof cp);
-    cp.in = nullptr;
-    cp.out = out;
-    cp.n = n;
-    cp.narrow = narrow;
-    cp.report = init_report;
-    memcpy(cp.ctr, p.ctr, sizeof cp.ctr);
-    memcpy(cp.rk, p.rk, sizeof cp.rk);
-    return launch_cipher_ctr(cp, stream);
-}
-
-// FULL mode needs an R x W int16 coefficient workspace between the transform
-// and the footprint kernels; it comes from the stream-ordered pool
-// (cudaMallocAsync / cudaFreeAsync on the caller's stream: no device sync).
-static int16_t* ws_alloc(const se_layout& lay, uint32_t width, cudaStream_t s) {
-    void* ws = nullptr;
-    if (cudaMallocAsync(&ws, lay.rows * width * sizeof(int16_t), s) != cudaSuccess) return nullptr;
-    return (int16_t*)ws;
-}
-
 }  // extern "C"
 
 namespace se {
 
-// fragment_protect with an optional device keystream scratch d_ks (>= a_bytes
-// + 16): the keystream goes there and is XORed in on the way out, so A' is
-// written once (used when A' lives in mapped host memory).
+// FULL mode: the R x W int16 Mallat coefficients between the transform and
+// the footprint kernels live in the caller's workspace.
+static uint64_t full_ws_bytes(uint64_t rows, uint32_t width) { return rows * width * sizeof(int16_t); }
+
+static int report_init(se_report* r, cudaStream_t s) {
+    if (cudaMemsetAsync(&r->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
+        cudaMemsetAsync(&r->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
+        return SE_ECUDA;
+    return SE_OK;
+}
+
+// Protect (rows a1-a9).  BLOCK8 device buffers: the persistent tile kernel
+// (k_tile.cu).  BLOCK8 with o.mapped (fragments in page-locked host memory,
+// se_host.cu): the per-CTA kernel, whose plain stores suit PCIe writes.
+// FULL: whole-matrix transform into o.ws, then the footprint kernel.  AES-CTR
+// of the A slice runs inside the fused kernels in every case.
 int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in, void* d_a,
-                 void* d_b, void* d_c, void* d_ks, void* stream) {
+                 void* d_b, void* d_c, const ImplOpts& o, void* stream) {
     se_layout lay;
     int rc = fused_checks(g, key, iv, lay);
     if (rc) return rc;
@@ -354,96 +293,58 @@ int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     fill_fused(p, g, lay, key, iv);
     p.in = (const uint8_t*)d_in;
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
-    p.ks = (const uint8_t*)d_ks;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
-        if (!(SE_PROT_FUSED_AES && !mask) &&
-            launch_keystream(p, d_ks ? (uint8_t*)d_ks : p.a, lay.a_bytes, stream, nullptr, mask))
-            return SE_ECUDA;
-        return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
+        const int e = o.mapped ? launch_protect_block8(p, g->levels, mask, stream)
+                               : launch_tile_block8(p, g->levels, mask, false, stream);
+        return e ? SE_ECUDA : SE_OK;
     }
-    if (d_ks) return SE_ENOTSUP;
-    keep_pool();
-    cudaStream_t s = (cudaStream_t)stream;
-    int16_t* ws = ws_alloc(lay, g->width, s);
-    if (!ws) return SE_ECUDA;
+    if (!o.ws || o.ws_bytes < full_ws_bytes(lay.rows, g->width)) return SE_EINVAL;
+    if (!aligned16(o.ws)) return SE_EALIGN;
+    int16_t* ws = (int16_t*)o.ws;
     DwtParams dp = dwt_params(g, lay);
     dp.in = p.in; dp.coef = ws;
     p.ws = ws; p.rows = lay.rows;
     int e = launch_dwt_full_fwd(dp, g->levels, stream);
-    if (!e && !(SE_PROT_FUSED_AES && !mask)) e = launch_keystream(p, p.a, lay.a_bytes, stream);
     if (!e) e = launch_protect_full(p, g->levels, mask, stream);
-    cudaFreeAsync(ws, s);
     return e ? SE_ECUDA : SE_OK;
 }
 
-}  // namespace se
-
-extern "C" {
-
-int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in,
-                     void* d_a, void* d_b, void* d_c, void* stream) {
-    return protect_impl(g, key, iv, d_in, d_a, d_b, d_c, nullptr, stream);
-}
-
-}  // extern "C"
-
-namespace se {
-
-// fragment_recover with an optional caller-provided keystream scratch
-// (>= a_bytes + 16 device bytes; the host-streaming path passes its slot
-// buffer) and an optional already-initialised report (report_ready).
+// Recover (row a10), the mirror of protect_impl.  The report is set to
+// {-1, 0} here unless o.report_ready.
 int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a, const void* d_b,
-                 const void* d_c, void* d_out, se_report* d_report, void* d_ks, bool report_ready, void* stream) {
+                 const void* d_c, void* d_out, se_report* d_report, const ImplOpts& o, void* stream) {
     se_layout lay;
     int rc = fused_checks(g, key, iv, lay);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    const bool plain_fused = SE_REC_FUSED_AES && (g->flags & SE_FLAG_PUBLIC_PLAIN) && g->mode == SE_MODE_BLOCK8;
-    // the report ({-1, 0}) is initialised by the keystream kernel in the masked
-    // BLOCK8 path (one fewer stream operation); elsewhere by memsets
-    const bool init_in_ks = d_report && !report_ready && g->n_bytes && g->mode == SE_MODE_BLOCK8 && !plain_fused;
-    if (d_report && !report_ready && !init_in_ks) {
-        if (cudaMemsetAsync(&d_report->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
-            cudaMemsetAsync(&d_report->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
-            return SE_ECUDA;
+    if (g->n_bytes != 0) {
+        if (!d_out || !d_a || !d_c || (lay.b_bytes && !d_b)) return SE_EINVAL;
+        if (!aligned16(d_out) || !aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
+        if (g->mode == SE_MODE_FULL) {
+            if (!o.ws || o.ws_bytes < full_ws_bytes(lay.rows, g->width)) return SE_EINVAL;
+            if (!aligned16(o.ws)) return SE_EALIGN;
+        }
     }
+    if (d_report && !o.report_ready && report_init(d_report, s)) return SE_ECUDA;
     if (g->n_bytes == 0) return SE_OK;
-    if (!d_out || !d_a || !d_c || (lay.b_bytes && !d_b)) return SE_EINVAL;
-    if (!aligned16(d_out) || !aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
     FusedParams p;
     fill_fused(p, g, lay, key, iv);
     p.out = (uint8_t*)d_out;
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     p.report = d_report;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
-    if (SE_REC_FUSED_AES && !mask && g->mode == SE_MODE_BLOCK8)   // AES inside the kernel (fused_cta.cuh)
-        return launch_recover_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
-    // keystream scratch (a_bytes, 7.8% of n at L = 2): the caller's, else the stream-ordered pool
-    void* ks = d_ks ? d_ks : ks_scratch(s, lay.a_bytes + 16);
-    if (!ks) return SE_ECUDA;
-    d_ks = ks;                                    // cached per stream: nothing to free below
-    p.ks = (const uint8_t*)ks;
-    int e = (!mask && SE_REC_FUSED_AES) ? 0
-          : launch_keystream(p, (uint8_t*)ks, lay.a_bytes, stream, init_in_ks ? d_report : nullptr);
     if (g->mode == SE_MODE_BLOCK8) {
-        if (!e) e = launch_recover_block8(p, g->levels, mask, stream);
-        if (!d_ks) cudaFreeAsync(ks, s);
+        const int e = o.mapped ? launch_recover_block8(p, g->levels, mask, stream)
+                               : launch_tile_block8(p, g->levels, mask, true, stream);
         return e ? SE_ECUDA : SE_OK;
     }
-    keep_pool();
-    int16_t* ws = e ? nullptr : ws_alloc(lay, g->width, s);
-    if (!ws) {
-        if (!d_ks) cudaFreeAsync(ks, s);
-        return SE_ECUDA;
-    }
+    int16_t* ws = (int16_t*)o.ws;
     p.ws = ws; p.rows = lay.rows;
     DwtParams dp = dwt_params(g, lay);
     dp.out = p.out; dp.coef = ws;
-    e = launch_recover_full(p, g->levels, mask, stream);                      // unmask + scatter
-    if (!e) e = launch_dwt_full_inv(dp, g->levels, d_report, stream);         // inverse + report
-    cudaFreeAsync(ws, s);
-    if (!d_ks) cudaFreeAsync(ks, s);
+    int e = launch_recover_full(p, g->levels, mask, stream);                   // unmask + scatter
+    if (!e) e = launch_dwt_full_inv(dp, g->levels, d_report, stream);          // inverse + report
     return e ? SE_ECUDA : SE_OK;
 }
 
@@ -451,9 +352,49 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
 
 extern "C" {
 
+int fragment_workspace_size(const se_geom* g, const se_stripe* st, uint64_t* bytes) {
+    if (!bytes) return SE_EINVAL;
+    se_layout lay;
+    int rc = fragment_layout(g, &lay);
+    if (rc) return rc;
+    *bytes = 0;
+    if (g->mode != SE_MODE_FULL) return SE_OK;
+    if (!st) {
+        *bytes = full_ws_bytes(lay.rows, g->width);
+        return SE_OK;
+    }
+    // stripes: the larger of the protect window (the stripe's rows) and the
+    // recover window (its fragment block rows, halos included)
+    const uint64_t rows = std::max(st->row_end > st->row_begin ? st->row_end - st->row_begin : 0, st->src_rows);
+    *bytes = full_ws_bytes(rows, g->width);
+    return SE_OK;
+}
+
+int fragment_protect_ws(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in, void* d_a,
+                        void* d_b, void* d_c, void* d_ws, uint64_t ws_bytes, void* stream) {
+    ImplOpts o;
+    o.ws = d_ws;
+    o.ws_bytes = ws_bytes;
+    return protect_impl(g, key, iv, d_in, d_a, d_b, d_c, o, stream);
+}
+
+int fragment_recover_ws(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
+                        const void* d_b, const void* d_c, void* d_out, se_report* d_report, void* d_ws,
+                        uint64_t ws_bytes, void* stream) {
+    ImplOpts o;
+    o.ws = d_ws;
+    o.ws_bytes = ws_bytes;
+    return recover_impl(g, key, iv, d_a, d_b, d_c, d_out, d_report, o, stream);
+}
+
+int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in,
+                     void* d_a, void* d_b, void* d_c, void* stream) {
+    return protect_impl(g, key, iv, d_in, d_a, d_b, d_c, ImplOpts(), stream);
+}
+
 int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
                      const void* d_b, const void* d_c, void* d_out, se_report* d_report, void* stream) {
-    return recover_impl(g, key, iv, d_a, d_b, d_c, d_out, d_report, nullptr, false, stream);
+    return recover_impl(g, key, iv, d_a, d_b, d_c, d_out, d_report, ImplOpts(), stream);
 }
 
 // ---------------------------------------------------------------- FULL-mode stripes (row e for a11)
@@ -507,71 +448,53 @@ static void stripe_fused(FusedParams& p, const se_geom* g, const se_layout& lay,
 extern "C" {
 
 int fragment_protect_stripe(const se_geom* g, const se_stripe* st, const uint8_t key[16], const uint8_t iv[16],
-                            const void* d_in, void* d_a, void* d_b, void* d_c, void* stream) {
+                            const void* d_in, void* d_a, void* d_b, void* d_c, void* d_ws, uint64_t ws_bytes,
+                            void* stream) {
     se_layout lay;
     int rc = stripe_checks(g, st, key, iv, lay, false);
     if (rc) return rc;
     if (!d_in || !d_a || !d_c || (lay.b_bits && !d_b)) return SE_EINVAL;
     if (!aligned16(d_in) || !aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
+    if (!d_ws || ws_bytes < full_ws_bytes(st->row_end - st->row_begin, g->width)) return SE_EINVAL;
+    if (!aligned16(d_ws)) return SE_EALIGN;
     FusedParams p;
     stripe_fused(p, g, lay, key, iv, st->row_begin, st->row_end);
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
-    keep_pool();
-    cudaStream_t s = (cudaStream_t)stream;
-    void* ws = nullptr;
-    if (cudaMallocAsync(&ws, (st->row_end - st->row_begin) * g->width * sizeof(int16_t), s) != cudaSuccess)
-        return SE_ECUDA;
     DwtParams dp = dwt_params(g, lay);
-    dp.in = (const uint8_t*)d_in; dp.coef = (int16_t*)ws;
+    dp.in = (const uint8_t*)d_in; dp.coef = (int16_t*)d_ws;
     dp.row0 = st->row_begin; dp.rows_out = st->row_end - st->row_begin;
     dp.src_row0 = st->src_row0; dp.src_rows = st->src_rows;
-    p.ws = (int16_t*)ws;
+    p.ws = (int16_t*)d_ws;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     int e = launch_dwt_full_fwd(dp, g->levels, stream);
-    if (!e && !(SE_PROT_FUSED_AES && !mask)) e = launch_keystream(p, p.a, p.a_bytes, stream);
     if (!e) e = launch_protect_full(p, g->levels, mask, stream);
-    cudaFreeAsync(ws, s);
     return e ? SE_ECUDA : SE_OK;
 }
 
 int fragment_recover_stripe(const se_geom* g, const se_stripe* st, const uint8_t key[16], const uint8_t iv[16],
                             const void* d_a, const void* d_b, const void* d_c, void* d_out, se_report* d_report,
-                            void* stream) {
+                            void* d_ws, uint64_t ws_bytes, void* stream) {
     se_layout lay;
     int rc = stripe_checks(g, st, key, iv, lay, true);
     if (rc) return rc;
     if (!d_a || !d_c || !d_out || (lay.b_bits && !d_b)) return SE_EINVAL;
     if (!aligned16(d_a) || !aligned16(d_c) || (d_b && !aligned16(d_b))) return SE_EALIGN;
-    cudaStream_t s = (cudaStream_t)stream;
-    if (d_report) {
-        if (cudaMemsetAsync(&d_report->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
-            cudaMemsetAsync(&d_report->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
-            return SE_ECUDA;
-    }
     const uint64_t e0 = st->src_row0, e1 = st->src_row0 + st->src_rows;
+    if (!d_ws || ws_bytes < full_ws_bytes(e1 - e0, g->width)) return SE_EINVAL;
+    if (!aligned16(d_ws)) return SE_EALIGN;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (d_report && report_init(d_report, s)) return SE_ECUDA;
     FusedParams p;
     stripe_fused(p, g, lay, key, iv, e0, e1);                              // the halo-extended block rows
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
-    keep_pool();
-    void* ks = nullptr;
-    void* ws = nullptr;
-    if (cudaMallocAsync(&ks, p.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
-    if (cudaMallocAsync(&ws, (e1 - e0) * g->width * sizeof(int16_t), s) != cudaSuccess) {
-        cudaFreeAsync(ks, s);
-        return SE_ECUDA;
-    }
-    p.ks = (const uint8_t*)ks;
-    p.ws = (int16_t*)ws;
+    p.ws = (int16_t*)d_ws;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     DwtParams dp = dwt_params(g, lay);
-    dp.out = (uint8_t*)d_out; dp.coef = (int16_t*)ws;
+    dp.out = (uint8_t*)d_out; dp.coef = (int16_t*)d_ws;
     dp.row0 = st->row_begin; dp.rows_out = st->row_end - st->row_begin;
     dp.src_row0 = e0; dp.src_rows = e1 - e0;
-    int e = (!mask && SE_REC_FUSED_AES) ? 0 : launch_keystream(p, (uint8_t*)ks, p.a_bytes, stream);
-    if (!e) e = launch_recover_full(p, g->levels, mask, stream);             // unmask + scatter (halo too)
-    if (!e) e = launch_dwt_full_inv(dp, g->levels, d_report, stream);        // the stripe's rows
-    cudaFreeAsync(ws, s);
-    cudaFreeAsync(ks, s);
+    int e = launch_recover_full(p, g->levels, mask, stream);              // unmask + scatter (halo too)
+    if (!e) e = launch_dwt_full_inv(dp, g->levels, d_report, stream);     // the stripe's rows
     return e ? SE_ECUDA : SE_OK;
 }
 
@@ -679,18 +602,8 @@ static int batch_common(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ct
     fill_fused(bp.base, &g, lay, key, zero_iv);       // shared fields: round keys, H(0), one
     bp.total_ctas = total_ctas;
     const bool mask = !(flags & SE_FLAG_PUBLIC_PLAIN);
-    cudaStream_t s = (cudaStream_t)stream;
-    void* ks = nullptr;
-    const bool aes_inside = !mask && (recover ? SE_REC_FUSED_AES : SE_PROT_FUSED_AES);   // unmasked: in-kernel AES
-    if (recover && total_ctas && !aes_inside) {       // keystream scratch for every file's A stream
-        keep_pool();
-        if (cudaMallocAsync(&ks, total_ctas * 16ull * lay.a_bits + 16, s) != cudaSuccess) return SE_ECUDA;
-        bp.ks = (uint8_t*)ks;
-    }
-    int e = (total_ctas && !aes_inside) ? launch_batch_keystream(bp, lay.a_bits, stream) : 0;
-    if (!e) e = launch_batch_block8(bp, total_ctas, levels, mask, recover, stream);
-    if (ks) cudaFreeAsync(ks, s);
-    return e ? SE_ECUDA : SE_OK;
+    // AES-CTR of every file's A slices runs inside the batch kernel: no keystream scratch
+    return launch_batch_block8(bp, total_ctas, levels, mask, recover, stream) ? SE_ECUDA : SE_OK;
 }
 
 int fragment_protect_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas, uint32_t levels,

@@ -107,17 +107,8 @@ int dct_recover(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
         dct_sched_consts(p, (g->flags & SE_DCT_KEYED) != 0);
     }
     aes_params(p, key, iv, g);
-    if (dct_fused_aes(1, g->level))
-        return launch_dct(p, g->channels, g->level, (g->flags & SE_DCT_KEYED) != 0, 1, stream) ? SE_ECUDA : SE_OK;
-    keep_pool();
-    cudaStream_t s = (cudaStream_t)stream;
-    void* ks = nullptr;
-    if (cudaMallocAsync(&ks, lay.a_bytes + 16, s) != cudaSuccess) return SE_ECUDA;
-    p.ks = (const uint8_t*)ks;
-    int e = launch_ks(key, iv, g, (uint8_t*)ks, lay.a_bytes, stream);
-    if (!e) e = launch_dct(p, g->channels, g->level, (g->flags & SE_DCT_KEYED) != 0, 1, stream);
-    cudaFreeAsync(ks, s);
-    return e ? SE_ECUDA : SE_OK;
+    // recovery always decrypts Fragment 1 inside the kernel: no keystream scratch
+    return launch_dct(p, g->channels, g->level, (g->flags & SE_DCT_KEYED) != 0, 1, stream) ? SE_ECUDA : SE_OK;
 }
 
 int dct_select(const se_dct_geom* g, const void* d_in, float* d_coef, void* stream) {

@@ -342,10 +342,9 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
         HostCtx& ctx = host_ctx(dev);
         std::lock_guard<std::mutex> lock(ctx.mu);
         if (ensure(ctx, 1)) return SE_ECUDA;
-        Slot& sl = ctx.slots[0];
-        if (lay.a_bytes + 16 > sl.cap[4]) cudaStreamSynchronize(ctx.streams[0]);
-        if (grow(sl.buf[4], sl.cap[4], lay.a_bytes + 16, ctx)) return SE_ECUDA;   // keystream scratch
-        int st = protect_impl(&g2, key, iv, din, da, db, dc, sl.buf[4], ctx.streams[0]);
+        ImplOpts o;
+        o.mapped = true;
+        int st = protect_impl(&g2, key, iv, din, da, db, dc, o, ctx.streams[0]);
         if (cudaStreamSynchronize(ctx.streams[0]) != cudaSuccess) st = SE_ECUDA;
         return st;
     }
@@ -378,9 +377,10 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
         cgs[k].n_bytes = c.byte1 - c.byte0;
         cgs[k].block_offset = g->block_offset + c.blk0;
         fragment_layout(&cgs[k], &cls[k]);
-        // staged: input + three fragment slices; hybrid: input + keystream scratch
+        // staged: input + three fragment slices (+ FULL mode: the coefficient workspace); hybrid: input
+        const uint64_t ws = g->mode == SE_MODE_FULL ? cls[k].rows * g->width * sizeof(int16_t) : 0;
         const uint64_t sizes[5] = {cgs[k].n_bytes, hybrid ? 0 : cls[k].a_bytes, hybrid ? 0 : cls[k].b_bytes,
-                                   hybrid ? 0 : cls[k].c_bytes, hybrid ? cls[k].a_bytes : 0};
+                                   hybrid ? 0 : cls[k].c_bytes, ws};
         for (int i = 0; i < 5; ++i) {
             if (!sizes[i] && i) continue;
             if (sizes[i] + 16 > sl.cap[i]) cudaStreamSynchronize(ctx.streams[k % n_streams]);
@@ -399,8 +399,9 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
                     return SE_ECUDA;
                 uint8_t* d[3];
                 for (int i = 0; i < 3; ++i) d[i] = dmap[i] ? (uint8_t*)dmap[i] + c.blk0 * bits[i] / 8 : nullptr;
-                int st = protect_impl(&cgs[k], key, iv, sl.buf[0], d[0], cls[k].b_bytes ? d[1] : nullptr, d[2],
-                                      sl.buf[4], s);
+                ImplOpts o;
+                o.mapped = true;
+                int st = protect_impl(&cgs[k], key, iv, sl.buf[0], d[0], cls[k].b_bytes ? d[1] : nullptr, d[2], o, s);
                 if (st) return st;
             }
             return SE_OK;
@@ -414,8 +415,11 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
             if (cudaMemcpyAsync(sl.buf[0], (const uint8_t*)h_in + c.byte0, sizes[0], cudaMemcpyHostToDevice, s) !=
                 cudaSuccess)
                 return SE_ECUDA;
-            int st = fragment_protect(&cgs[k], key, iv, sl.buf[0], sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr,
-                                      sl.buf[3], s);
+            ImplOpts o;
+            o.ws = sl.buf[4];
+            o.ws_bytes = sl.cap[4];
+            int st = protect_impl(&cgs[k], key, iv, sl.buf[0], sl.buf[1], cl.b_bytes ? sl.buf[2] : nullptr,
+                                  sl.buf[3], o, s);
             if (st) return st;
             for (int i = 0; i < 3; ++i)
                 if (sizes[i + 1] && cudaMemcpyAsync(hout[i] + c.blk0 * bits[i] / 8, sl.buf[i + 1], sizes[i + 1],
@@ -460,11 +464,10 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
             ctx.hinit[0].bad_blocks = 0;
             ctx.reps_cap = 1;
         }
-        Slot& sl = ctx.slots[0];
-        if (lay.a_bytes + 16 > sl.cap[4]) cudaStreamSynchronize(ctx.streams[0]);
-        if (grow(sl.buf[4], sl.cap[4], lay.a_bytes + 16, ctx)) return SE_ECUDA;
         cudaStream_t s0 = ctx.streams[0];
-        int st = recover_impl(&g2, key, iv, da, db, dc, dout, ctx.reps, sl.buf[4], false, s0);
+        ImplOpts o;
+        o.mapped = true;
+        int st = recover_impl(&g2, key, iv, da, db, dc, dout, ctx.reps, o, s0);
         if (st == SE_OK &&
             cudaMemcpyAsync(ctx.hreps, ctx.reps, sizeof(se_report), cudaMemcpyDeviceToHost, s0) != cudaSuccess)
             st = SE_ECUDA;
@@ -517,8 +520,10 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
         cgs[k].n_bytes = c.byte1 - c.byte0;
         cgs[k].block_offset = g->block_offset + c.blk0;
         fragment_layout(&cgs[k], &cls[k]);
-        const uint64_t sizes[5] = {cgs[k].n_bytes, cls[k].a_bytes, cls[k].b_bytes, cls[k].c_bytes, cls[k].a_bytes};
+        const uint64_t ws = g->mode == SE_MODE_FULL ? cls[k].rows * g->width * sizeof(int16_t) : 0;
+        const uint64_t sizes[5] = {cgs[k].n_bytes, cls[k].a_bytes, cls[k].b_bytes, cls[k].c_bytes, ws};
         for (int i = 0; i < 5; ++i) {
+            if (i == 4 && !sizes[i]) continue;
             if (sizes[i] + 16 > sl.cap[i]) cudaStreamSynchronize(ctx.streams[k % n_streams]);
             if (grow(sl.buf[i], sl.cap[i], sizes[i] + 16, ctx)) return SE_ECUDA;
         }
@@ -540,11 +545,14 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
                     return SE_ECUDA;
                 }
             }
-            // report_ready = false: the chunk's report is initialised by its keystream kernel
-            // (or memsets on the unmasked path) - no host-to-device copy per chunk
+            // the chunk's report is initialised by recover_impl (two memsets)
             uint8_t* dst = hybrid ? (uint8_t*)dout + c.byte0 : (uint8_t*)sl.buf[0];
+            ImplOpts o;
+            o.mapped = hybrid || zin;          // host-mapped buffers: the per-CTA kernels' plain accesses
+            o.ws = sl.buf[4];
+            o.ws_bytes = sl.cap[4];
             int st = recover_impl(&cgs[k], key, iv, src[0], cl.b_bytes ? src[1] : nullptr, src[2],
-                                  dst, ctx.reps + k, sl.buf[4], false, s);
+                                  dst, ctx.reps + k, o, s);
             if (st) return st;
             if ((!hybrid && cudaMemcpyAsync((uint8_t*)h_out + c.byte0, sl.buf[0], sizes[0], cudaMemcpyDeviceToHost,
                                             s) != cudaSuccess) ||

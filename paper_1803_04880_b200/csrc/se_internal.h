@@ -11,14 +11,6 @@ namespace se {
 
 constexpr int kBlocksPerCta = 128;   // one thread per 8x8 block, 128 blocks per CTA
 
-#ifndef SE_PROT_FUSED_AES
-#define SE_PROT_FUSED_AES 0  // unmasked protect: AES of the A slice inside the fused kernel
-#endif
-#ifndef SE_REC_FUSED_AES
-#define SE_REC_FUSED_AES 1   // unmasked recover: AES of the A slice inside the fused kernel (measured:
-                             // C2 plain recover 489 -> 532 GB/s; masked recover keeps the keystream
-                             // kernel, 175 vs 171.5 with the AES inside)
-#endif
 
 // ---- message-schedule specialisation of the B / C mask hashes (sha2_spec.cuh)
 // bit t set: schedule word W_t depends on the block (t < 64)
@@ -63,12 +55,13 @@ struct FusedParams {
     uint8_t* c;               // C' stream
     se_report* report;        // recover only, nullable
     int16_t* ws;              // FULL mode: R x W Mallat coefficient workspace
-    const uint8_t* ks;        // recover: AES-CTR keystream of the A stream (scratch)
     uint64_t rows;            // R (FULL mode)
     uint64_t n_bytes;
     uint64_t n_blocks;
     uint64_t block_offset;    // global index of local block 0 (hash nonce, C16)
     uint64_t a_bytes, b_bytes, c_bytes;
+    uint64_t n_tiles;         // k_tile.cu: tiles of the launch
+    uint64_t fast_tiles;      // k_tile.cu: leading tiles moved by bulk copies (the rest: per-thread path)
     uint32_t width;
     uint32_t bpr;             // 8x8 blocks per block-row = width / 8
     uint32_t one;             // = 1, opaque to ptxas: adds become IMADs (sha2_device.cuh)
@@ -96,7 +89,6 @@ static_assert(sizeof(JobDerived) <= sizeof(((se_job*)0)->derived), "se_job.deriv
 struct BatchParams {
     const se_job* jobs;       // device array, sorted by cta_begin
     se_report* reports;       // recover: one per job, nullable
-    uint8_t* ks;              // recover: keystream scratch, file j at cta_begin_j*16*a_bits
     uint64_t total_ctas;
     uint32_t n_jobs;
     uint32_t pad_;
@@ -167,19 +159,26 @@ void dct_sched_consts(DctParams& p, bool keyed);
 // host helpers shared by the API translation units (se_api.cu)
 void cipher_setup(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block, CipherParams& cp);
 void sha512_kiv(const uint8_t key[16], const uint8_t iv[16], uint32_t kiv[8], uint64_t mid[8], uint64_t h0[8]);
-void keep_pool();
-void* ks_scratch(cudaStream_t s, size_t bytes);     // per-stream cached recovery keystream scratch
+// options of the shared protect / recover implementation (se_api.cu)
+struct ImplOpts {
+    bool mapped = false;          // BLOCK8 buffers in page-locked host memory (se_host.cu): per-CTA kernels
+    bool report_ready = false;    // recover: the report is already {-1, 0}
+    void* ws = nullptr;           // FULL mode: caller workspace (fragment_workspace_size)
+    uint64_t ws_bytes = 0;
+};
+constexpr uint64_t kMaxBlocks = 1ull << 32;     // 8x8 blocks per call (256 GiB)
 int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in, void* d_a,
-                 void* d_b, void* d_c, void* d_ks, void* stream);
+                 void* d_b, void* d_c, const ImplOpts& o, void* stream);
 int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a, const void* d_b,
-                 const void* d_c, void* d_out, se_report* d_report, void* d_ks, bool report_ready, void* stream);
+                 const void* d_c, void* d_out, se_report* d_report, const ImplOpts& o, void* stream);
 
 // launchers (return cudaError_t as int)
 int launch_protect_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
 int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void* stream);
+// persistent warp-specialised single-file kernels (k_tile.cu)
+int launch_tile_block8(const FusedParams& p, uint32_t levels, bool mask, bool recover, void* stream);
 int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,
                         void* stream);
-int launch_batch_keystream(const BatchParams& bp, uint32_t a_bits, void* stream);
 int launch_dwt_fwd_block8(const DwtParams& p, uint32_t levels, void* stream);
 // FULL mode (row a11): whole-matrix transform kernels and the footprint CTA kernels
 int launch_dwt_full_fwd(const DwtParams& p, uint32_t levels, void* stream);

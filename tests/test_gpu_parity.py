@@ -138,7 +138,7 @@ def test_launch_evidence(dev):
     a, b, c = se.fragment_protect(x, 256, 2, KEY, IV)
     se.fragment_recover(a, b, c, x.numel(), 256, 2, KEY, IV)
     torch.cuda.synchronize()
-    assert se.launch_count() == 4           # AES-CTR keystream + fused kernel, per direction
+    assert se.launch_count() == 2           # one fused kernel per direction (AES-CTR inside)
 
 
 # ---------------------------------------------------------------- full-size configs
