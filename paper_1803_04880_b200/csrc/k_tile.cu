@@ -33,12 +33,17 @@
 
 namespace se {
 
-template <int L>
+// TILE: masked kernels (ALU-bound on SHA-2) 512 blocks = 16 consumer warps;
+// PUBLIC_PLAIN kernels (issue-bound) 384 blocks = 12 consumer warps, so the
+// tile's 120 AES blocks (L = 2) are one pass of the 4 AES warps and keep
+// ahead of the consumers (at 512, the 160-block second pass on one warp fell
+// behind: consumers spun ~100 mbarrier polls per tile waiting for keystream).
+template <int L, bool MASK>
 struct TileCfg {
     using R = Rec<L>;
-    static constexpr int TILE = (L == 1) ? 256 : 512;
+    static constexpr int TILE = (L == 1) ? 256 : MASK ? 512 : 384;
     static constexpr int NCW = TILE / 32;
-    static constexpr int NAW = 4;      // 20 warps = 5 per SM sub-partition: 96 registers per thread
+    static constexpr int NAW = 4;      // masked: 20 warps = 5 per SM sub-partition: 96 registers per thread
     static constexpr int NC = 32 * NCW;
     static constexpr int NT = 32 * (NCW + NAW);
     static constexpr int A_BYTES = TILE * R::ABITS / 8;
@@ -110,12 +115,10 @@ __device__ __forceinline__ void named_bar() { asm volatile("bar.sync 1, %0;" ::"
 // one bulk copy per (block-row run, pixel row).
 struct TileMap {
     bool contig;
-    __device__ __forceinline__ uint32_t base(const FusedParams& p, uint64_t t, uint32_t u, int tile) const {
-        if (contig) {
-            const uint64_t b = t * tile + u;
-            const uint64_t brl = b / p.bpr - (t * tile) / p.bpr, bc = b % p.bpr;
-            return (uint32_t)(8 * brl * p.width + 8 * bc);
-        }
+    // contiguous: u = brl * bpr + bc -> 8W*brl + 8bc = 8u + 7W*brl, brl = u / bpr
+    // by multiply-shift (p.bpr_magic = ceil(2^20 / bpr), exact for u < 2^10)
+    __device__ __forceinline__ uint32_t base(const FusedParams& p, uint64_t, uint32_t u, int) const {
+        if (contig) return 8u * u + 7u * p.width * ((u * p.bpr_magic) >> 20);
         return 8u * u;
     }
     __device__ __forceinline__ uint32_t stride(const FusedParams& p, int tile) const {
@@ -234,10 +237,10 @@ __device__ __forceinline__ void get_stream(const uint32_t* words, const uint32_t
 
 // ---------------------------------------------------------------- AES producer warps
 
-template <int L>
+template <int L, bool MASK>
 __device__ __forceinline__ void aes_producer(const FusedParams& p, const uint32_t* lut, uint8_t* ks_base,
                                              uint32_t ks_full, uint32_t ks_empty) {
-    using T = TileCfg<L>;
+    using T = TileCfg<L, MASK>;
     const AesLane al = aes_lane(lut);
     const int at = threadIdx.x - T::NC;                  // 0 .. 32*NAW-1
     uint32_t k = 0;
@@ -261,8 +264,8 @@ __device__ __forceinline__ void aes_producer(const FusedParams& p, const uint32_
 // ---------------------------------------------------------------- the kernel
 
 template <int L, bool MASK, bool RECOVER>
-__global__ void __launch_bounds__(TileCfg<L>::NT, 1) k_tile(const __grid_constant__ FusedParams p) {
-    using T = TileCfg<L>;
+__global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_constant__ FusedParams p) {
+    using T = TileCfg<L, MASK>;
     using R = Rec<L>;
     using S = typename T::template Smem<RECOVER>;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(TileCfg<L>::NT, 1) k_tile(const __grid_constan
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;");
     if (threadIdx.x >= T::NC) {                           // AES warps
-        aes_producer<L>(p, lut, smem + S::KS_OFF, ks_full, ks_empty);
+        aes_producer<L, MASK>(p, lut, smem + S::KS_OFF, ks_full, ks_empty);
         return;
     }
 
@@ -325,7 +328,6 @@ __global__ void __launch_bounds__(TileCfg<L>::NT, 1) k_tile(const __grid_constan
         const uint64_t blk = t * T::TILE + ct;
         const bool valid = blk < p.n_blocks;
         const uint64_t gb = p.block_offset + blk;
-        const uint64_t br = blk / p.bpr, bc = blk - br * p.bpr;
         if (fast) {
             mbar_wait(full + 8 * slot, (phase >> slot) & 1);
             phase ^= 1u << slot;
@@ -350,14 +352,22 @@ __global__ void __launch_bounds__(TileCfg<L>::NT, 1) k_tile(const __grid_constan
                         unpack4(q.y, v[i][4], v[i][5], v[i][6], v[i][7]);
                     }
                 } else {
+                    const uint64_t br = blk / p.bpr, bc = blk - br * p.bpr;
                     load_block(p.in, p.n_bytes, p.width, br, bc, v);
                 }
-                dwt8_fwd<L>(v, p.one);                                            // rows a2-a4
+                if (MASK) dwt8_fwd<L>(v, p.one);                                  // rows a2-a4 (adds on the FMA pipe)
+                else dwt8_fwd_lean<L>(v);                                         // rows a2-a4 (fewest instructions)
                 for_each_field<L, 0>([&](int s, int pos, int i, int j, int w) {     // row a5
                     const int off = (s == 0) ? (1 << (w - 1)) - 128 : (1 << (w - 1));   // C9 (+ C8 on LL)
-                    if (s == 0) put_field(A, pos, v[i][j], off, w, p.one);
-                    else if (s == 1) put_field(B, pos, v[i][j], off, w, p.one);
-                    else put_field(C, pos, v[i][j], off, w, p.one);
+                    if (MASK) {
+                        if (s == 0) put_field(A, pos, v[i][j], off, w, p.one);
+                        else if (s == 1) put_field(B, pos, v[i][j], off, w, p.one);
+                        else put_field(C, pos, v[i][j], off, w, p.one);
+                    } else {
+                        if (s == 0) put_field_lean(A, pos, v[i][j], off, w);
+                        else if (s == 1) put_field_lean(B, pos, v[i][j], off, w);
+                        else put_field_lean(C, pos, v[i][j], off, w);
+                    }
                 });
                 if (MASK) {
                     if (R::BBITS) {
@@ -405,13 +415,27 @@ __global__ void __launch_bounds__(TileCfg<L>::NT, 1) k_tile(const __grid_constan
                     else mask_c<R::AW, R::ABYTES>(p, gb, A, C);                   // C21 (L = 1)
                 }
                 int v[8][8];
-                for_each_field<L, 0>([&](int s, int pos, int i, int j, int w) {
-                    const int off = (s == 0) ? (1 << (w - 1)) - 128 : (1 << (w - 1));
-                    if (s == 0) v[i][j] = get_field(A, pos, off, w, p.one);
-                    else if (s == 1) v[i][j] = get_field(B, pos, off, w, p.one);
-                    else v[i][j] = get_field(C, pos, off, w, p.one);
-                });
-                dwt8_inv<L>(v, p.one);
+                if (MASK) {
+                    for_each_field<L, 0>([&](int s, int pos, int i, int j, int w) {
+                        const int off = (s == 0) ? (1 << (w - 1)) - 128 : (1 << (w - 1));
+                        if (s == 0) v[i][j] = get_field(A, pos, off, w, p.one);
+                        else if (s == 1) v[i][j] = get_field(B, pos, off, w, p.one);
+                        else v[i][j] = get_field(C, pos, off, w, p.one);
+                    });
+                    dwt8_inv<L>(v, p.one);
+                } else {
+                    for_each_field<L, 0>([&](int s, int pos, int, int, int) {
+                        if (s == 0) flip_top(A, pos);
+                        else if (s == 1) flip_top(B, pos);
+                        else flip_top(C, pos);
+                    });
+                    for_each_field<L, 0>([&](int s, int pos, int i, int j, int w) {
+                        if (s == 0) v[i][j] = get_field_lean(A, pos, w) + 128;       // LL: uncentered (C8)
+                        else if (s == 1) v[i][j] = get_field_lean(B, pos, w);
+                        else v[i][j] = get_field_lean(C, pos, w);
+                    });
+                    dwt8_inv_lean<L>(v);
+                }
                 int orv = 0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
@@ -428,6 +452,7 @@ __global__ void __launch_bounds__(TileCfg<L>::NT, 1) k_tile(const __grid_constan
                         *reinterpret_cast<uint2*>(out + base + i * st) = q;
                     }
                 } else {
+                    const uint64_t br = blk / p.bpr, bc = blk - br * p.bpr;
                     store_block(p.out, p.n_bytes, p.width, br, bc, v);
                 }
             }
@@ -494,7 +519,7 @@ static int sm_count() {
 
 template <int L, bool MASK, bool RECOVER>
 static void tile_l(FusedParams p, cudaStream_t s) {
-    using T = TileCfg<L>;
+    using T = TileCfg<L, MASK>;
     using S = typename T::template Smem<RECOVER>;
     static bool attr_set[64] = {false};
     int dev = 0;
@@ -515,6 +540,7 @@ static void tile_l(FusedParams p, cudaStream_t s) {
         }
     }
     p.fast_tiles = fast;
+    p.bpr_magic = (uint32_t)(((1u << 20) + p.bpr - 1) / p.bpr);
     const unsigned grid = (unsigned)std::min<uint64_t>(p.n_tiles, (uint64_t)sm_count());
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

@@ -7,6 +7,7 @@
 // caller's stream.  No device allocation, no synchronisation on the hot path:
 // FULL mode takes a caller-owned workspace (fragment_workspace_size).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -269,6 +270,16 @@ namespace se {
 // the footprint kernels live in the caller's workspace.
 static uint64_t full_ws_bytes(uint64_t rows, uint32_t width) { return rows * width * sizeof(int16_t); }
 
+// SE_KERNEL=cta (measurement knob): single-file BLOCK8 calls on the per-CTA
+// kernels instead of the persistent tile kernels.
+static bool cta_kernels() {
+    static const bool v = [] {
+        const char* e = getenv("SE_KERNEL");
+        return e && strcmp(e, "cta") == 0;
+    }();
+    return v;
+}
+
 static int report_init(se_report* r, cudaStream_t s) {
     if (cudaMemsetAsync(&r->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
         cudaMemsetAsync(&r->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
@@ -295,7 +306,7 @@ int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
-        const int e = o.mapped ? launch_protect_block8(p, g->levels, mask, stream)
+        const int e = (o.mapped || cta_kernels()) ? launch_protect_block8(p, g->levels, mask, stream)
                                : launch_tile_block8(p, g->levels, mask, false, stream);
         return e ? SE_ECUDA : SE_OK;
     }
@@ -335,7 +346,7 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     p.report = d_report;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
-        const int e = o.mapped ? launch_recover_block8(p, g->levels, mask, stream)
+        const int e = (o.mapped || cta_kernels()) ? launch_recover_block8(p, g->levels, mask, stream)
                                : launch_tile_block8(p, g->levels, mask, true, stream);
         return e ? SE_ECUDA : SE_OK;
     }

@@ -180,6 +180,77 @@ __device__ __forceinline__ void dwt8_inv(int (&v)[8][8], uint32_t one) {
     dwt2_level_inv<8>(v, one, m1);
 }
 
+// ------------------------------------------------------------------ lean lifting
+// The same transform written for issue-bound kernels (PUBLIC_PLAIN tile
+// kernels, k_tile.cu): plain integer adds, so ptxas fuses the three-operand
+// sums into IADD3 and each shift-and-add into one LEA.HI.
+//   predict  x_o - floor((x_l + x_r) / 2) = x_o + floor((1 - x_l - x_r) / 2)
+//   update   x_e + floor((d_l + d_r + 2) / 4)
+//   inverse  x_e = s + floor((1 - d_l - d_r) / 4)   (= s - floor((d_l + d_r + 2) / 4))
+//            x_o = d + floor((x_l + x_r) / 2)
+// (floor via the arithmetic shift; -floor(m / 2^k) = floor((2^k - 1 - m) / 2^k)).
+template <int N>
+__device__ __forceinline__ void lift_fwd_lean(int (&x)[N]) {
+    constexpr int H = N / 2;
+    int s[H], d[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k)
+        d[k] = (2 * k + 2 < N) ? x[2 * k + 1] + ((1 - x[2 * k] - x[2 * k + 2]) >> 1) : x[2 * k + 1] - x[2 * k];
+#pragma unroll
+    for (int k = 0; k < H; ++k) s[k] = x[2 * k] + (((k == 0 ? d[0] : d[k - 1]) + d[k] + 2) >> 2);
+#pragma unroll
+    for (int k = 0; k < H; ++k) { x[k] = s[k]; x[H + k] = d[k]; }
+}
+
+template <int N>
+__device__ __forceinline__ void lift_inv_lean(int (&y)[N]) {
+    constexpr int H = N / 2;
+    int x[N];
+#pragma unroll
+    for (int k = 0; k < H; ++k) x[2 * k] = y[k] + ((1 - (k == 0 ? y[H] : y[H + k - 1]) - y[H + k]) >> 2);
+#pragma unroll
+    for (int k = 0; k < H; ++k)
+        x[2 * k + 1] = (2 * k + 2 < N) ? y[H + k] + ((x[2 * k] + x[2 * k + 2]) >> 1) : y[H + k] + x[2 * k];
+#pragma unroll
+    for (int k = 0; k < N; ++k) y[k] = x[k];
+}
+
+template <int M, bool INV>
+__device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8]) {
+    // forward: rows then columns (C5); inverse: columns then rows
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool rows = (pass == 0) != INV;
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            int t[M];
+#pragma unroll
+            for (int b = 0; b < M; ++b) t[b] = rows ? v[a][b] : v[b][a];
+            if (INV) lift_inv_lean<M>(t);
+            else lift_fwd_lean<M>(t);
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                if (rows) v[a][b] = t[b];
+                else v[b][a] = t[b];
+            }
+        }
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void dwt8_fwd_lean(int (&v)[8][8]) {
+    dwt2_level_lean<8, false>(v);
+    if (L >= 2) dwt2_level_lean<4, false>(v);
+    if (L >= 3) dwt2_level_lean<2, false>(v);
+}
+
+template <int L>
+__device__ __forceinline__ void dwt8_inv_lean(int (&v)[8][8]) {
+    if (L >= 3) dwt2_level_lean<2, true>(v);
+    if (L >= 2) dwt2_level_lean<4, true>(v);
+    dwt2_level_lean<8, true>(v);
+}
+
 // ------------------------------------------------------------------ records
 template <int L, int MODE = 0>
 struct Rec {
@@ -232,6 +303,37 @@ __device__ __forceinline__ int get_field(const uint32_t (&r)[NW], int pos, int o
         v = isub((int)u, off, -(int)one);
     }
     return v;
+}
+
+// Lean field placement (issue-bound kernels): v + off placed with one
+// shift-add per field; the additions of constants chain and fold.
+template <int NW>
+__device__ __forceinline__ void put_field_lean(uint32_t (&r)[NW], int pos, int v, int off, int w) {
+    const int word = pos >> 5, end = (pos & 31) + w;
+    const uint32_t u = (uint32_t)(v + off);
+    if (end <= 32) {
+        r[word] += u << (32 - end);
+    } else {
+        r[word] += u >> (end - 32);
+        r[word + 1] += u << (64 - end);
+    }
+}
+
+// Lean field extraction: the caller has XORed every field's top bit in place
+// (flip_top), so each field is the sign-extended w-bit value v = u - 2^(w-1)
+// (offset binary, C9): one or two shifts.
+template <int NW>
+__device__ __forceinline__ int get_field_lean(const uint32_t (&r)[NW], int pos, int w) {
+    const int word = pos >> 5, start = pos & 31, end = start + w;
+    uint32_t top;
+    if (end <= 32) top = r[word] << start;
+    else top = __funnelshift_l(r[word + 1], r[word], start);
+    return (int)top >> (32 - w);
+}
+
+template <int NW>
+__device__ __forceinline__ void flip_top(uint32_t (&r)[NW], int pos) {
+    r[pos >> 5] ^= 0x80000000u >> (pos & 31);
 }
 
 // Visit every field of the three records in the canonical order (C10):

@@ -65,6 +65,7 @@ struct FusedParams {
     uint32_t width;
     uint32_t bpr;             // 8x8 blocks per block-row = width / 8
     uint32_t one;             // = 1, opaque to ptxas: adds become IMADs (sha2_device.cuh)
+    uint32_t bpr_magic;       // k_tile.cu: ceil(2^20 / bpr) (block row of a tile-local block)
     uint32_t ctr[4];          // IV + block_offset*a_bits/128, big-endian words
     uint32_t rk[44];          // AES-128 round keys, big-endian words
     uint32_t kiv[8];          // K || IV as big-endian words (SHA W0..W7)

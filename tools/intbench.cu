@@ -9,7 +9,7 @@
 #define CHAINS 8
 constexpr int ITERS = 4096;
 
-__device__ unsigned long long g_cycles[4096];
+__device__ unsigned long long g_cycles[3 * 4096];   // per CTA: SM id, start, end (clock64)
 
 template <int OP>
 __global__ void __launch_bounds__(256) k(uint32_t* out, uint32_t seed, uint32_t one) {
@@ -53,7 +53,13 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, uint32_t seed, uint32_t 
     for (int c = 0; c < CHAINS; ++c) r ^= x[c];
     out[blockIdx.x * blockDim.x + threadIdx.x] = r;
     __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x < 4096) g_cycles[blockIdx.x] = (unsigned long long)(clock64() - c0);
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_cycles[3 * blockIdx.x] = sm;
+        g_cycles[3 * blockIdx.x + 1] = (unsigned long long)c0;
+        g_cycles[3 * blockIdx.x + 2] = (unsigned long long)clock64();
+    }
 }
 
 template <int OP>
@@ -61,6 +67,7 @@ float run(uint32_t* d, int grid, const char* name, int sms, float ops_per_chain_
     k<OP><<<grid, 256>>>(d, 1, 1);
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int w = 0; w < 20; ++w) k<OP><<<grid, 256>>>(d, 1, 1);      // warm the clocks up
     cudaEventRecord(a);
     k<OP><<<grid, 256>>>(d, 1, 1);
     cudaEventRecord(b);
@@ -69,16 +76,26 @@ float run(uint32_t* d, int grid, const char* name, int sms, float ops_per_chain_
     cudaEventElapsedTime(&ms, a, b);
     int clk_khz;
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
-    static unsigned long long cyc[4096];
-    cudaMemcpyFromSymbol(cyc, g_cycles, sizeof(unsigned long long) * (grid < 4096 ? grid : 4096));
-    double mean_cyc = 0;
+    static unsigned long long cyc[3 * 4096];
     const int nc = grid < 4096 ? grid : 4096;
-    for (int i = 0; i < nc; ++i) mean_cyc += (double)cyc[i] / nc;
+    cudaMemcpyFromSymbol(cyc, g_cycles, sizeof(unsigned long long) * 3 * nc);
+    // per SM: its CTAs' lane ops over its busy window (first start .. last end,
+    // clock64 is the SM's own cycle counter); averaged over SMs
+    static unsigned long long lo[1024], hi[1024], cnt[1024];
+    for (int i = 0; i < 1024; ++i) { lo[i] = ~0ull; hi[i] = 0; cnt[i] = 0; }
+    for (int i = 0; i < nc; ++i) {
+        const unsigned sm = (unsigned)cyc[3 * i] & 1023u;
+        if (cyc[3 * i + 1] < lo[sm]) lo[sm] = cyc[3 * i + 1];
+        if (cyc[3 * i + 2] > hi[sm]) hi[sm] = cyc[3 * i + 2];
+        ++cnt[sm];
+    }
+    double sum_rate = 0;
+    int nsm = 0;
+    for (int i = 0; i < 1024; ++i)
+        if (cnt[i]) { sum_rate += (double)cnt[i] * 256 * ITERS * CHAINS * ops_per_chain_iter / (double)(hi[i] - lo[i]); ++nsm; }
     double lane_ops = (double)grid * 256 * ITERS * CHAINS * ops_per_chain_iter;
     double per_s = lane_ops / (ms / 1e3);
-    // all grid/sms CTAs of an SM are co-resident (8 x 256 threads), so the
-    // SM's lane ops per SM cycle = CTAs per SM x ops per CTA / CTA cycles
-    const double per_clk_sm = (double)(grid / sms) * 256 * ITERS * CHAINS * ops_per_chain_iter / mean_cyc;
+    const double per_clk_sm = sum_rate / nsm;
     printf("{\"op\": \"%s\", \"ms\": %.4f, \"Tlane_ops_per_s\": %.3f, \"lane_ops_per_clk_per_sm\": %.2f, "
            "\"lane_ops_per_clk_per_sm_at_max_clock\": %.2f, \"effective_mhz\": %.0f}\n",
            name, ms, per_s / 1e12, per_clk_sm, per_s / sms / (clk_khz * 1e3), per_s / sms / per_clk_sm / 1e6);
