@@ -264,6 +264,11 @@ const char* se_strerror(int status);
 /* Number of kernel launches issued by this thread since the last reset
  * (bench/test evidence of native launches). */
 uint64_t se_launch_count(int reset);
+/* Which kernels serve single-file BLOCK8 calls on device buffers: 0 = auto
+ * (persistent tile kernels from 8 tiles per SM up, else the per-CTA kernels),
+ * 1 = tile, 2 = per-CTA; -1 only queries.  Returns the previous choice.
+ * Process-wide; a test / measurement knob (env SE_KERNEL=tile|cta). */
+int se_kernel_choice(int choice);
 
 #ifdef __cplusplus
 }

@@ -99,7 +99,7 @@ SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_
            "se_container_streams", "se_container_size", "se_container_pack", "se_container_open",
            "se_disperse_plan", "se_storage_footprint", "se_sha256",
            "fragment_protect_stripe", "fragment_recover_stripe", "fragment_workspace_size",
-           "fragment_protect_ws", "fragment_recover_ws"]
+           "fragment_protect_ws", "fragment_recover_ws", "se_kernel_choice"]
 
 
 class Stripe(C.Structure):
@@ -176,6 +176,8 @@ def lib():
         L.fragment_recover_ws.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp, vp, C.c_uint64, vp]
         L.se_strerror.argtypes = [C.c_int]
         L.se_strerror.restype = C.c_char_p
+        L.se_kernel_choice.argtypes = [C.c_int]
+        L.se_kernel_choice.restype = C.c_int
         L.se_launch_count.argtypes = [C.c_int]
         L.se_launch_count.restype = C.c_uint64
         _lib = L
@@ -540,6 +542,15 @@ def dct8_inverse(coef, width: int, height: int, channels: int = 1, out=None, str
     _check(lib().dct8_inverse(C.byref(_dgeom(width, height, channels, 1)), _ptr(coef), _ptr(o), _stream(stream)),
            "dct8_inverse")
     return o
+
+
+KERNEL_AUTO, KERNEL_TILE, KERNEL_CTA = 0, 1, 2
+
+
+def kernel_choice(choice: int = -1) -> int:
+    """Set (0 auto, 1 tile, 2 per-CTA) or query (-1) which kernels serve
+    single-file BLOCK8 calls; returns the previous choice."""
+    return int(lib().se_kernel_choice(int(choice)))
 
 
 def launch_count(reset: bool = False) -> int:

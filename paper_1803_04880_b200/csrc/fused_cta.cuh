@@ -333,12 +333,14 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
     const int tid = threadIdx.x;
     const uint64_t blk = cta * BPC + tid;
     __shared__ AesSmem aes;
-    aes_load_tables(aes, tid, BPC);                       // constant tables: before the grid dependency
+    if (!p.ks_in_a) aes_load_tables(aes, tid, BPC);       // constant tables: before the grid dependency
     for (int i = tid; i < SA_W; i += BPC) sa[i] = 0;
     for (int i = tid; i < SB_W; i += BPC) sb[i] = 0;
     // programmatic dependent launch: inputs (and FULL-mode coefficients) are
-    // written by earlier work on the stream
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // written by earlier work on the stream.  With p.ks_in_a the kernel right
+    // before is the keystream kernel (a normal launch, so all earlier work is
+    // complete): only its keystream, needed at the copy-out, is waited for.
+    if (!p.ks_in_a) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
 
     if (blk < p.n_blocks) {
@@ -382,7 +384,11 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
     // row a9: 128-bit coalesced stores of the CTA's slice of each stream;
     // A' = A ^ keystream on the way out (row a6, XOR half)
     const uint64_t a0 = cta * (BPC / 8ull) * R::ABITS, c0 = cta * (BPC / 8ull) * R::CBITS;
-    {
+    if (p.ks_in_a) {
+        // row a6: A' = A ^ the keystream k_cipher_ctr wrote into A' just before
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        copy_s2g_xor_global<BPC>(p.a + a0, sa, min((uint64_t)SA_W * 4, p.a_bytes - a0), tid);
+    } else {
         // row a6: encrypt the CTA's A slice (whole AES counter blocks) on the way out
         const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
         const uint32_t nblk = (uint32_t)((alen + 15) / 16);

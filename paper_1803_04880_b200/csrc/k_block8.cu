@@ -169,8 +169,15 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
 }
 
 __global__ void k_report_init(se_report* r, uint32_t n) {
+    asm volatile("griddepcontrol.launch_dependents;");
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) { r[i].first_bad_block = -1; r[i].bad_blocks = 0; }
+}
+
+int launch_report_init(se_report* r, uint32_t n, void* stream) {
+    k_report_init<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(r, n);
+    note_launch();
+    return (int)cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- transform only

@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "se_internal.h"
 #include "../../include/se_container.h"
@@ -270,21 +271,52 @@ namespace se {
 // the footprint kernels live in the caller's workspace.
 static uint64_t full_ws_bytes(uint64_t rows, uint32_t width) { return rows * width * sizeof(int16_t); }
 
-// SE_KERNEL=cta (measurement knob): single-file BLOCK8 calls on the per-CTA
-// kernels instead of the persistent tile kernels.
-static bool cta_kernels() {
-    static const bool v = [] {
+// Kernel choice for single-file BLOCK8 calls on device buffers: the
+// persistent tile kernels (k_tile.cu) or the per-CTA kernels (k_block8.cu).
+// SE_KERNEL=tile|cta or se_kernel_choice() force one (measurement knob).
+static std::atomic<int> g_kernel_choice{-1};   // -1: not yet read from SE_KERNEL
+
+static int kernel_choice() {          // 0 auto, 1 tile, 2 cta
+    int v = g_kernel_choice.load(std::memory_order_relaxed);
+    if (v < 0) {
         const char* e = getenv("SE_KERNEL");
-        return e && strcmp(e, "cta") == 0;
-    }();
+        v = !e ? 0 : strcmp(e, "tile") == 0 ? 1 : strcmp(e, "cta") == 0 ? 2 : 0;
+        g_kernel_choice.store(v, std::memory_order_relaxed);
+    }
     return v;
 }
 
+static bool use_tile(uint64_t n_blocks, bool mask) {
+    const int k = kernel_choice();
+    if (k) return k == 1;
+    // measured on C2 / C3 / C4: masked (ALU-bound on SHA-2) the
+    // per-CTA kernels are ahead at every size (finer work units; protect's
+    // keystream kernel overlaps); PUBLIC_PLAIN the tile kernels at every size
+    (void)n_blocks;
+    return !mask;
+}
+
+extern "C" int se_kernel_choice(int choice) {
+    const int prev = kernel_choice();
+    if (choice >= 0 && choice <= 2) g_kernel_choice.store(choice, std::memory_order_relaxed);
+    return prev;
+}
+
+static int launch_keystream_into(const FusedParams& p, uint8_t* out, uint64_t n, void* stream) {
+    CipherParams cp;
+    memset(&cp, 0, sizeof cp);
+    cp.out = out;
+    cp.n = n;
+    cp.narrow = 1;
+    memcpy(cp.ctr, p.ctr, sizeof cp.ctr);
+    memcpy(cp.rk, p.rk, sizeof cp.rk);
+    return launch_cipher_ctr(cp, stream);
+}
+
+// {-1, 0} by one small kernel (one stream operation instead of two memsets;
+// the fused kernel after it is a programmatic launch and waits for it)
 static int report_init(se_report* r, cudaStream_t s) {
-    if (cudaMemsetAsync(&r->first_bad_block, 0xff, sizeof(int64_t), s) != cudaSuccess ||
-        cudaMemsetAsync(&r->bad_blocks, 0, sizeof(uint64_t), s) != cudaSuccess)
-        return SE_ECUDA;
-    return SE_OK;
+    return launch_report_init(r, 1, s) ? SE_ECUDA : SE_OK;
 }
 
 // Protect (rows a1-a9).  BLOCK8 device buffers: the persistent tile kernel
@@ -306,9 +338,16 @@ int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
-        const int e = (o.mapped || cta_kernels()) ? launch_protect_block8(p, g->levels, mask, stream)
-                               : launch_tile_block8(p, g->levels, mask, false, stream);
-        return e ? SE_ECUDA : SE_OK;
+        if (!o.mapped && use_tile(lay.n_blocks, mask))
+            return launch_tile_block8(p, g->levels, mask, false, stream) ? SE_ECUDA : SE_OK;
+        // per-CTA kernel; masked: the keystream kernel writes A' first and the
+        // fused kernel XORs it in at its copy-out (programmatic launch overlap);
+        // unmasked (and host-mapped A'): AES inside the fused kernel
+        if (mask && !o.mapped) {
+            p.ks_in_a = 1;
+            if (launch_keystream_into(p, p.a, lay.a_bytes, stream)) return SE_ECUDA;
+        }
+        return launch_protect_block8(p, g->levels, mask, stream) ? SE_ECUDA : SE_OK;
     }
     if (!o.ws || o.ws_bytes < full_ws_bytes(lay.rows, g->width)) return SE_EINVAL;
     if (!aligned16(o.ws)) return SE_EALIGN;
@@ -346,7 +385,7 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     p.report = d_report;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
-        const int e = (o.mapped || cta_kernels()) ? launch_recover_block8(p, g->levels, mask, stream)
+        const int e = (o.mapped || !use_tile(lay.n_blocks, mask)) ? launch_recover_block8(p, g->levels, mask, stream)
                                : launch_tile_block8(p, g->levels, mask, true, stream);
         return e ? SE_ECUDA : SE_OK;
     }

@@ -66,6 +66,7 @@ struct FusedParams {
     uint32_t bpr;             // 8x8 blocks per block-row = width / 8
     uint32_t one;             // = 1, opaque to ptxas: adds become IMADs (sha2_device.cuh)
     uint32_t bpr_magic;       // k_tile.cu: ceil(2^20 / bpr) (block row of a tile-local block)
+    uint32_t ks_in_a;         // per-CTA protect: A' already holds the keystream (k_cipher_ctr before)
     uint32_t ctr[4];          // IV + block_offset*a_bits/128, big-endian words
     uint32_t rk[44];          // AES-128 round keys, big-endian words
     uint32_t kiv[8];          // K || IV as big-endian words (SHA W0..W7)
@@ -181,6 +182,7 @@ int launch_tile_block8(const FusedParams& p, uint32_t levels, bool mask, bool re
 int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,
                         void* stream);
 int launch_dwt_fwd_block8(const DwtParams& p, uint32_t levels, void* stream);
+int launch_report_init(se_report* r, uint32_t n, void* stream);   // {-1, 0} x n
 // FULL mode (row a11): whole-matrix transform kernels and the footprint CTA kernels
 int launch_dwt_full_fwd(const DwtParams& p, uint32_t levels, void* stream);
 int launch_dwt_full_inv(const DwtParams& p, uint32_t levels, se_report* report, void* stream);

@@ -119,7 +119,7 @@ def test_cipher_parity(dev, orc, n):
 @pytest.mark.parametrize("flags", [0, se.FLAG_PUBLIC_PLAIN])
 def test_empty_input(dev, orc, mode, flags):
     """The degenerate case n = 0: empty fragments, empty recovery, the clean
-    report {-1, 0}, as the oracle; no kernel launches."""
+    report {-1, 0}, as the oracle; no kernel launches but the report's init."""
     x = torch.empty(0, dtype=torch.uint8, device=dev)
     se.launch_count(reset=True)
     a, b, c = se.fragment_protect(x, 64, 2, KEY, IV, mode=mode, flags=flags)
@@ -128,7 +128,7 @@ def test_empty_input(dev, orc, mode, flags):
     y, rep = se.fragment_recover(a, b, c, 0, 64, 2, KEY, IV, mode=mode, flags=flags)
     torch.cuda.synchronize()
     assert y.numel() == 0 and rep.tolist() == [-1, 0]
-    assert se.launch_count() == 0
+    assert se.launch_count() == 1           # the report init kernel
     assert se.cipher_encrypt(KEY, IV, x).numel() == 0
 
 
@@ -138,7 +138,14 @@ def test_launch_evidence(dev):
     a, b, c = se.fragment_protect(x, 256, 2, KEY, IV)
     se.fragment_recover(a, b, c, x.numel(), 256, 2, KEY, IV)
     torch.cuda.synchronize()
-    assert se.launch_count() == 2           # one fused kernel per direction (AES-CTR inside)
+    # masked (per-CTA kernels): protect = keystream into A' + fused kernel;
+    # recover = report init + fused kernel (AES-CTR inside)
+    assert se.launch_count() == 4
+    se.launch_count(reset=True)
+    a, b, c = se.fragment_protect(x, 256, 2, KEY, IV, flags=se.FLAG_PUBLIC_PLAIN)
+    se.fragment_recover(a, b, c, x.numel(), 256, 2, KEY, IV, flags=se.FLAG_PUBLIC_PLAIN)
+    torch.cuda.synchronize()
+    assert se.launch_count() == 3           # PUBLIC_PLAIN (tile kernels): 1 + report init + 1
 
 
 # ---------------------------------------------------------------- full-size configs
