@@ -269,6 +269,11 @@ uint64_t se_launch_count(int reset);
  * 1 = tile, 2 = per-CTA; -1 only queries.  Returns the previous choice.
  * Process-wide; a test / measurement knob (env SE_KERNEL=tile|cta). */
 int se_kernel_choice(int choice);
+/* Rows per segment of the streaming FULL-mode transform: 32, 64, 128, 256, or
+ * 0 = chosen by matrix size (default).  Returns the previous value (SE_EINVAL
+ * for another value).  Process-wide test knob: each length runs different
+ * halo / window code, so the tests compare every length with the oracle. */
+int se_full_segment_rows(int rows);
 
 #ifdef __cplusplus
 }

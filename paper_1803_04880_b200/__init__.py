@@ -64,7 +64,14 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         return obj
 
     with ThreadPoolExecutor(max_workers=len(sources())) as ex:
-        objs = list(ex.map(compile_one, sources()))
+        futs = [ex.submit(compile_one, src) for src in sources()]
+    errors = [f.exception() for f in futs if f.exception() is not None]
+    if errors:
+        for f in futs:
+            if f.exception() is None and os.path.exists(f.result()):
+                os.remove(f.result())
+        raise errors[0]
+    objs = [f.result() for f in futs]
     tmp = target + f".tmp{os.getpid()}"
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
     for o in objs:
@@ -99,7 +106,7 @@ SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_
            "se_container_streams", "se_container_size", "se_container_pack", "se_container_open",
            "se_disperse_plan", "se_storage_footprint", "se_sha256",
            "fragment_protect_stripe", "fragment_recover_stripe", "fragment_workspace_size",
-           "fragment_protect_ws", "fragment_recover_ws", "se_kernel_choice"]
+           "fragment_protect_ws", "fragment_recover_ws", "se_kernel_choice", "se_full_segment_rows"]
 
 
 class Stripe(C.Structure):
@@ -176,6 +183,7 @@ def lib():
         L.fragment_recover_ws.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp, vp, C.c_uint64, vp]
         L.se_strerror.argtypes = [C.c_int]
         L.se_strerror.restype = C.c_char_p
+        L.se_full_segment_rows.argtypes = [C.c_int]
         L.se_kernel_choice.argtypes = [C.c_int]
         L.se_kernel_choice.restype = C.c_int
         L.se_launch_count.argtypes = [C.c_int]
@@ -551,6 +559,14 @@ def kernel_choice(choice: int = -1) -> int:
     """Set (0 auto, 1 tile, 2 per-CTA) or query (-1) which kernels serve
     single-file BLOCK8 calls; returns the previous choice."""
     return int(lib().se_kernel_choice(int(choice)))
+
+
+def full_segment_rows(rows: int) -> int:
+    """Test knob: rows per segment of the FULL-mode streaming transform (0 = auto)."""
+    r = int(lib().se_full_segment_rows(int(rows)))
+    if r < 0:
+        raise SEError(r, "se_full_segment_rows")
+    return r
 
 
 def launch_count(reset: bool = False) -> int:

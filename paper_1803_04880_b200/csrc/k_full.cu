@@ -28,6 +28,8 @@
 // exact at the matrix borders, elsewhere their error stays inside the halo.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 
 #include "fused_cta.cuh"
@@ -579,6 +581,8 @@ __global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS_FULL) k_recover_ful
 // halved (down to 32) until the grid holds one full wave of warps (24 per
 // SM at ~80 registers): shorter segments re-read relatively more halo rows
 // (2H per segment).
+static std::atomic<int> g_seg_override{0};     // se_full_segment_rows (tests): 0 = by size
+
 template <int L>
 static void stream_shape(const DwtParams& p, int& seg, int& ncg, int& nseg, unsigned& grid) {
     using F = FStream<L>;
@@ -586,6 +590,7 @@ static void stream_shape(const DwtParams& p, int& seg, int& ncg, int& nseg, unsi
     const uint64_t rows = std::min<uint64_t>(p.row0 + p.rows_out, p.rows) - p.row0;
     seg = 256;
     while (seg > 32 && (uint64_t)ncg * ((rows + seg - 1) / seg) < 148ull * 24) seg /= 2;
+    if (const int o = g_seg_override.load(std::memory_order_relaxed)) seg = o;
     nseg = (int)((rows + seg - 1) / seg);
     grid = (unsigned)(((uint64_t)ncg * nseg + kStreamWarps - 1) / kStreamWarps);
 }
@@ -607,6 +612,19 @@ static int full_inv_l(const DwtParams& p, se_report* rep, cudaStream_t s) {
     if (grid) k_dwt_full_inv<L><<<grid, kStreamThreads, 0, s>>>(p, rep, seg, ncg, nseg);
     return (int)cudaGetLastError();
 }
+
+}  // namespace se
+
+// Segment rows of the streaming FULL-mode transform (32, 64, 128 or 256;
+// 0 = chosen by size, the default).  Test knob: the segment length decides
+// which halo and window code runs, so the tests compare every length with the
+// oracle.  Returns the previous value, or SE_EINVAL for another length.
+extern "C" int se_full_segment_rows(int rows) {
+    if (rows != 0 && rows != 32 && rows != 64 && rows != 128 && rows != 256) return SE_EINVAL;
+    return se::g_seg_override.exchange(rows);
+}
+
+namespace se {
 
 int launch_dwt_full_fwd(const DwtParams& p, uint32_t levels, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;

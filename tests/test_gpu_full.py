@@ -176,3 +176,34 @@ def test_full_streaming_fuzz(dev, orc, n, W, L):
     coef = se.dwt_fwd(to_dev(x, dev), W, L, mode=FULL)
     assert np.array_equal(coef.cpu().numpy().astype(np.int32), orc.dwt_fwd(x, W, L, orc.MODE_FULL))
     assert np.array_equal(se.dwt_inv(coef, n, W, L, mode=FULL).cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("seg", [64, 128, 256])
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_full_segment_lengths(dev, orc, seg, L):
+    """only 32-row segments were ever compared.  Force each
+    segment length (se_full_segment_rows) on a matrix several segments tall
+    with a ragged last segment: transform, inverse and FULL fragments equal
+    the oracle."""
+    n, W = 256 * 1000 - 77, 256                      # R = 1000 rows: 4 / 8 / 16 segments + ragged
+    x = data(n, seg + L)
+    prev = se.full_segment_rows(seg)
+    try:
+        coef = se.dwt_fwd(to_dev(x, dev), W, L, mode=FULL)
+        ref = orc.dwt_fwd(x, W, L, orc.MODE_FULL)
+        assert np.array_equal(coef.cpu().numpy().astype(np.int32), ref)
+        assert np.array_equal(se.dwt_inv(coef, n, W, L, mode=FULL).cpu().numpy(), x)
+        a, b, c = se.fragment_protect(to_dev(x, dev), W, L, KEY, IV, mode=FULL)
+        oa, ob, oc = orc.protect(x, W, L, KEY, IV, mode=orc.MODE_FULL)
+        assert np.array_equal(a.cpu().numpy(), oa)
+        assert np.array_equal(b.cpu().numpy(), ob)
+        assert np.array_equal(c.cpu().numpy(), oc)
+        back, rep = se.fragment_recover(a, b, c, n, W, L, KEY, IV, mode=FULL)
+        assert np.array_equal(back.cpu().numpy(), x) and rep.cpu().tolist() == [-1, 0]
+    finally:
+        se.full_segment_rows(prev)
+
+
+def test_full_segment_knob_rejects_other_lengths(dev):
+    with pytest.raises(se.SEError):
+        se.full_segment_rows(48)

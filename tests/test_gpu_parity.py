@@ -257,3 +257,35 @@ def test_virtual_stripes_equal_whole(dev, world):
         assert torch.equal(back, xs) and rep.cpu().tolist() == [-1, 0]
     for s in range(3):
         assert torch.equal(torch.cat(parts[s]), whole[s])
+
+
+def test_batch_1100_files_multi_pass_search(dev, orc):
+    """with >1,024 jobs the batch kernel's 32-ary job search
+    takes several dependent passes (1,100 -> 35 -> 2 -> 1).  Sampled files -
+    first, last, the files around CTA-count boundaries and ~50 random ones -
+    equal the oracle element by element; every file round-trips."""
+    rng = np.random.default_rng(1100)
+    n_files = 1100
+    sizes = np.exp(rng.uniform(np.log(64), np.log(48 * 1024), size=n_files)).astype(np.int64)
+    sizes[5] = 1
+    sizes[6] = 8 * 1024                            # exactly one CTA of 128 blocks at W = 64... plus a row
+    files = [synth.random_bytes(int(s), 7000 + i) for i, s in enumerate(sizes)]
+    widths = [synth.width_rule(int(s)) for s in sizes]
+    ivs = [synth.iv_for(5, i) for i in range(n_files)]
+    batch = se.Batch([to_dev(f, dev) for f in files], widths, ivs, 2, KEY)
+    begins = [int(batch.jobs[i].cta_begin) for i in range(n_files)]
+    assert batch.total_ctas > 1100
+    streams = batch.protect()
+    picks = {0, 1, n_files - 2, n_files - 1} | set(rng.integers(0, n_files, size=50).tolist())
+    # files whose CTA range starts right at / after a multiple of 32 CTAs (search lane boundaries)
+    picks |= {i for i in range(1, n_files) if begins[i] // 32 != begins[i - 1] // 32}
+    for i in sorted(picks)[:160]:
+        oa, ob, oc = orc.protect(files[i], widths[i], 2, KEY, ivs[i])
+        a, b, c = streams[i]
+        assert np.array_equal(a.cpu().numpy(), oa), i
+        assert np.array_equal(b.cpu().numpy(), ob), i
+        assert np.array_equal(c.cpu().numpy(), oc), i
+    outs, reps = batch.recover()
+    for f, o in zip(files, outs):
+        assert np.array_equal(o.cpu().numpy(), f)
+    assert (reps.cpu().numpy() == np.array([-1, 0])).all()
