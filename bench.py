@@ -345,6 +345,49 @@ def run_se(args):
         allreduce_max(t)                                    # max over ranks
     ms_step, mp_max, mr_max = (float(v) for v in t.tolist())
 
+    # ---- the PUBLIC_PLAIN measurement mode (C26) on the same input in the same
+    #      run: the HBM-bound sub-path (transform + split + AES), reported beside
+    #      the masked headline with its own roofline
+    variants = {}
+    if masked and not args.no_variants:
+        pflags = flags | se.FLAG_PUBLIC_PLAIN
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                se.fragment_protect(x, W, L, key, iv, flags=pflags, block_offset=boff, out=(a, b, cc), stream=stream)
+                se.fragment_recover(a, b, cc, n, W, L, key, iv, flags=pflags, block_offset=boff, out=out,
+                                    report=rep, stream=stream)
+        stream.synchronize()
+        assert torch.equal(out, x) and rep.cpu().tolist() == [-1, 0], "PUBLIC_PLAIN round trip"
+        pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                l2_flush(flush, k)
+                pev[k][0].record(stream)
+                se.fragment_protect(x, W, L, key, iv, flags=pflags, block_offset=boff, out=(a, b, cc), stream=stream)
+                pev[k][1].record(stream)
+                se.fragment_recover(a, b, cc, n, W, L, key, iv, flags=pflags, block_offset=boff, out=out,
+                                    report=rep, stream=stream)
+                pev[k][2].record(stream)
+        stream.synchronize()
+        pp = sum(e[0].elapsed_time(e[1]) for e in pev) / args.steps
+        pr = sum(e[1].elapsed_time(e[2]) for e in pev) / args.steps
+        tv = torch.tensor([pp + pr, pp, pr], dtype=torch.float64, device=dev)
+        if world > 1:
+            allreduce_max(tv)
+        pms, pp_max, pr_max = (float(v) for v in tv.tolist())
+        pdom, pdom_ms = ("k_tile_protect", pp) if pp >= pr else ("k_tile_recover", pr)
+        pkey = f"k_tile<{L}, 0, {0 if pdom == 'k_tile_protect' else 1}>"
+        variants["public_plain"] = {
+            "what": "PUBLIC_PLAIN (C26): B and C left unmasked, transform + split + AES-CTR on A only; "
+                    "same input, same run, L2 flushed between steps",
+            "value": None, "unit": "GB/s", "ms_per_step": round(pms, 5),
+            "kernels_ms": {"protect": round(pp, 5), "recover": round(pr, 5)},
+            "max_over_ranks_ms": {"protect": round(pp_max, 5), "recover": round(pr_max, 5)},
+            "_dom": (pkey, pdom_ms)}
+
     # ---- e2e: same metric through the public host API (pinned host buffers,
     #      H2D of the inputs and D2H of the results inside the timed region)
     e2e = run_e2e(se, torch, x_np, W, L, key, iv, flags | (se.FLAG_HOST_MAPPED if args.e2e_mapped else 0), dev,
@@ -391,7 +434,10 @@ def run_se(args):
     gbs = total_bytes / (ms_step / 1e3) / 1e9
     # dominant kernel = the slower of the two fused calls (each call is one kernel launch)
     dom_name, dom_ms = ("k_protect_block8", mp) if mp >= mr else ("k_recover_block8", mr)
-    kkey = f"{dom_name}<{L}, {1 if masked else 0}>"
+    if masked:      # per-CTA kernels (se_api.cu use_tile); protect = keystream kernel + fused kernel
+        kkey = f"{dom_name}<{L}, 1>"
+    else:           # the persistent tile kernels
+        kkey = f"k_tile<{L}, 0, {0 if dom_name == 'k_protect_block8' else 1}>"
     roofline = make_roofline(kkey, config_dict(args, world)["workload"], L, masked, n, lay, dom_ms, peaks, peak_src)
     hbm_bytes = n + lay["a_bytes"] + lay["b_bytes"] + lay["c_bytes"]
     line = {
@@ -420,12 +466,19 @@ def run_se(args):
                                     "median": round(statistics.median(p + r for p, r in zip(t_prot, t_rec)), 5),
                                     "best": round(min(p + r for p, r in zip(t_prot, t_rec)), 5)}},
         "max_over_ranks_ms": {"protect": round(mp_max, 5), "recover": round(mr_max, 5)},
+        "variants": variants or None,
         "comparator_aes128_ctr_gbs": None if aes_gbs is None else round(aes_gbs, 2),
         "security_battery": battery,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if "public_plain" in variants:
+        v = variants["public_plain"]
+        pkey, pdom_ms = v.pop("_dom")
+        v["value"] = round(total_bytes / (v["ms_per_step"] / 1e3) / 1e9, 3)
+        v["roofline"] = make_roofline(pkey, config_dict(args, world)["workload"] + " (PUBLIC_PLAIN)", L, False, n,
+                                      lay, pdom_ms, peaks, peak_src)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(x_np, W, L, key, iv, flags, args.cpu_seconds, block_offset=boff)
     if world > 1:
@@ -878,10 +931,21 @@ def oracle_time(x_np, W, L, key, iv, flags, n_blocks_sample, threads, reps=1, bl
     return nb * reps, dt
 
 
+def oracle_rate(x_np, W, L, key, iv, flags, threads, block_offset=0, min_seconds=0.5):
+    """Blocks per second of the oracle on `threads` threads, from a probe grown
+    until it runs >= min_seconds (a tiny probe is dominated by thread start-up)."""
+    total_nb = -(-x_np.size // (W * 8)) * (W // 8)
+    nb = min(total_nb, 256 * threads)
+    while True:
+        done, dt = oracle_time(x_np, W, L, key, iv, flags, nb, threads, block_offset=block_offset)
+        if dt >= min_seconds or nb >= total_nb:
+            return done / max(dt, 1e-6)
+        nb = min(total_nb, int(nb * max(2.0, 1.5 * min_seconds / max(dt, 1e-3))))
+
+
 def cpu_baseline(x_np, W, L, key, iv, flags, seconds, block_offset=0):
     threads = os.cpu_count() or 1
-    nb_probe, dt_probe = oracle_time(x_np, W, L, key, iv, flags, 256 * threads, threads, block_offset=block_offset)
-    rate = nb_probe / max(dt_probe, 1e-6)
+    rate = oracle_rate(x_np, W, L, key, iv, flags, threads, block_offset)
     total_nb = -(-x_np.size // (W * 8)) * (W // 8)
     want = max(128, rate * seconds)
     nb = int(min(total_nb, want))
@@ -934,8 +998,7 @@ def run_reference(args):
     total_bytes = sum(x.size for x, _ in inputs)
     nb_of = [-(-x.size // (W * 8)) * (W // 8) for x, _ in inputs]
     x0, iv0 = inputs[0]
-    nb_probe, dt_probe = oracle_time(x0, W, L, key, iv0, flags, 128 * threads, threads)
-    rate = nb_probe / max(dt_probe, 1e-6)                     # blocks/s, all threads
+    rate = oracle_rate(x0, W, L, key, iv0, flags, threads, min_seconds=0.3)   # blocks/s, all threads
     nb_warm = int(min(nb_of[0], max(128, rate * 1.0)))
     for _ in range(args.warmup):
         oracle_time(x0, W, L, key, iv0, flags, nb_warm, threads)
@@ -990,6 +1053,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparator", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the PUBLIC_PLAIN line inside the masked run")
     ap.add_argument("--dct", type=int, default=0, choices=[0, 1, 2],
                     help="NEXT row f3: bench the Chapter 4 DCT SE at this protection level instead")
     ap.add_argument("--dct-keyed", action="store_true", help="level 2 with the keyed hash framing (D9)")
