@@ -439,9 +439,12 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
     const uint64_t a0 = cta * (BPC / 8ull) * R::ABITS, c0 = cta * (BPC / 8ull) * R::CBITS;
     const uint64_t alen = min((uint64_t)SA_W * 4, p.a_bytes - a0);
     __shared__ AesSmem aes;
-    aes_load_tables(aes, tid, BPC);                       // constant tables: before the grid dependency
+    if (!p.ks_in_out) aes_load_tables(aes, tid, BPC);     // constant tables: before the grid dependency
     if (tid == 0) { s_first = ~0ull; s_bad = 0; }
-    asm volatile("griddepcontrol.wait;" ::: "memory");    // fragments / report written by earlier work
+    // fragments / report written by earlier work.  With p.ks_in_out the kernel
+    // right before is the keystream kernel (a normal launch: everything earlier
+    // is complete), so only its keystream is waited for, just before use.
+    if (!p.ks_in_out) asm volatile("griddepcontrol.wait;" ::: "memory");
     copy_g2s<BPC>(sa, p.a + a0, alen, SA_W * 4, tid);
     if (R::BBITS) {
         const uint64_t b0 = cta * (BPC / 8ull) * R::BBITS;
@@ -460,7 +463,14 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         smem_get_record<R::CW, R::CBITS>(sc, SC_W, (uint32_t)tid * R::CBITS, C);
         if (MASK && R::BBITS) mask_c<R::BW, R::BBYTES, SPEC>(p, gb, B, C);    // C from B'
     }
-    {
+    if (p.ks_in_out) {
+        // row a6: the keystream kernel wrote this CTA's A-slice keystream into the
+        // first row run of the CTA's own output region (which only this CTA
+        // writes, after this read): A' -> A in shared memory
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        const uint64_t b0 = cta * BPC, br0 = b0 / p.bpr, bc0 = b0 - br0 * p.bpr;
+        xor_g2s<BPC>(sa, p.out + 8 * br0 * (uint64_t)p.width + 8 * bc0, alen, tid);
+    } else {
         // row a6: decrypt the CTA's A slice (whole AES counter blocks) in shared memory
         const uint32_t nblk = (uint32_t)((alen + 15) / 16);
         for (uint32_t j = tid; j < nblk; j += BPC) {

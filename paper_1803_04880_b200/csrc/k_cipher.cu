@@ -54,6 +54,13 @@ __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ Ciphe
         if constexpr (LANE) aes128_block(lane, p.rk, x);
         else aes128_block(small, p.rk, x);
         const uint64_t off = j * 16;
+        if (p.cta_ablocks) {                  // scatter: keystream only, whole AES blocks (se_api.cu checks)
+            const uint64_t cta = j / p.cta_ablocks, b0 = cta * kBlocksPerCta;
+            const uint64_t br = b0 / p.bpr, bc = b0 - br * p.bpr;
+            uint8_t* dst = p.out + 8 * br * (uint64_t)p.width + 8 * bc + 16 * (j - cta * p.cta_ablocks);
+            *reinterpret_cast<uint4*>(dst) = make_uint4(bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3]));
+            continue;
+        }
         if (off + 16 <= p.n) {
             const uint4 q = p.in ? __ldg(reinterpret_cast<const uint4*>(p.in + off)) : make_uint4(0, 0, 0, 0);
             uint4 r;

@@ -67,6 +67,8 @@ struct FusedParams {
     uint32_t one;             // = 1, opaque to ptxas: adds become IMADs (sha2_device.cuh)
     uint32_t bpr_magic;       // k_tile.cu: ceil(2^20 / bpr) (block row of a tile-local block)
     uint32_t ks_in_a;         // per-CTA protect: A' already holds the keystream (k_cipher_ctr before)
+    uint32_t ks_in_out;       // per-CTA recover: each CTA's A-slice keystream sits at the start of its
+                              // own output region (k_cipher_ctr before, scatter mode)
     uint32_t ctr[4];          // IV + block_offset*a_bits/128, big-endian words
     uint32_t rk[44];          // AES-128 round keys, big-endian words
     uint32_t kiv[8];          // K || IV as big-endian words (SHA W0..W7)
@@ -107,6 +109,12 @@ struct CipherParams {
     uint32_t narrow;          // keystream: one 128-thread CTA per SM (k_cipher.cu)
     se_report* report;        // nullable: initialised to {-1, 0} by this kernel (the fused recover
                               // kernel that follows updates it only after griddepcontrol.wait)
+    // scatter mode (cta_ablocks != 0): AES block j goes to the output region of
+    // recover CTA i = j / cta_ablocks (128 blocks per CTA): out + 8*br*W + 8*bc
+    // of its first 8x8 block (br, bc), + 16 * (j % cta_ablocks)
+    uint32_t cta_ablocks;
+    uint32_t bpr;
+    uint32_t width;
 };
 
 struct DwtParams {

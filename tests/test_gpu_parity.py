@@ -289,3 +289,31 @@ def test_batch_1100_files_multi_pass_search(dev, orc):
     for f, o in zip(files, outs):
         assert np.array_equal(o.cpu().numpy(), f)
     assert (reps.cpu().numpy() == np.array([-1, 0])).all()
+
+
+@pytest.mark.parametrize("W,rows,L", [(1024, 8 * 37, 2), (2048, 8 * 11, 3), (6144, 8 * 5, 2)])
+def test_recover_keystream_in_output_region(dev, orc, W, rows, L):
+    """Masked per-CTA recovery on whole rows of a multiple of 1024 bytes: the
+    keystream kernel parks each CTA's A-slice keystream at the start of that
+    CTA's own output region (and initialises the report).  Fragments from the
+    oracle, clean, damaged and under a wrong key: bytes and report equal the
+    oracle's."""
+    n = W * rows
+    x = make_input(n, W + rows, "bitmap")
+    prev = se.kernel_choice(se.KERNEL_AUTO)
+    try:
+        a, b, c = orc.protect(x, W, L, KEY, IV)
+        ga, gb, gc = se.fragment_protect(to_dev(x, dev), W, L, KEY, IV)
+        assert np.array_equal(ga.cpu().numpy(), a) and np.array_equal(gc.cpu().numpy(), c)
+        back, rep = se.fragment_recover(to_dev(a, dev), to_dev(b, dev), to_dev(c, dev), n, W, L, KEY, IV)
+        assert np.array_equal(back.cpu().numpy(), x) and rep.cpu().tolist() == [-1, 0]
+        a2, c2 = a.copy(), c.copy()
+        a2[len(a2) // 2] ^= 0x21
+        c2[60 * 200 + 5] ^= 0x04
+        for key, aa, cc in ((KEY, a2, c2), (bytes([KEY[0] ^ 4]) + KEY[1:], a, c)):
+            back, rep = se.fragment_recover(to_dev(aa, dev), to_dev(b, dev), to_dev(cc, dev), n, W, L, key, IV)
+            oback, orep = orc.recover(aa, b, cc, n, W, L, key, IV)
+            assert np.array_equal(back.cpu().numpy(), oback)
+            assert tuple(rep.cpu().tolist()) == orep and orep[1] > 0
+    finally:
+        se.kernel_choice(prev)
