@@ -250,6 +250,87 @@ __device__ __forceinline__ void mask_c(const FusedParams& p, uint64_t gb, const 
     for (int k = 0; k < 15; ++k) C[k] ^= (k & 1) ? (uint32_t)H[k / 2] : (uint32_t)(H[k / 2] >> 32);
 }
 
+// ---------------------------------------------------------------- stream slices in shared memory
+
+// Write this thread's NB-bit record (logical MSB-first words) into the warp's
+// part of a dense stream slice (memory byte order) at `words`; each warp's 32
+// records fill exactly NB whole words.  Record-centric for NB >= 32: a lane
+// writes the words that start inside its record, taking the bits past its
+// record end from the next lane's first word (one shuffle).  ks (nullable):
+// keystream words XORed in (A').
+template <int NB, int NW>
+__device__ __forceinline__ void put_stream(uint32_t* words, const uint32_t* ks, const uint32_t (&rec)[NW], int ct) {
+    const int lane = ct & 31, warp = ct >> 5;
+    const uint32_t wbase = (uint32_t)warp * NB;
+    if constexpr (NB % 32 == 0) {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const uint32_t w = wbase + lane * NW + k;
+            uint32_t v = bswap32(rec[k]);
+            if (ks) v ^= ks[w];
+            words[w] = v;
+        }
+    } else if constexpr (NB >= 32) {
+        constexpr int r = NB % 32;
+        const uint32_t nx = __shfl_down_sync(0xffffffffu, rec[0], 1);
+        uint32_t Z[NW + 1];
+#pragma unroll
+        for (int k = 0; k < NW - 1; ++k) Z[k] = rec[k];
+        Z[NW - 1] = rec[NW - 1] | (nx >> r);
+        Z[NW] = nx << (32 - r);
+        const uint32_t s0 = (uint32_t)lane * NB;
+        const uint32_t w0 = (s0 + 31) >> 5, o = (w0 << 5) - s0;          // first word starting in the record
+        const uint32_t w1 = (s0 + NB + 31) >> 5;                          // one past the last
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            if (w0 + k < w1) {
+                const uint32_t w = wbase + w0 + k;
+                uint32_t v = bswap32(__funnelshift_l(Z[k + 1], Z[k], o));
+                if (ks) v ^= ks[w];
+                words[w] = v;
+            }
+        }
+    } else {
+        // NB < 32 (A at L = 3): word-centric, lane w < NB assembles word w
+        // from the <= ceil(32/NB) + 1 records it overlaps
+        uint32_t acc = 0;
+        const int w = lane;
+        const int r0 = (32 * w) / NB;
+#pragma unroll
+        for (int j = 0; j <= 32 / NB + 1; ++j) {
+            const int rr = r0 + j;
+            const uint32_t val = __shfl_sync(0xffffffffu, rec[0], rr & 31);
+            const int pos = NB * rr - 32 * w;                 // record start relative to the word's MSB
+            if (rr < 32 && pos < 32 && pos > -NB) acc |= pos >= 0 ? (val >> pos) : (val << -pos);
+        }
+        if (w < NB) {
+            const uint32_t ww = wbase + w;
+            uint32_t v = bswap32(acc);
+            if (ks) v ^= ks[ww];
+            words[ww] = v;
+        }
+    }
+}
+
+// Read record `u` (NB bits, tile-local) of a dense stream slice in shared
+// memory (memory byte order) as logical MSB-first words; ks (nullable) is
+// XORed in first.
+template <int NB, int NW>
+__device__ __forceinline__ void get_stream(const uint32_t* words, const uint32_t* ks, uint32_t u, uint32_t (&rec)[NW]) {
+    const uint32_t s0 = u * NB, w = s0 >> 5, sh = s0 & 31;
+    uint32_t S[NW + 1];
+#pragma unroll
+    for (int k = 0; k <= NW; ++k) {
+        if (k == NW && (NB % 32) == 0) { S[k] = 0; continue; }
+        uint32_t m = words[w + k];
+        if (ks) m ^= ks[w + k];
+        S[k] = bswap32(m);
+    }
+#pragma unroll
+    for (int k = 0; k < NW; ++k) rec[k] = (NB % 32 == 0) ? S[k] : __funnelshift_l(S[k + 1], S[k], sh);
+    rec[NW - 1] &= head_mask(NB % 32);
+}
+
 // ---------------------------------------------------------------- FULL-mode footprints (row a11)
 
 // The coefficients of input footprint (br, bc) inside the R x W Mallat layout,
