@@ -87,10 +87,13 @@ __device__ __forceinline__ W64 ror64(W64 v) {
     return W64{__funnelshift_r(v.hi, v.lo, N - 32), __funnelshift_r(v.lo, v.hi, N - 32)};
 }
 #ifndef SE_SHR_FMA
-#define SE_SHR_FMA 1
+#define SE_SHR_FMA 0
 #endif
-// x >> n as IMAD.HI (x * 2^(32-n)).hi on the FMA pipe (2 issue slots there,
-// measured) instead of SHF on the saturated ALU pipe.
+// SE_SHR_FMA 1: x >> n as IMAD.HI (x * 2^(32-n)).hi on the FMA pipe (2 issue
+// slots there) instead of SHF on the ALU pipe.  Round 1 measured it ahead on
+// C2 with the old kernels; re-measured in round 2 (tools/gpu_r2_call15.sh,
+// variants A/B): C4 113.7 -> 114.3 GB/s and C2 88.9 -> 90.9 GB/s with the
+// plain shift, so 0.
 __device__ __forceinline__ uint32_t fshr(uint32_t x, int n, uint32_t one) {
 #if SE_SHR_FMA
     uint32_t r;
