@@ -108,7 +108,10 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
     __shared__ uint32_t s_job;
     using R = Rec<L>;
     const uint32_t x = blockIdx.x;
-    asm volatile("griddepcontrol.wait;" ::: "memory");   // job table / report init written by earlier work
+    // job table / report init written by earlier work; with the keystream kernel
+    // right before (protect, base.ks_in_a: a normal launch, so everything
+    // earlier is complete) only its keystream is waited for, at the copy-out
+    if (!bp.base.ks_in_a) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x < 32) {
         // largest j with cta_begin <= x: 32-ary search by warp 0 (3 dependent
         // loads for 10,000 jobs instead of 14 for a binary search)

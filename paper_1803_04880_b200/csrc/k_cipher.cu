@@ -79,6 +79,46 @@ __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ Ciphe
 }
 
 
+// Keystream of every file's A stream in a batch (fragment_protect_batch):
+// one thread per 16-byte counter block over all CTAs of the launch (a CTA's A
+// slice is exactly ABITS counter blocks), written into each file's own A'
+// buffer; the fused batch kernel follows with programmatic serialization and
+// XORs its records in (no scratch).
+template <int ABITS>
+__global__ void __launch_bounds__(kCipherThreads) k_batch_keystream(const __grid_constant__ BatchParams bp) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    __shared__ AesSmem aes;
+    aes_load_tables(aes, threadIdx.x, kCipherThreads);
+    __syncthreads();
+    const uint64_t total = bp.total_ctas * (uint64_t)ABITS;
+    const uint64_t stride = (uint64_t)gridDim.x * kCipherThreads;
+    for (uint64_t idx = (uint64_t)blockIdx.x * kCipherThreads + threadIdx.x; idx < total; idx += stride) {
+        const uint64_t cta = idx / ABITS, t = idx - cta * ABITS;
+        uint32_t lo = 0, hi = bp.n_jobs - 1;               // largest job with cta_begin <= cta
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) / 2;
+            if (bp.jobs[mid].cta_begin <= cta) lo = mid;
+            else hi = mid - 1;
+        }
+        const se_job& job = bp.jobs[lo];
+        const uint64_t rows = ((job.n_bytes + job.width - 1) / job.width + 7) / 8 * 8;
+        const uint64_t a_bytes = (rows / 8 * (job.width / 8) * ABITS + 7) / 8;
+        const uint64_t lcta = cta - job.cta_begin;
+        const uint64_t off = (lcta * ABITS + t) * 16;
+        if (off >= a_bytes) continue;
+        const JobDerived& dv = *reinterpret_cast<const JobDerived*>(job.derived);
+        uint32_t x[4];
+        ctr_add(dv.ctr, lcta * ABITS + t, x);
+        aes128_block(aes, bp.base.rk, x);
+        uint8_t* dst = job.a + off;
+        if (off + 16 <= a_bytes) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3]));
+        } else {
+            for (uint64_t k = 0; k < a_bytes - off; ++k) dst[k] = (uint8_t)(x[k / 4] >> (24 - 8 * (k % 4)));
+        }
+    }
+}
+
 // 64 KB of dynamic shared memory needs an opt-in, once per kernel and device
 template <auto Kernel>
 static void allow_lut() {
@@ -95,6 +135,23 @@ static void allow_lut() {
 constexpr int kCipherCtasPerSm = 3;
 constexpr int kKeystreamCtasPerSm = 8;
 
+
+int launch_batch_keystream(const BatchParams& bp, uint32_t a_bits, void* stream) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t total = bp.total_ctas * (uint64_t)a_bits;
+    const uint64_t want = (total + kCipherThreads - 1) / kCipherThreads;
+    const uint64_t cap = (uint64_t)sms * kKeystreamCtasPerSm;
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (grid == 0) return 0;
+    if (a_bits == 40) k_batch_keystream<40><<<grid, kCipherThreads, 0, s>>>(bp);
+    else if (a_bits == 160) k_batch_keystream<160><<<grid, kCipherThreads, 0, s>>>(bp);
+    else k_batch_keystream<10><<<grid, kCipherThreads, 0, s>>>(bp);
+    note_launch();
+    return (int)cudaGetLastError();
+}
 
 int launch_cipher_ctr(const CipherParams& p, void* stream) {
     int dev = 0, sms = 148;

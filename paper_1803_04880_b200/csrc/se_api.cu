@@ -681,7 +681,13 @@ static int batch_common(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ct
     fill_fused(bp.base, &g, lay, key, zero_iv);       // shared fields: round keys, H(0), one
     bp.total_ctas = total_ctas;
     const bool mask = !(flags & SE_FLAG_PUBLIC_PLAIN);
-    // AES-CTR of every file's A slices runs inside the batch kernel: no keystream scratch
+    // masked protect: a keystream kernel writes every file's keystream into its
+    // A' and the batch kernel XORs it in; otherwise the AES-CTR of each A slice
+    // runs inside the batch kernel.  No scratch either way.
+    if (mask && !recover && total_ctas) {
+        bp.base.ks_in_a = 1;
+        if (launch_batch_keystream(bp, lay.a_bits, stream)) return SE_ECUDA;
+    }
     return launch_batch_block8(bp, total_ctas, levels, mask, recover, stream) ? SE_ECUDA : SE_OK;
 }
 

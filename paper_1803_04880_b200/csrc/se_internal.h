@@ -189,6 +189,7 @@ int launch_recover_block8(const FusedParams& p, uint32_t levels, bool mask, void
 int launch_tile_block8(const FusedParams& p, uint32_t levels, bool mask, bool recover, void* stream);
 int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,
                         void* stream);
+int launch_batch_keystream(const BatchParams& bp, uint32_t a_bits, void* stream);   // into each job's A'
 int launch_dwt_fwd_block8(const DwtParams& p, uint32_t levels, void* stream);
 int launch_report_init(se_report* r, uint32_t n, void* stream);   // {-1, 0} x n
 // FULL mode (row a11): whole-matrix transform kernels and the footprint CTA kernels
