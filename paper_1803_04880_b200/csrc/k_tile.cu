@@ -72,6 +72,10 @@ struct TileCfg {
 
 // ---------------------------------------------------------------- PTX helpers
 
+#ifndef SE_MBAR_SUSPEND_NS
+#define SE_MBAR_SUSPEND_NS 4000
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -83,11 +87,14 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps (up to the hint)
+// until the phase completes instead of re-polling, which cost ~30 issue slots
+// per block in the PUBLIC_PLAIN kernels
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t done = 0;
     do {
-        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
-                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p;}"
+                     : "=r"(done) : "r"(bar), "r"(parity), "n"(SE_MBAR_SUSPEND_NS) : "memory");
     } while (!done);
 }
 // global -> shared bulk copy, completion counted on `bar` (bytes and addresses 16-aligned)
@@ -267,8 +274,16 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const uint2 q = *reinterpret_cast<const uint2*>(in + base + i * st);
-                        unpack4(q.x, v[i][0], v[i][1], v[i][2], v[i][3]);
-                        unpack4(q.y, v[i][4], v[i][5], v[i][6], v[i][7]);
+                        if (MASK) {
+                            unpack4(q.x, v[i][0], v[i][1], v[i][2], v[i][3]);
+                            unpack4(q.y, v[i][4], v[i][5], v[i][6], v[i][7]);
+                        } else {                  // one PRMT per byte (the shift-and-mask form takes two)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                v[i][j] = (int)__byte_perm(q.x, 0, 0x4440 | j);
+                                v[i][4 + j] = (int)__byte_perm(q.y, 0, 0x4440 | j);
+                            }
+                        }
                     }
                 } else {
                     const uint64_t br = blk / p.bpr, bc = blk - br * p.bpr;
