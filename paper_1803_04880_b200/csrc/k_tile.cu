@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
                     load_block(p.in, p.n_bytes, p.width, br, bc, v);
                 }
                 if (MASK) dwt8_fwd<L>(v, p.one);                                  // rows a2-a4 (adds on the FMA pipe)
-                else dwt8_fwd_lean<L>(v);                                         // rows a2-a4 (fewest instructions)
+                else dwt8_fwd_lean<L>(v, p.one);                                  // rows a2-a4 (fewest instructions)
                 for_each_field<L, 0>([&](int s, int pos, int i, int j, int w) {     // row a5
                     const int off = (s == 0) ? (1 << (w - 1)) - 128 : (1 << (w - 1));   // C9 (+ C8 on LL)
                     if (MASK) {
@@ -298,9 +298,9 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
                         else if (s == 1) put_field(B, pos, v[i][j], off, w, p.one);
                         else put_field(C, pos, v[i][j], off, w, p.one);
                     } else {
-                        if (s == 0) put_field_lean(A, pos, v[i][j], off, w);
-                        else if (s == 1) put_field_lean(B, pos, v[i][j], off, w);
-                        else put_field_lean(C, pos, v[i][j], off, w);
+                        if (s == 0) put_field_lean(A, pos, v[i][j], off, w, p.one);
+                        else if (s == 1) put_field_lean(B, pos, v[i][j], off, w, p.one);
+                        else put_field_lean(C, pos, v[i][j], off, w, p.one);
                     }
                 });
                 if (MASK) {
@@ -364,11 +364,11 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
                         else flip_top(C, pos);
                     });
                     for_each_field<L, 0>([&](int s, int pos, int i, int j, int w) {
-                        if (s == 0) v[i][j] = get_field_lean(A, pos, w) + 128;       // LL: uncentered (C8)
-                        else if (s == 1) v[i][j] = get_field_lean(B, pos, w);
-                        else v[i][j] = get_field_lean(C, pos, w);
+                        if (s == 0) v[i][j] = get_field_lean(A, pos, w, p.one) + 128;   // LL: uncentered (C8)
+                        else if (s == 1) v[i][j] = get_field_lean(B, pos, w, p.one);
+                        else v[i][j] = get_field_lean(C, pos, w, p.one);
                     });
-                    dwt8_inv_lean<L>(v);
+                    dwt8_inv_lean<L>(v, p.one);
                 }
                 int orv = 0;
 #pragma unroll

@@ -202,21 +202,34 @@ __device__ __forceinline__ void lift_fwd_lean(int (&x)[N]) {
     for (int k = 0; k < H; ++k) { x[k] = s[k]; x[H + k] = d[k]; }
 }
 
+#ifndef SE_INV_PRED_FMA
+#define SE_INV_PRED_FMA 1
+#endif
 template <int N>
-__device__ __forceinline__ void lift_inv_lean(int (&y)[N]) {
+__device__ __forceinline__ void lift_inv_lean(int (&y)[N], uint32_t one) {
     constexpr int H = N / 2;
     int x[N];
 #pragma unroll
     for (int k = 0; k < H; ++k) x[2 * k] = y[k] + ((1 - (k == 0 ? y[H] : y[H + k - 1]) - y[H + k]) >> 2);
 #pragma unroll
-    for (int k = 0; k < H; ++k)
-        x[2 * k + 1] = (2 * k + 2 < N) ? y[H + k] + ((x[2 * k] + x[2 * k + 2]) >> 1) : y[H + k] + x[2 * k];
+    for (int k = 0; k < H; ++k) {
+        if (2 * k + 2 < N) {
+#if SE_INV_PRED_FMA
+            // the two-operand sum as an IMAD (FMA pipe; recovery's ALU pipe is the busier)
+            x[2 * k + 1] = y[H + k] + (iadd(x[2 * k], x[2 * k + 2], one) >> 1);
+#else
+            x[2 * k + 1] = y[H + k] + ((x[2 * k] + x[2 * k + 2]) >> 1);
+#endif
+        } else {
+            x[2 * k + 1] = y[H + k] + x[2 * k];
+        }
+    }
 #pragma unroll
     for (int k = 0; k < N; ++k) y[k] = x[k];
 }
 
 template <int M, bool INV>
-__device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8]) {
+__device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8], uint32_t one) {
     // forward: rows then columns (C5); inverse: columns then rows
 #pragma unroll
     for (int pass = 0; pass < 2; ++pass) {
@@ -226,7 +239,7 @@ __device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8]) {
             int t[M];
 #pragma unroll
             for (int b = 0; b < M; ++b) t[b] = rows ? v[a][b] : v[b][a];
-            if (INV) lift_inv_lean<M>(t);
+            if (INV) lift_inv_lean<M>(t, one);
             else lift_fwd_lean<M>(t);
 #pragma unroll
             for (int b = 0; b < M; ++b) {
@@ -238,17 +251,17 @@ __device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8]) {
 }
 
 template <int L>
-__device__ __forceinline__ void dwt8_fwd_lean(int (&v)[8][8]) {
-    dwt2_level_lean<8, false>(v);
-    if (L >= 2) dwt2_level_lean<4, false>(v);
-    if (L >= 3) dwt2_level_lean<2, false>(v);
+__device__ __forceinline__ void dwt8_fwd_lean(int (&v)[8][8], uint32_t one) {
+    dwt2_level_lean<8, false>(v, one);
+    if (L >= 2) dwt2_level_lean<4, false>(v, one);
+    if (L >= 3) dwt2_level_lean<2, false>(v, one);
 }
 
 template <int L>
-__device__ __forceinline__ void dwt8_inv_lean(int (&v)[8][8]) {
-    if (L >= 3) dwt2_level_lean<2, true>(v);
-    if (L >= 2) dwt2_level_lean<4, true>(v);
-    dwt2_level_lean<8, true>(v);
+__device__ __forceinline__ void dwt8_inv_lean(int (&v)[8][8], uint32_t one) {
+    if (L >= 3) dwt2_level_lean<2, true>(v, one);
+    if (L >= 2) dwt2_level_lean<4, true>(v, one);
+    dwt2_level_lean<8, true>(v, one);
 }
 
 // ------------------------------------------------------------------ records
@@ -307,12 +320,23 @@ __device__ __forceinline__ int get_field(const uint32_t (&r)[NW], int pos, int o
 
 // Lean field placement (issue-bound kernels): v + off placed with one
 // shift-add per field; the additions of constants chain and fold.
+#ifndef SE_PACK_FMA
+#define SE_PACK_FMA 0
+#endif
 template <int NW>
-__device__ __forceinline__ void put_field_lean(uint32_t (&r)[NW], int pos, int v, int off, int w) {
+__device__ __forceinline__ void put_field_lean(uint32_t (&r)[NW], int pos, int v, int off, int w, uint32_t one) {
     const int word = pos >> 5, end = (pos & 31) + w;
     const uint32_t u = (uint32_t)(v + off);
     if (end <= 32) {
+#if SE_PACK_FMA
+        // u << k as an IMAD by an opaque power of two (FMA pipe); v * 2^k + (r + off * 2^k)
+        uint32_t t;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(u), "r"(one << (32 - end)), "r"(r[word]));
+        r[word] = t;
+#else
+        (void)one;
         r[word] += u << (32 - end);
+#endif
     } else {
         r[word] += u >> (end - 32);
         r[word + 1] += u << (64 - end);
@@ -322,12 +346,26 @@ __device__ __forceinline__ void put_field_lean(uint32_t (&r)[NW], int pos, int v
 // Lean field extraction: the caller has XORed every field's top bit in place
 // (flip_top), so each field is the sign-extended w-bit value v = u - 2^(w-1)
 // (offset binary, C9): one or two shifts.
+#ifndef SE_EXTRACT_FMA
+#define SE_EXTRACT_FMA 1
+#endif
 template <int NW>
-__device__ __forceinline__ int get_field_lean(const uint32_t (&r)[NW], int pos, int w) {
+__device__ __forceinline__ int get_field_lean(const uint32_t (&r)[NW], int pos, int w, uint32_t one) {
     const int word = pos >> 5, start = pos & 31, end = start + w;
     uint32_t top;
-    if (end <= 32) top = r[word] << start;
-    else top = __funnelshift_l(r[word + 1], r[word], start);
+    if (end <= 32) {
+#if SE_EXTRACT_FMA
+        // the left shift as an IMAD by an opaque power of two: the recovery
+        // kernel's ALU pipe is the busier one (~83 %)
+        if (start) asm("mul.lo.u32 %0, %1, %2;" : "=r"(top) : "r"(r[word]), "r"(one << start));
+        else top = r[word];
+#else
+        (void)one;
+        top = r[word] << start;
+#endif
+    } else {
+        top = __funnelshift_l(r[word + 1], r[word], start);
+    }
     return (int)top >> (32 - w);
 }
 
