@@ -158,34 +158,38 @@ def sampled_ranges(nb, k=6, seed=0):
     return [(g * 128, min(nb, (g + 1) * 128)) for g in sorted(picks)]
 
 
-def check_sampled(orc, x, W, L, a, b, c, iv, seed):
+def check_sampled(orc, x, W, L, a, b, c, iv, seed, flags=0):
     lay = orc.layout(x.size, W, L)
     ha, hb, hc = a.cpu().numpy(), b.cpu().numpy(), c.cpu().numpy()
     bits = (lay["a_bits"], lay["b_bits"], lay["c_bits"])
     for b0, b1 in sampled_ranges(lay["n_blocks"], seed=seed):
         bufs = [np.zeros(lay[k], np.uint8) for k in ("a_bytes", "b_bytes", "c_bytes")]
-        orc.protect(x, W, L, KEY, iv, block_range=(b0, b1), out=bufs)
+        orc.protect(x, W, L, KEY, iv, flags=flags, block_range=(b0, b1), out=bufs)
         for s, (got, ref) in enumerate(zip((ha, hb, hc), bufs)):
             lo, hi = b0 * bits[s] // 8, -(-b1 * bits[s] // 8)
             assert np.array_equal(got[lo:hi], ref[lo:hi]), ("stream", s, "blocks", b0, b1)
 
 
+@pytest.mark.parametrize("flags", [0, se.FLAG_PUBLIC_PLAIN])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 33, 4])
-def test_config_full_size(dev, orc, cfg):
+def test_config_full_size(dev, orc, cfg, flags):
+    """The BASELINE configs at full size in the bench's launch configuration
+    (masked: per-CTA kernels + keystream kernels; PUBLIC_PLAIN: the tile
+    kernels), sampled against the oracle where the whole file is too big."""
     base = 4 if cfg == 4 else 3 if cfg == 33 else cfg
     c = synth.CONFIGS[base]
     x = synth.config_input(cfg)
     W, L, iv = c["width"], c["levels"], synth.iv_for(base)
     xt = to_dev(x, dev)
-    a, b, cc = se.fragment_protect(xt, W, L, KEY, iv)
+    a, b, cc = se.fragment_protect(xt, W, L, KEY, iv, flags=flags)
     if cfg in (1, 2):          # small enough for the whole oracle
-        oa, ob, oc = orc.protect(x, W, L, KEY, iv)
+        oa, ob, oc = orc.protect(x, W, L, KEY, iv, flags=flags)
         assert np.array_equal(a.cpu().numpy(), oa)
         assert np.array_equal(b.cpu().numpy(), ob)
         assert np.array_equal(cc.cpu().numpy(), oc)
     else:
-        check_sampled(orc, x, W, L, a, b, cc, iv, seed=cfg)
-    back, rep = se.fragment_recover(a, b, cc, x.size, W, L, KEY, iv)
+        check_sampled(orc, x, W, L, a, b, cc, iv, seed=cfg, flags=flags)
+    back, rep = se.fragment_recover(a, b, cc, x.size, W, L, KEY, iv, flags=flags)
     assert rep.cpu().tolist() == [-1, 0]
     assert torch.equal(back, xt)
     del a, b, cc, back, xt
