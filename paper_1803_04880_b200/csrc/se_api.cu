@@ -286,13 +286,12 @@ static int kernel_choice() {          // 0 auto, 1 tile, 2 cta
     return v;
 }
 
-static bool use_tile(uint64_t n_blocks, bool mask) {
+static bool use_tile(bool mask) {
     const int k = kernel_choice();
     if (k) return k == 1;
-    // measured on C2 / C3 / C4: masked (ALU-bound on SHA-2) the
-    // per-CTA kernels are ahead at every size (finer work units; protect's
-    // keystream kernel overlaps); PUBLIC_PLAIN the tile kernels at every size
-    (void)n_blocks;
+    // measured on C2 / C3 / C4: masked (ALU-bound on SHA-2)
+    // the per-CTA kernels are ahead at every size (finer work units; the
+    // keystream kernels overlap); PUBLIC_PLAIN the tile kernels at every size
     return !mask;
 }
 
@@ -320,12 +319,13 @@ static int launch_keystream_into(const FusedParams& p, uint8_t* out, uint64_t n,
     cp.width = p.width;
     cp.out = out;
     cp.n = n;
-    cp.narrow = 1;
     static const int lut = [] {
         const char* e = getenv("SE_KS_LUT");
-        return e ? atoi(e) : 1;       // measured: C4 masked protect 4.855 -> 4.721 ms, C2 / C3 slightly faster
+        return e ? atoi(e) : 1;
     }();
-    cp.lane_lut = lut;        // 1: the 64 KB lane-replicated table (standalone cipher kernel)
+    // 1: the 64 KB lane-replicated table (measured: C4 masked protect 4.855 ->
+    // 4.721 ms against the 5 KB tables, C2 / C3 slightly faster)
+    cp.lane_lut = lut;
     memcpy(cp.ctr, p.ctr, sizeof cp.ctr);
     memcpy(cp.rk, p.rk, sizeof cp.rk);
     return launch_cipher_ctr(cp, stream);
@@ -356,7 +356,7 @@ int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
     p.a = (uint8_t*)d_a; p.b = (uint8_t*)d_b; p.c = (uint8_t*)d_c;
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
     if (g->mode == SE_MODE_BLOCK8) {
-        if (!o.mapped && use_tile(lay.n_blocks, mask))
+        if (!o.mapped && use_tile(mask))
             return launch_tile_block8(p, g->levels, mask, false, stream) ? SE_ECUDA : SE_OK;
         // per-CTA kernel; masked: the keystream kernel writes A' first and the
         // fused kernel XORs it in at its copy-out (programmatic launch overlap);
@@ -395,7 +395,7 @@ int recover_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
         }
     }
     const bool mask = !(g->flags & SE_FLAG_PUBLIC_PLAIN);
-    const bool tile = g->mode == SE_MODE_BLOCK8 && !o.mapped && use_tile(lay.n_blocks, mask);
+    const bool tile = g->mode == SE_MODE_BLOCK8 && !o.mapped && use_tile(mask);
     // masked per-CTA recovery on whole 1024-byte-multiple rows (C2, C3, C4): the
     // keystream kernel writes each CTA's A-slice keystream into the start of
     // that CTA's own output region and initialises the report
