@@ -16,13 +16,20 @@ namespace se {
 // Centering (C8) is applied to LL_L only, after the transform (see lift_fwd).
 // The 4 bytes of w as ints.  SE_UNPACK 0: shifts and masks (ALU pipe);
 // 1: byte conversions with selectors (I2F.U8 + F2I, conversion pipe) to free
-// ALU slots in the SHA-bound masked kernels - measured slower (C2 masked
-// protect 182.7 vs 185.7 GB/s, plain 591 vs 638), so 0.
+// ALU slots in the SHA-bound masked kernels - measured slower in round 1
+// (C2 masked protect 182.7 vs 185.7 GB/s); 2: one PRMT per byte - round 2,
+// C4 masked protect 4.702 -> 4.681 ms (C2 within noise), so 2.
 #ifndef SE_UNPACK
-#define SE_UNPACK 0
+#define SE_UNPACK 2
 #endif
 __device__ __forceinline__ void unpack4(uint32_t w, int& b0, int& b1, int& b2, int& b3) {
-#if SE_UNPACK == 1
+#if SE_UNPACK == 2
+    // one PRMT per byte (the shift-and-mask form takes two for the middle bytes)
+    b0 = (int)__byte_perm(w, 0, 0x4440);
+    b1 = (int)__byte_perm(w, 0, 0x4441);
+    b2 = (int)__byte_perm(w, 0, 0x4442);
+    b3 = (int)__byte_perm(w, 0, 0x4443);
+#elif SE_UNPACK == 1
     int* out[4] = {&b0, &b1, &b2, &b3};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -544,13 +551,18 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         smem_get_record<R::CW, R::CBITS>(sc, SC_W, (uint32_t)tid * R::CBITS, C);
         if (MASK && R::BBITS) mask_c<R::BW, R::BBYTES, SPEC>(p, gb, B, C);    // C from B'
     }
-    if (p.ks_in_out) {
+    if (p.ks_in_out == 1) {
         // row a6: the keystream kernel wrote this CTA's A-slice keystream into the
         // first row run of the CTA's own output region (which only this CTA
         // writes, after this read): A' -> A in shared memory
         asm volatile("griddepcontrol.wait;" ::: "memory");
         const uint64_t b0 = cta * BPC, br0 = b0 / p.bpr, bc0 = b0 - br0 * p.bpr;
         xor_g2s<BPC>(sa, p.out + 8 * br0 * (uint64_t)p.width + 8 * bc0, alen, tid);
+    } else if (p.ks_in_out == 2) {
+        // FULL mode: the keystream of the whole A stream sits at the start of the
+        // output, which only the inverse transform after this kernel writes
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        xor_g2s<BPC>(sa, p.out + a0, alen, tid);
     } else {
         // row a6: decrypt the CTA's A slice (whole AES counter blocks) in shared memory
         const uint32_t nblk = (uint32_t)((alen + 15) / 16);

@@ -67,8 +67,10 @@ struct FusedParams {
     uint32_t one;             // = 1, opaque to ptxas: adds become IMADs (sha2_device.cuh)
     uint32_t bpr_magic;       // k_tile.cu: ceil(2^20 / bpr) (block row of a tile-local block)
     uint32_t ks_in_a;         // per-CTA protect: A' already holds the keystream (k_cipher_ctr before)
-    uint32_t ks_in_out;       // per-CTA recover: each CTA's A-slice keystream sits at the start of its
-                              // own output region (k_cipher_ctr before, scatter mode)
+    uint32_t ks_in_out;       // per-CTA recover, keystream written by k_cipher_ctr just before: 1 = each
+                              // CTA's A slice at the start of its own output region (scatter mode),
+                              // 2 = the whole A stream at the start of out (FULL mode: out is written
+                              // only by the inverse transform afterwards)
     uint32_t ctr[4];          // IV + block_offset*a_bits/128, big-endian words
     uint32_t rk[44];          // AES-128 round keys, big-endian words
     uint32_t kiv[8];          // K || IV as big-endian words (SHA W0..W7)
