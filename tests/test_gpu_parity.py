@@ -321,3 +321,36 @@ def test_recover_keystream_in_output_region(dev, orc, W, rows, L):
             assert tuple(rep.cpu().tolist()) == orep and orep[1] > 0
     finally:
         se.kernel_choice(prev)
+
+
+def test_c5_full_workload_sampled(dev, orc):
+    """BASELINE config 5 at full size in the bench's launch configuration: the
+    10,000 files (log-uniform 1 KiB-16 MiB, ~17 GB) in one batched launch per
+    direction, as `bench.py --config 5` builds them; 30 sampled files (the
+    smallest, the largest, and random ones) equal the oracle element by
+    element, every file round-trips."""
+    sizes = synth.c5_file_sizes(10000, 5)
+    gen = torch.Generator(device=dev)
+    files = []
+    for i in range(len(sizes)):
+        gen.manual_seed(5_000_000 + i)
+        files.append(torch.randint(0, 256, (int(sizes[i]),), dtype=torch.uint8, device=dev, generator=gen))
+    widths = [synth.width_rule(int(s)) for s in sizes]
+    ivs = [synth.iv_for(5, i) for i in range(len(sizes))]
+    batch = se.Batch(files, widths, ivs, 2, KEY)
+    streams = batch.protect()
+    rng = np.random.default_rng(55)
+    order = np.argsort(sizes)
+    picks = {int(order[0]), int(order[1]), int(order[-1])} | set(rng.integers(0, len(sizes), size=27).tolist())
+    for i in sorted(picks):
+        x = files[i].cpu().numpy()
+        oa, ob, oc = orc.protect(x, widths[i], 2, KEY, ivs[i])
+        a, b, c = streams[i]
+        assert np.array_equal(a.cpu().numpy(), oa), i
+        assert np.array_equal(b.cpu().numpy(), ob), i
+        assert np.array_equal(c.cpu().numpy(), oc), i
+    outs, reps = batch.recover()
+    assert all(torch.equal(o, f) for o, f in zip(outs, files))
+    assert (reps.cpu().numpy() == np.array([-1, 0])).all()
+    del files, outs, streams, batch
+    torch.cuda.empty_cache()
