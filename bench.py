@@ -394,6 +394,10 @@ def run_se(args):
                   args.e2e_steps, chunk_bytes=args.e2e_chunk_kib << 10, n_streams=args.e2e_streams,
                   block_offset=boff, world=world) if args.e2e_steps > 0 else \
         {"value": None, "unit": "GB/s", "note": "skipped (--e2e-steps 0, profiling runs only)"}
+    if args.e2e_steps > 0:      # the asynchronous pair, recover chunk-pipelined behind protect, for comparison
+        e2e["pipelined_variant"] = run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, args.e2e_steps,
+                                           chunk_bytes=args.e2e_chunk_kib << 10, n_streams=args.e2e_streams,
+                                           block_offset=boff, world=world, pipelined=True)
 
     # ---- comparator: AES-128-CTR over all input bytes on the same GPU (paper methodology)
     aes_gbs = None
@@ -665,7 +669,7 @@ def run_multi(args):
 
 
 def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=0, n_streams=3, block_offset=0,
-            world=1):
+            world=1, pipelined=False):
     """The same metric end to end through the public host API: one step =
     fragment_protect_host (pinned input -> H2D -> fused kernel -> D2H of the three
     fragments) + fragment_recover_host (H2D fragments -> kernel -> D2H bytes);
@@ -680,6 +684,14 @@ def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=0, n_
     hout = se._host_empty(n)
 
     def one():
+        if pipelined:       # recover chunk k starts as soon as protect chunk k's fragments are in host memory
+            _, tp = se.fragment_protect_host_async(hx, W, L, key, iv, flags=flags, block_offset=block_offset,
+                                                   out=frag, chunk_bytes=chunk_bytes, n_streams=n_streams)
+            _, tr = se.fragment_recover_host_async(*frag, n, W, L, key, iv, flags=flags, block_offset=block_offset,
+                                                   out=hout, chunk_bytes=chunk_bytes, n_streams=n_streams, after=tp)
+            rep = tr.wait()
+            tp.wait()
+            return rep
         se.fragment_protect_host(hx, W, L, key, iv, flags=flags, block_offset=block_offset, out=frag,
                                  chunk_bytes=chunk_bytes, n_streams=n_streams)
         _, rep = se.fragment_recover_host(*frag, n, W, L, key, iv, flags=flags, block_offset=block_offset,
@@ -706,9 +718,11 @@ def run_e2e(se, torch, x_np, W, L, key, iv, flags, dev, steps, chunk_bytes=0, n_
            if mapped else (f"{chunk_bytes >> 10} KiB chunks" if chunk_bytes else
                            f"library-default chunks ({min(16 << 20, max(4 << 20, n // 4)) >> 10} KiB)")
            + f" on {n_streams} streams")
+    calls = ("fragment_protect_host_async + fragment_recover_host_async(after=protect ticket) + se_host_wait"
+             if pipelined else "fragment_protect_host + fragment_recover_host")
     return {"value": round(n * world / (ms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n + frag_bytes,
             "d2h_bytes_per_step": frag_bytes + n, "ms_per_step": round(ms, 4),
-            "path": f"fragment_protect_host + fragment_recover_host (C ABI, pinned host buffers, {how}), "
+            "path": f"{calls} (C ABI, pinned host buffers, {how}), "
                     f"host wall clock" + (", max over ranks; bytes are per rank" if world > 1 else "")}
 
 

@@ -186,6 +186,27 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
                           const void* h_a, const void* h_b, const void* h_c, void* h_out,
                           se_report* h_report, uint64_t chunk_bytes, uint32_t n_streams);
 
+/* Asynchronous forms: the same work enqueued on the library's per-device
+ * streams; the call returns once everything is enqueued and hands back a
+ * ticket.  A recover may name a protect ticket (`after`) whose fragments it
+ * reads: each of its chunks then waits only for the protect chunks it
+ * overlaps, so the recover's host-to-device copies run under the protect's
+ * device-to-host traffic (one pipeline fill and drain for the round trip,
+ * P:2682-2695).  se_host_wait blocks until a ticket's work is done, fills
+ * *h_report (nullable; recover tickets), frees the ticket and returns the
+ * call's status.  Host buffers must stay valid until then.  One ticket per
+ * direction and device is in flight at a time: a new call of the same
+ * direction first waits for the previous one's work (its report is kept). */
+typedef struct se_host_ticket se_host_ticket;
+int fragment_protect_host_async(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
+                                const void* h_in, void* h_a, void* h_b, void* h_c,
+                                uint64_t chunk_bytes, uint32_t n_streams, se_host_ticket** ticket);
+int fragment_recover_host_async(const se_geom* g, const uint8_t key[16], const uint8_t iv[16],
+                                const void* h_a, const void* h_b, const void* h_c, void* h_out,
+                                uint64_t chunk_bytes, uint32_t n_streams, const se_host_ticket* after,
+                                se_host_ticket** ticket);
+int se_host_wait(se_host_ticket* ticket, se_report* h_report);
+
 /* ---- FULL-mode row stripes with halo rows (row e for a11) ---------------
  * A FULL-mode file (whole-matrix DWT) split into stripes of block rows for
  * several GPUs.  Lifting reaches 2(2^L - 1) input rows beyond a stripe

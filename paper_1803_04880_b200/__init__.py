@@ -106,7 +106,8 @@ SYMBOLS = ["fragment_layout", "fragment_protect", "fragment_recover", "fragment_
            "se_container_streams", "se_container_size", "se_container_pack", "se_container_open",
            "se_disperse_plan", "se_storage_footprint", "se_sha256",
            "fragment_protect_stripe", "fragment_recover_stripe", "fragment_workspace_size",
-           "fragment_protect_ws", "fragment_recover_ws", "se_kernel_choice", "se_full_segment_rows"]
+           "fragment_protect_ws", "fragment_recover_ws", "se_kernel_choice", "se_full_segment_rows",
+           "fragment_protect_host_async", "fragment_recover_host_async", "se_host_wait"]
 
 
 class Stripe(C.Structure):
@@ -152,6 +153,11 @@ def lib():
         L.fragment_recover_batch.argtypes = [C.c_uint32, vp, C.c_uint64, C.c_uint32, C.c_uint32, u8p, vp, vp]
         L.fragment_protect_host.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, C.c_uint64, C.c_uint32]
         L.fragment_recover_host.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, vp, C.c_uint64, C.c_uint32]
+        L.fragment_protect_host_async.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, C.c_uint64, C.c_uint32,
+                                                  C.POINTER(C.c_void_p)]
+        L.fragment_recover_host_async.argtypes = [gp, u8p, u8p, vp, vp, vp, vp, C.c_uint64, C.c_uint32, vp,
+                                                  C.POINTER(C.c_void_p)]
+        L.se_host_wait.argtypes = [vp, vp]
         L.dwt_fwd.argtypes = [gp, vp, vp, vp]
         L.dwt_inv.argtypes = [gp, vp, vp, vp]
         L.cipher_encrypt.argtypes = [u8p, u8p, C.c_uint64, vp, vp, C.c_uint64, vp]
@@ -659,6 +665,57 @@ def fragment_recover_host(a, b, c, n_bytes: int, width: int, levels: int, key, i
                                        _ptr(b) if b is not None and b.numel() else None, _ptr(c), _ptr(o),
                                        C.byref(rep), int(chunk_bytes), int(n_streams)), "fragment_recover_host")
     return o, (int(rep.first_bad_block), int(rep.bad_blocks))
+
+
+class HostTicket:
+    """An asynchronous host call in flight (fragment_*_host_async); wait()
+    blocks until its work is done and returns the recover report (or None)."""
+
+    def __init__(self, handle, keep):
+        self._h = handle
+        self._keep = keep            # host tensors the call reads / writes
+        self.report = None
+
+    def wait(self):
+        if self._h is None:
+            return self.report
+        rep = Report()
+        st = lib().se_host_wait(self._h, C.byref(rep))
+        self._h = None
+        self._keep = None
+        _check(st, "se_host_wait")
+        self.report = (int(rep.first_bad_block), int(rep.bad_blocks))
+        return self.report
+
+
+def fragment_protect_host_async(x, width: int, levels: int, key, iv, mode: int = MODE_BLOCK8, flags: int = 0,
+                                block_offset: int = 0, out=None, chunk_bytes: int = 0, n_streams: int = 0):
+    """Enqueue fragment_protect_host; returns ((A', B', C') host tensors, HostTicket)."""
+    lay = fragment_layout(x.numel(), width, levels, mode, flags, block_offset)
+    a, b, c = out if out is not None else (_host_empty(lay["a_bytes"]), _host_empty(lay["b_bytes"]),
+                                           _host_empty(lay["c_bytes"]))
+    g = _geom(x.numel(), width, levels, mode, flags, block_offset)
+    h = C.c_void_p()
+    _check(lib().fragment_protect_host_async(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(x), _ptr(a),
+                                             _ptr(b) if b.numel() else None, _ptr(c), int(chunk_bytes),
+                                             int(n_streams), C.byref(h)), "fragment_protect_host_async")
+    return (a, b, c), HostTicket(h, (x, a, b, c))
+
+
+def fragment_recover_host_async(a, b, c, n_bytes: int, width: int, levels: int, key, iv, mode: int = MODE_BLOCK8,
+                                flags: int = 0, block_offset: int = 0, out=None, chunk_bytes: int = 0,
+                                n_streams: int = 0, after=None):
+    """Enqueue fragment_recover_host, chunk by chunk after the protect ticket
+    `after` (if given); returns (host bytes tensor, HostTicket)."""
+    o = out if out is not None else _host_empty(n_bytes)
+    g = _geom(n_bytes, width, levels, mode, flags, block_offset)
+    h = C.c_void_p()
+    _check(lib().fragment_recover_host_async(C.byref(g), _bytes16(key, "key"), _bytes16(iv, "iv"), _ptr(a),
+                                             _ptr(b) if b is not None and b.numel() else None, _ptr(c), _ptr(o),
+                                             int(chunk_bytes), int(n_streams),
+                                             after._h if after is not None else None, C.byref(h)),
+           "fragment_recover_host_async")
+    return o, HostTicket(h, (a, b, c, o))
 
 
 # ---------------------------------------------------------------- security battery (f2)

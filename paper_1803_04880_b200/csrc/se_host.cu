@@ -125,6 +125,25 @@ struct Slot {
     size_t cap[5] = {0, 0, 0, 0, 0};
 };
 
+}  // namespace se
+
+// Asynchronous host calls (fragment_*_host_async): the per-chunk completion
+// events, in chunk order with each chunk's first block, so a dependent call
+// can wait chunk by chunk; recover tickets also carry the chunk reports.
+struct se_host_ticket {
+    int op = 0;                             // 0 protect, 1 recover
+    std::vector<uint64_t> blk0, nblk;       // chunk block ranges
+    std::vector<cudaEvent_t> done;          // chunk k's results are in host memory
+    std::vector<cudaEvent_t> tail;          // one per stream: everything enqueued has finished
+    std::vector<se_report> reps;            // recover: per-chunk reports, read at se_host_wait
+    const se_report* hreps = nullptr;       // recover: the context's pinned mirror until then
+    void* ctx = nullptr;                    // the HostCtx it runs in
+    bool collected = false;
+    int status = SE_OK;
+};
+
+namespace se {
+
 struct GraphKey {
     int op;                   // 0 protect, 1 recover
     uint32_t n_streams;
@@ -149,13 +168,17 @@ struct HostCtx {
     se_report* hinit = nullptr;           // pinned {-1, 0} per chunk: one H2D initialises a report
     size_t reps_cap = 0;
     std::mutex mu;
+    se_host_ticket* pending = nullptr;    // the asynchronous call still using this context, if any
 };
 
-static HostCtx& host_ctx(int dev) {
+// One context per (device, direction): a protect and a recover can be in
+// flight at the same time (the asynchronous calls below), each with its own
+// streams and staging slots.
+static HostCtx& host_ctx(int dev, int op) {
     static std::mutex m;
-    static std::map<int, HostCtx*> ctxs;
+    static std::map<std::pair<int, int>, HostCtx*> ctxs;
     std::lock_guard<std::mutex> g(m);
-    HostCtx*& c = ctxs[dev];
+    HostCtx*& c = ctxs[{dev, op}];
     if (!c) c = new HostCtx();
     return *c;
 }
@@ -316,14 +339,82 @@ static bool hybrid_enabled(int op) {
     return (mask >> op) & 1;
 }
 
+// Finish the asynchronous call still using ctx (if any): wait for all its
+// work, keep its chunk reports in the ticket, release the context.
+static void settle(HostCtx& c) {
+    se_host_ticket* t = c.pending;
+    if (!t) return;
+    for (cudaEvent_t e : t->tail)
+        if (cudaEventSynchronize(e) != cudaSuccess) t->status = SE_ECUDA;
+    if (t->op == 1 && t->hreps && !t->collected) {
+        t->reps.assign(t->hreps, t->hreps + t->done.size());
+        t->collected = true;
+    }
+    c.pending = nullptr;
+}
+
+// Record chunk k's completion on its stream (asynchronous calls).
+static int ticket_chunk(se_host_ticket* t, size_t k, cudaStream_t s) {
+    if (!t) return SE_OK;
+    return cudaEventRecord(t->done[k], s) == cudaSuccess ? SE_OK : SE_ECUDA;
+}
+
+// Make stream s wait for every chunk of `after` overlapping blocks [b0, b1).
+static int ticket_wait(const se_host_ticket* after, uint64_t b0, uint64_t b1, cudaStream_t s) {
+    if (!after) return SE_OK;
+    for (size_t j = 0; j < after->done.size(); ++j)
+        if (after->blk0[j] < b1 && b0 < after->blk0[j] + after->nblk[j] &&
+            cudaStreamWaitEvent(s, after->done[j], 0) != cudaSuccess)
+            return SE_ECUDA;
+    return SE_OK;
+}
+
+static int ticket_open(se_host_ticket* t, int op, HostCtx& c, const std::vector<Chunk>& chunks) {
+    if (!t) return SE_OK;
+    t->op = op;
+    t->ctx = &c;
+    for (const Chunk& ch : chunks) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SE_ECUDA;
+        t->done.push_back(e);
+        t->blk0.push_back(ch.blk0);
+        t->nblk.push_back(ch.nblk);
+    }
+    return SE_OK;
+}
+
+// Close an asynchronous call: one tail event per stream it used.
+static int ticket_close(se_host_ticket* t, HostCtx& c, uint32_t n_streams) {
+    for (uint32_t i = 0; i < n_streams; ++i) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SE_ECUDA;
+        t->tail.push_back(e);
+        if (cudaEventRecord(e, c.streams[i]) != cudaSuccess) return SE_ECUDA;
+    }
+    c.pending = t;
+    return SE_OK;
+}
+
+static void ticket_free(se_host_ticket* t) {
+    if (!t) return;
+    for (cudaEvent_t e : t->done) cudaEventDestroy(e);
+    for (cudaEvent_t e : t->tail) cudaEventDestroy(e);
+    delete t;
+}
+
 }  // namespace se
 
 using namespace se;
 
 extern "C" {
 
-int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_in,
-                          void* h_a, void* h_b, void* h_c, uint64_t chunk_bytes, uint32_t n_streams) {
+}  // extern "C"
+
+// fragment_protect_host / fragment_protect_host_async.  t != nullptr: the
+// asynchronous form (no final synchronisation; chunk events in t).
+static int protect_host_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_in,
+                             void* h_a, void* h_b, void* h_c, uint64_t chunk_bytes, uint32_t n_streams,
+                             se_host_ticket* t) {
     se_layout lay;
     int rc = fragment_layout(g, &lay);
     if (rc) return rc;
@@ -339,12 +430,20 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
         g2.flags &= ~(uint32_t)SE_FLAG_HOST_MAPPED;
         int dev = 0;
         cudaGetDevice(&dev);
-        HostCtx& ctx = host_ctx(dev);
+        HostCtx& ctx = host_ctx(dev, 0);
         std::lock_guard<std::mutex> lock(ctx.mu);
+        settle(ctx);
         if (ensure(ctx, 1)) return SE_ECUDA;
         ImplOpts o;
         o.mapped = true;
+        const std::vector<Chunk> one{Chunk{0, g->n_bytes, 0, lay.n_blocks}};
+        if (ticket_open(t, 0, ctx, one)) return SE_ECUDA;
         int st = protect_impl(&g2, key, iv, din, da, db, dc, o, ctx.streams[0]);
+        if (t) {
+            if (st == SE_OK) st = ticket_chunk(t, 0, ctx.streams[0]);
+            if (st == SE_OK) st = ticket_close(t, ctx, 1);
+            return st;
+        }
         if (cudaStreamSynchronize(ctx.streams[0]) != cudaSuccess) st = SE_ECUDA;
         return st;
     }
@@ -362,9 +461,11 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
         : make_chunks(g, lay, chunk_bytes, hybrid ? kBlocksPerCta : 1);
     int dev = 0;
     cudaGetDevice(&dev);
-    HostCtx& ctx = host_ctx(dev);
+    HostCtx& ctx = host_ctx(dev, 0);
     std::lock_guard<std::mutex> lock(ctx.mu);
+    settle(ctx);
     if (ensure(ctx, n_streams)) return SE_ECUDA;
+    if (ticket_open(t, 0, ctx, chunks)) return SE_ECUDA;
     const uint32_t bits[3] = {lay.a_bits, lay.b_bits, lay.c_bits};
     uint8_t* hout[3] = {(uint8_t*)h_a, (uint8_t*)h_b, (uint8_t*)h_c};
     std::vector<se_geom> cgs(chunks.size());
@@ -402,6 +503,7 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
                 ImplOpts o;
                 o.mapped = true;
                 int st = protect_impl(&cgs[k], key, iv, sl.buf[0], d[0], cls[k].b_bytes ? d[1] : nullptr, d[2], o, s);
+                if (!st) st = ticket_chunk(t, k, s);
                 if (st) return st;
             }
             return SE_OK;
@@ -425,16 +527,52 @@ int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t
                 if (sizes[i + 1] && cudaMemcpyAsync(hout[i] + c.blk0 * bits[i] / 8, sl.buf[i + 1], sizes[i + 1],
                                                     cudaMemcpyDeviceToHost, s) != cudaSuccess)
                     return SE_ECUDA;
+            if (ticket_chunk(t, k, s)) return SE_ECUDA;
         }
         return SE_OK;
     };
+    if (t) {                                  // asynchronous: issue directly, no final synchronisation
+        const int st = issue();
+        return st ? st : ticket_close(t, ctx, n_streams);
+    }
     const GraphKey gk = make_key(0, g, key, iv, h_in, h_a, h_b, h_c, chunk_bytes, n_streams);
     return run_chunks(ctx, gk, n_streams, issue);
 }
 
-int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_a,
-                          const void* h_b, const void* h_c, void* h_out, se_report* h_report, uint64_t chunk_bytes,
-                          uint32_t n_streams) {
+extern "C" {
+
+int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_in,
+                          void* h_a, void* h_b, void* h_c, uint64_t chunk_bytes, uint32_t n_streams) {
+    return protect_host_impl(g, key, iv, h_in, h_a, h_b, h_c, chunk_bytes, n_streams, nullptr);
+}
+
+int fragment_protect_host_async(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_in,
+                                void* h_a, void* h_b, void* h_c, uint64_t chunk_bytes, uint32_t n_streams,
+                                se_host_ticket** out) {
+    if (!out) return SE_EINVAL;
+    *out = nullptr;
+    se_host_ticket* t = new se_host_ticket();
+    const int st = protect_host_impl(g, key, iv, h_in, h_a, h_b, h_c, chunk_bytes, n_streams, t);
+    if (st != SE_OK) {
+        HostCtx* c = (HostCtx*)t->ctx;
+        if (c && c->pending == t) c->pending = nullptr;
+        for (uint32_t i = 0; c && i < c->streams.size(); ++i) cudaStreamSynchronize(c->streams[i]);
+        ticket_free(t);
+        return st;
+    }
+    *out = t;
+    return SE_OK;
+}
+
+}  // extern "C"
+
+// fragment_recover_host / fragment_recover_host_async (t != nullptr; `after`:
+// a protect ticket whose chunks must reach host memory before the chunks of
+// this call that read them are copied).
+static int recover_host_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_a,
+                             const void* h_b, const void* h_c, void* h_out, se_report* h_report,
+                             uint64_t chunk_bytes, uint32_t n_streams, const se_host_ticket* after,
+                             se_host_ticket* t) {
     se_layout lay;
     int rc = fragment_layout(g, &lay);
     if (rc) return rc;
@@ -451,8 +589,9 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
         g2.flags &= ~(uint32_t)SE_FLAG_HOST_MAPPED;
         int dev = 0;
         cudaGetDevice(&dev);
-        HostCtx& ctx = host_ctx(dev);
+        HostCtx& ctx = host_ctx(dev, 1);
         std::lock_guard<std::mutex> lock(ctx.mu);
+        settle(ctx);
         if (ensure(ctx, 1)) return SE_ECUDA;
         if (ctx.reps_cap < 1) {
             drop_graphs(ctx);
@@ -467,10 +606,18 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
         cudaStream_t s0 = ctx.streams[0];
         ImplOpts o;
         o.mapped = true;
+        const std::vector<Chunk> one{Chunk{0, g->n_bytes, 0, lay.n_blocks}};
+        if (ticket_open(t, 1, ctx, one) || ticket_wait(after, 0, lay.n_blocks, s0)) return SE_ECUDA;
         int st = recover_impl(&g2, key, iv, da, db, dc, dout, ctx.reps, o, s0);
         if (st == SE_OK &&
             cudaMemcpyAsync(ctx.hreps, ctx.reps, sizeof(se_report), cudaMemcpyDeviceToHost, s0) != cudaSuccess)
             st = SE_ECUDA;
+        if (t) {
+            t->hreps = ctx.hreps;
+            if (st == SE_OK) st = ticket_chunk(t, 0, s0);
+            if (st == SE_OK) st = ticket_close(t, ctx, 1);
+            return st;
+        }
         if (cudaStreamSynchronize(s0) != cudaSuccess) st = SE_ECUDA;
         if (st == SE_OK && h_report) *h_report = ctx.hreps[0];
         return st;
@@ -492,8 +639,9 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
         : make_chunks(g, lay, chunk_bytes, (hybrid || zin) ? kBlocksPerCta : 1);
     int dev = 0;
     cudaGetDevice(&dev);
-    HostCtx& ctx = host_ctx(dev);
+    HostCtx& ctx = host_ctx(dev, 1);
     std::lock_guard<std::mutex> lock(ctx.mu);
+    settle(ctx);
     if (ensure(ctx, n_streams)) return SE_ECUDA;
     if (chunks.size() > ctx.reps_cap) {
         for (auto s : ctx.streams) cudaStreamSynchronize(s);
@@ -529,12 +677,15 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
         }
     }
     se_report* reps = ctx.hreps;          // pinned: the per-chunk copies stay asynchronous
+    if (ticket_open(t, 1, ctx, chunks)) return SE_ECUDA;
+    if (t) t->hreps = ctx.hreps;
     auto issue = [&]() -> int {
         for (size_t k = 0; k < chunks.size(); ++k) {
             const Chunk& c = chunks[k];
             cudaStream_t s = ctx.streams[k % n_streams];
             Slot& sl = ctx.slots[k % n_streams];
             const se_layout& cl = cls[k];
+            if (ticket_wait(after, c.blk0, c.blk0 + c.nblk, s)) return SE_ECUDA;
             const uint64_t sizes[4] = {cgs[k].n_bytes, cl.a_bytes, cl.b_bytes, cl.c_bytes};
             const void* src[3] = {sl.buf[1], sl.buf[2], sl.buf[3]};
             for (int i = 0; i < 3; ++i) {
@@ -558,9 +709,14 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
                                             s) != cudaSuccess) ||
                 cudaMemcpyAsync(&reps[k], ctx.reps + k, sizeof(se_report), cudaMemcpyDeviceToHost, s) != cudaSuccess)
                 return SE_ECUDA;
+            if (ticket_chunk(t, k, s)) return SE_ECUDA;
         }
         return SE_OK;
     };
+    if (t) {                                  // asynchronous: issue directly, no final synchronisation
+        const int st = issue();
+        return st ? st : ticket_close(t, ctx, n_streams);
+    }
     const GraphKey gk = make_key(1, g, key, iv, h_out, h_a, h_b, h_c, chunk_bytes, n_streams);
     int status = run_chunks(ctx, gk, n_streams, issue);
     if (status == SE_OK && h_report) {
@@ -573,6 +729,61 @@ int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t
         }
     }
     return status;
+}
+
+extern "C" {
+
+int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_a,
+                          const void* h_b, const void* h_c, void* h_out, se_report* h_report, uint64_t chunk_bytes,
+                          uint32_t n_streams) {
+    return recover_host_impl(g, key, iv, h_a, h_b, h_c, h_out, h_report, chunk_bytes, n_streams, nullptr, nullptr);
+}
+
+int fragment_recover_host_async(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_a,
+                                const void* h_b, const void* h_c, void* h_out, uint64_t chunk_bytes,
+                                uint32_t n_streams, const se_host_ticket* after, se_host_ticket** out) {
+    if (!out) return SE_EINVAL;
+    *out = nullptr;
+    if (after && after->op != 0) return SE_EINVAL;
+    se_host_ticket* t = new se_host_ticket();
+    const int st = recover_host_impl(g, key, iv, h_a, h_b, h_c, h_out, nullptr, chunk_bytes, n_streams, after, t);
+    if (st != SE_OK) {
+        HostCtx* c = (HostCtx*)t->ctx;
+        if (c && c->pending == t) c->pending = nullptr;
+        for (uint32_t i = 0; c && i < c->streams.size(); ++i) cudaStreamSynchronize(c->streams[i]);
+        ticket_free(t);
+        return st;
+    }
+    *out = t;
+    return SE_OK;
+}
+
+int se_host_wait(se_host_ticket* t, se_report* h_report) {
+    if (!t) return SE_EINVAL;
+    HostCtx* c = (HostCtx*)t->ctx;
+    int st;
+    {
+        std::lock_guard<std::mutex> lock(c->mu);
+        if (c->pending == t) settle(*c);
+        for (cudaEvent_t e : t->tail)           // settled earlier by a later call: already complete
+            if (cudaEventSynchronize(e) != cudaSuccess) t->status = SE_ECUDA;
+        st = t->status;
+    }
+    if (h_report) {
+        h_report->first_bad_block = -1;
+        h_report->bad_blocks = 0;
+        if (t->op == 1 && st == SE_OK) {
+            for (size_t k = 0; k < t->reps.size(); ++k) {
+                if (t->reps[k].bad_blocks) {
+                    const int64_t fb = (int64_t)t->blk0[k] + t->reps[k].first_bad_block;
+                    if (h_report->first_bad_block < 0 || fb < h_report->first_bad_block) h_report->first_bad_block = fb;
+                    h_report->bad_blocks += t->reps[k].bad_blocks;
+                }
+            }
+        }
+    }
+    ticket_free(t);
+    return st;
 }
 
 }  // extern "C"

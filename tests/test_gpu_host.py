@@ -146,3 +146,42 @@ def test_host_hybrid_staging(dev, orc, W, offset):
     assert np.array_equal(a.numpy(), oa) and np.array_equal(b.numpy(), ob) and np.array_equal(c.numpy(), oc)
     back, rep = se.fragment_recover_host(a, b, c, n, W, L, KEY, IV, chunk_bytes=256 * 1024, n_streams=3)
     assert np.array_equal(back.numpy(), x) and rep == (-1, 0)
+
+
+@pytest.mark.parametrize("flags", [0, se.FLAG_PUBLIC_PLAIN])
+@pytest.mark.parametrize("n,W,L,chunk", [(1024 * 8 * 37 + 1234, 1024, 2, 64 * 1024), (6144 * 2048, 6144, 2, 0),
+                                         (4096 * 8 * 300, 4096, 3, 1 << 20)])
+def test_host_async_round_trip(dev, orc, n, W, L, chunk, flags):
+    """fragment_protect_host_async then fragment_recover_host_async chunk by
+    chunk after it: fragments equal the oracle's (and the blocking call's),
+    bytes round-trip, the report is clean."""
+    x = synth.random_bytes(n, n % 97)
+    hx = host(x)
+    (a, b, c), tp = se.fragment_protect_host_async(hx, W, L, KEY, IV, flags=flags, chunk_bytes=chunk, n_streams=3)
+    out, tr = se.fragment_recover_host_async(a, b, c, n, W, L, KEY, IV, flags=flags, chunk_bytes=chunk,
+                                             n_streams=3, after=tp)
+    assert tr.wait() == (-1, 0)
+    tp.wait()
+    assert np.array_equal(out.numpy(), x)
+    oa, ob, oc = orc.protect(x, W, L, KEY, IV, flags=flags)
+    assert np.array_equal(a.numpy(), oa) and np.array_equal(b.numpy(), ob) and np.array_equal(c.numpy(), oc)
+
+
+def test_host_async_report_and_back_to_back(dev, orc):
+    """Two protects in a row (the second settles the first), a recover of
+    damaged fragments: the report equals the oracle's."""
+    n, W, L = 1024 * 8 * 64, 1024, 2
+    x1, x2 = synth.random_bytes(n, 1), synth.random_bytes(n, 2)
+    (a1, b1, c1), t1 = se.fragment_protect_host_async(host(x1), W, L, KEY, IV, chunk_bytes=128 * 1024)
+    (a2, b2, c2), t2 = se.fragment_protect_host_async(host(x2), W, L, KEY, IV, chunk_bytes=128 * 1024)
+    t2.wait()
+    t1.wait()
+    oa, ob, oc = orc.protect(x1, W, L, KEY, IV)
+    assert np.array_equal(a1.numpy(), oa) and np.array_equal(c1.numpy(), oc)
+    c1[60 * 300 + 2] ^= 0x20
+    a1[5 * 1000] ^= 0x01
+    out, tr = se.fragment_recover_host_async(a1, b1, c1, n, W, L, KEY, IV, chunk_bytes=128 * 1024)
+    rep = tr.wait()
+    oback, orep = orc.recover(a1.numpy(), b1.numpy(), c1.numpy(), n, W, L, KEY, IV)
+    assert rep == orep and orep[1] > 0
+    assert np.array_equal(out.numpy(), oback)
