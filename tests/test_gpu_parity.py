@@ -354,3 +354,37 @@ def test_c5_full_workload_sampled(dev, orc):
     assert (reps.cpu().numpy() == np.array([-1, 0])).all()
     del files, outs, streams, batch
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("flags", [0, se.FLAG_PUBLIC_PLAIN])
+def test_protect_recover_capture_into_cuda_graph(dev, orc, flags):
+    """The device-resident calls are stream-ordered with no host
+    synchronisation or allocation, so a protect + recover round trip can be
+    captured once into a CUDA graph and replayed on new data (the per-CTA
+    path with its keystream kernels when masked, the tile kernels when
+    PUBLIC_PLAIN)."""
+    n, W, L = 1024 * 8 * 200, 1024, 2
+    x0 = synth.random_bytes(n, 11)
+    x = to_dev(x0, dev)
+    lay = se.fragment_layout(n, W, L)
+    a, b, c = (se._empty(lay[k], dev) for k in ("a_bytes", "b_bytes", "c_bytes"))
+    out = se._empty(n, dev)
+    rep = torch.empty(2, dtype=torch.int64, device=dev)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):                       # warm-up outside the capture (module loading)
+        se.fragment_protect(x, W, L, KEY, IV, flags=flags, out=(a, b, c), stream=s)
+        se.fragment_recover(a, b, c, n, W, L, KEY, IV, flags=flags, out=out, report=rep, stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        se.fragment_protect(x, W, L, KEY, IV, flags=flags, out=(a, b, c), stream=s)
+        se.fragment_recover(a, b, c, n, W, L, KEY, IV, flags=flags, out=out, report=rep, stream=s)
+    for seed in (12, 13):
+        x1 = synth.random_bytes(n, seed)
+        x.copy_(torch.from_numpy(x1))
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), x1) and rep.cpu().tolist() == [-1, 0]
+        oa, _, oc = orc.protect(x1, W, L, KEY, IV, flags=flags)
+        assert np.array_equal(a.cpu().numpy(), oa) and np.array_equal(c.cpu().numpy(), oc)
