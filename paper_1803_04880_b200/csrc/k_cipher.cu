@@ -10,7 +10,6 @@
 
 namespace se {
 
-constexpr int kCipherThreads = 256;
 #ifndef SE_LANE_THREADS
 #define SE_LANE_THREADS 1024
 #endif
@@ -85,20 +84,33 @@ __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ Ciphe
 // buffer; the fused batch kernel follows with programmatic serialization and
 // XORs its records in (no scratch).
 template <int ABITS>
-__global__ void __launch_bounds__(kCipherThreads) k_batch_keystream(const __grid_constant__ BatchParams bp) {
+__global__ void __launch_bounds__(kLaneThreads) k_batch_keystream(const __grid_constant__ BatchParams bp) {
     asm volatile("griddepcontrol.launch_dependents;");
-    __shared__ AesSmem aes;
-    aes_load_tables(aes, threadIdx.x, kCipherThreads);
+    extern __shared__ __align__(16) uint32_t lut[];
+    aes_load_lut(lut, threadIdx.x, kLaneThreads);          // lane-replicated table (as k_cipher_ctr)
     __syncthreads();
+    const AesLane lane = aes_lane(lut);
     const uint64_t total = bp.total_ctas * (uint64_t)ABITS;
-    const uint64_t stride = (uint64_t)gridDim.x * kCipherThreads;
-    for (uint64_t idx = (uint64_t)blockIdx.x * kCipherThreads + threadIdx.x; idx < total; idx += stride) {
+    const uint64_t stride = (uint64_t)gridDim.x * kLaneThreads;
+    for (uint64_t idx = (uint64_t)blockIdx.x * kLaneThreads + threadIdx.x; idx < total; idx += stride) {
         const uint64_t cta = idx / ABITS, t = idx - cta * ABITS;
-        uint32_t lo = 0, hi = bp.n_jobs - 1;               // largest job with cta_begin <= cta
+        // the job of this counter block: the warp searches once for its first
+        // lane's fused-kernel CTA; lanes whose CTA lies in a later job search alone
+        const uint64_t cta0 = __shfl_sync(0xffffffffu, cta, 0);
+        uint32_t lo = 0, hi = bp.n_jobs - 1;                   // largest job with cta_begin <= cta0
         while (lo < hi) {
             const uint32_t mid = (lo + hi + 1) / 2;
-            if (bp.jobs[mid].cta_begin <= cta) lo = mid;
+            if (bp.jobs[mid].cta_begin <= cta0) lo = mid;
             else hi = mid - 1;
+        }
+        if (lo + 1 < bp.n_jobs && bp.jobs[lo + 1].cta_begin <= cta) {
+            uint32_t l2 = lo + 1, h2 = bp.n_jobs - 1;
+            while (l2 < h2) {
+                const uint32_t mid = (l2 + h2 + 1) / 2;
+                if (bp.jobs[mid].cta_begin <= cta) l2 = mid;
+                else h2 = mid - 1;
+            }
+            lo = l2;
         }
         const se_job& job = bp.jobs[lo];
         const uint64_t rows = ((job.n_bytes + job.width - 1) / job.width + 7) / 8 * 8;
@@ -109,7 +121,7 @@ __global__ void __launch_bounds__(kCipherThreads) k_batch_keystream(const __grid
         const JobDerived& dv = *reinterpret_cast<const JobDerived*>(job.derived);
         uint32_t x[4];
         ctr_add(dv.ctr, lcta * ABITS + t, x);
-        aes128_block(aes, bp.base.rk, x);
+        aes128_block(lane, bp.base.rk, x);
         uint8_t* dst = job.a + off;
         if (off + 16 <= a_bytes) {
             *reinterpret_cast<uint4*>(dst) = make_uint4(bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3]));
@@ -141,14 +153,22 @@ int launch_batch_keystream(const BatchParams& bp, uint32_t a_bits, void* stream)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t total = bp.total_ctas * (uint64_t)a_bits;
-    const uint64_t want = (total + kCipherThreads - 1) / kCipherThreads;
-    const uint64_t cap = (uint64_t)sms * kKeystreamCtasPerSm;
+    const uint64_t want = (total + kLaneThreads - 1) / kLaneThreads;
+    const int lane_ctas = kCipherCtasPerSm < 2048 / kLaneThreads ? kCipherCtasPerSm : 2048 / kLaneThreads;
+    const uint64_t cap = (uint64_t)sms * lane_ctas;
     const unsigned grid = (unsigned)(want < cap ? want : cap);
     cudaStream_t s = (cudaStream_t)stream;
     if (grid == 0) return 0;
-    if (a_bits == 40) k_batch_keystream<40><<<grid, kCipherThreads, 0, s>>>(bp);
-    else if (a_bits == 160) k_batch_keystream<160><<<grid, kCipherThreads, 0, s>>>(bp);
-    else k_batch_keystream<10><<<grid, kCipherThreads, 0, s>>>(bp);
+    if (a_bits == 40) {
+        allow_lut<k_batch_keystream<40>>();
+        k_batch_keystream<40><<<grid, kLaneThreads, kAesLutBytes, s>>>(bp);
+    } else if (a_bits == 160) {
+        allow_lut<k_batch_keystream<160>>();
+        k_batch_keystream<160><<<grid, kLaneThreads, kAesLutBytes, s>>>(bp);
+    } else {
+        allow_lut<k_batch_keystream<10>>();
+        k_batch_keystream<10><<<grid, kLaneThreads, kAesLutBytes, s>>>(bp);
+    }
     note_launch();
     return (int)cudaGetLastError();
 }
