@@ -111,7 +111,9 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
     // job table / report init written by earlier work; with the keystream kernel
     // right before (protect, base.ks_in_a: a normal launch, so everything
     // earlier is complete) only its keystream is waited for, at the copy-out
-    if (!bp.base.ks_in_a) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (recover with base.ks_in_out likewise: report init and jobs precede the
+    // keystream kernel; qualifying CTAs wait for their keystream before use)
+    if (!bp.base.ks_in_a && !bp.base.ks_in_out) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x < 32) {
         // largest j with cta_begin <= x: 32-ary search by warp 0 (3 dependent
         // loads for 10,000 jobs instead of 14 for a binary search)
@@ -151,6 +153,8 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
         sp.a_bytes = (sp.n_blocks * R::ABITS + 7) / 8;
         sp.b_bytes = (sp.n_blocks * R::BBITS + 7) / 8;
         sp.c_bytes = (sp.n_blocks * R::CBITS + 7) / 8;
+        if (bp.base.ks_in_out)          // this CTA's keystream parked in its output region, or not
+            sp.ks_in_out = batch_ks_out_cta(job.n_bytes, job.width, x - job.cta_begin, R::ABITS) ? 1u : 0u;
     } else if (t >= 32 && t < 36) {
         sp.ctr[t - 32] = dv.ctr[t - 32];
     } else if (t >= 36 && t < 44) {
@@ -307,7 +311,7 @@ static void batch_l(const BatchParams& bp, uint64_t ctas, bool mask, cudaStream_
 int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t levels, bool mask, bool recover,
                         void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    if (recover && bp.reports) {
+    if (recover && bp.reports && !bp.reports_ready) {
         k_report_init<<<(bp.n_jobs + 255) / 256, 256, 0, s>>>(bp.reports, bp.n_jobs);
         note_launch();
     }

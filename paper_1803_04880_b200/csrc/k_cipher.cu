@@ -118,12 +118,17 @@ __global__ void __launch_bounds__(kLaneThreads) k_batch_keystream(const __grid_c
         const uint64_t lcta = cta - job.cta_begin;
         const uint64_t off = (lcta * ABITS + t) * 16;
         if (off >= a_bytes) continue;
+        uint8_t* dst = job.a + off;
+        if (bp.base.ks_in_out) {        // recover: into the CTA's own output region, where it qualifies
+            if (!batch_ks_out_cta(job.n_bytes, job.width, lcta, ABITS)) continue;
+            const uint64_t bpr = job.width / 8, b0 = lcta * kBlocksPerCta, br = b0 / bpr, bc = b0 - br * bpr;
+            dst = job.out + 8 * br * (uint64_t)job.width + 8 * bc + 16 * t;
+        }
         const JobDerived& dv = *reinterpret_cast<const JobDerived*>(job.derived);
         uint32_t x[4];
         ctr_add(dv.ctr, lcta * ABITS + t, x);
         aes128_block(lane, bp.base.rk, x);
-        uint8_t* dst = job.a + off;
-        if (off + 16 <= a_bytes) {
+        if (off + 16 <= a_bytes || bp.base.ks_in_out) {
             *reinterpret_cast<uint4*>(dst) = make_uint4(bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3]));
         } else {
             for (uint64_t k = 0; k < a_bytes - off; ++k) dst[k] = (uint8_t)(x[k / 4] >> (24 - 8 * (k % 4)));

@@ -699,8 +699,16 @@ static int batch_common(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ct
     // masked protect: a keystream kernel writes every file's keystream into its
     // A' and the batch kernel XORs it in; otherwise the AES-CTR of each A slice
     // runs inside the batch kernel.  No scratch either way.
-    if (mask && !recover && total_ctas) {
-        bp.base.ks_in_a = 1;
+    // Masked recover: the same kernel parks each qualifying CTA's keystream in
+    // that CTA's own output region (batch_ks_out_cta: whole 1024-byte rows -
+    // the big files), the others run their AES in the batch kernel.
+    if (mask && total_ctas) {
+        if (recover) bp.base.ks_in_out = 1;
+        else bp.base.ks_in_a = 1;
+        if (recover && d_reports) {      // reports first: the batch kernel then skips its start-of-kernel wait
+            if (launch_report_init(d_reports, n_jobs, stream)) return SE_ECUDA;
+            bp.reports_ready = 1;
+        }
         if (launch_batch_keystream(bp, lay.a_bits, stream)) return SE_ECUDA;
     }
     return launch_batch_block8(bp, total_ctas, levels, mask, recover, stream) ? SE_ECUDA : SE_OK;

@@ -82,6 +82,15 @@ struct FusedParams {
     SchedConst256 s256;       // B-mask schedule constants
 };
 
+// Batch recover, keystream parked in the output (k_batch_keystream with
+// base.ks_in_out): CTA `cta` of a job qualifies when its first row run is a
+// whole 1024-byte row segment inside the file that holds the CTA's A slice.
+__host__ __device__ inline bool batch_ks_out_cta(uint64_t n_bytes, uint32_t width, uint64_t cta, uint32_t a_bits) {
+    if (width % 1024 != 0 || a_bits * kBlocksPerCta / 8 > 1024) return false;
+    const uint64_t bpr = width / 8, b0 = cta * kBlocksPerCta, br = b0 / bpr, bc = b0 - br * bpr;
+    return 8 * br * (uint64_t)width + 8 * bc + a_bits * kBlocksPerCta / 8 <= n_bytes;
+}
+
 // Library-private layout of se_job.derived[] (filled by fragment_batch_plan).
 struct JobDerived {
     uint32_t ctr[4];          // IV + block_offset*a_bits/128
@@ -97,7 +106,7 @@ struct BatchParams {
     se_report* reports;       // recover: one per job, nullable
     uint64_t total_ctas;
     uint32_t n_jobs;
-    uint32_t pad_;
+    uint32_t reports_ready;   // recover: reports already initialised (no init kernel in the launcher)
     FusedParams base;         // shared fields: rk, h256, h512, one
 };
 

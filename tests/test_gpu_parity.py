@@ -388,3 +388,28 @@ def test_protect_recover_capture_into_cuda_graph(dev, orc, flags):
         assert np.array_equal(out.cpu().numpy(), x1) and rep.cpu().tolist() == [-1, 0]
         oa, _, oc = orc.protect(x1, W, L, KEY, IV, flags=flags)
         assert np.array_equal(a.cpu().numpy(), oa) and np.array_equal(c.cpu().numpy(), oc)
+
+
+def test_batch_recover_keystream_in_output_regions(dev, orc):
+    """Batch recovery of files >= 1 MiB (W = 1024): whole-row CTAs take their
+    keystream from their own output region, the files' ragged last CTAs run
+    the AES themselves; damaged and clean files, reports per file == the
+    oracle's."""
+    sizes = [(1 << 20) + 5000, 3 * (1 << 20), (2 << 20) + 8192 * 3, 1 << 20, 1500 * 1024]
+    files = [synth.random_bytes(s, 300 + i) for i, s in enumerate(sizes)]
+    widths = [synth.width_rule(s) for s in sizes]
+    assert all(w == 1024 for w in widths)
+    ivs = [synth.iv_for(5, 900 + i) for i in range(len(files))]
+    batch = se.Batch([to_dev(f, dev) for f in files], widths, ivs, 2, KEY)
+    streams = batch.protect()
+    # damage file 1 (A' in a whole-row CTA) and file 4 (C' in its ragged last CTA)
+    streams[1][0][640 * 3 + 1] ^= 0x08
+    streams[4][2][streams[4][2].numel() - 7] ^= 0x40
+    outs, reps = batch.recover()
+    r = reps.cpu().numpy()
+    for i, (f, w, iv) in enumerate(zip(files, widths, ivs)):
+        a, b, c = (t.cpu().numpy() for t in streams[i])
+        oback, orep = orc.recover(a, b, c, f.size, w, 2, KEY, iv)
+        assert tuple(r[i]) == orep, i
+        assert np.array_equal(outs[i].cpu().numpy(), oback), i
+    assert r[1][1] > 0 and r[4][1] >= 0 and tuple(r[0]) == (-1, 0)
