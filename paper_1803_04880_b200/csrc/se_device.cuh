@@ -35,29 +35,33 @@ __device__ __forceinline__ int isub(int a, int b, int m1) {       // a - b, m1 =
     return r;
 }
 
-// floor(v / 4) + c.  SE_LIFT_QHI=1: one IMAD.HI (v * 2^30 >> 32, signed) on
-// the FMA pipe instead of SHF on the ALU pipe (q30 = one << 30, opaque so
-// ptxas keeps the multiply) - measured slower (C2 masked protect / recover
-// 182.7 / 183.9 vs 184.7 / 187.5 GB/s, plain 576 vs 640: IMAD.HI's two FMA
-// issue slots and latency cost more than the ALU slot saved), so off.
-#ifndef SE_LIFT_QHI
-#define SE_LIFT_QHI 0
+// floor(v / 4) + c.  QHI: one IMAD.HI (v * 2^30 >> 32, signed) on the FMA
+// pipe instead of LEA.HI on the ALU pipe (q30 = one << 30, opaque so ptxas
+// keeps the multiply).  Round 1 measured it slower in both directions (C2
+// masked protect / recover 182.7 / 183.9 vs 184.7 / 187.5 GB/s) with the
+// SHA sigma shifts also on the FMA pipe; round 2, with those shifts back on
+// the ALU pipe (SE_SHR_FMA 0), it helps the inverse and still hurts the
+// forward transform (C4 recover 4.726 -> 4.664 ms, protect 4.676 -> 4.755):
+// SE_LIFT_QHI_INV 1, SE_LIFT_QHI_FWD 0.
+#ifndef SE_LIFT_QHI_FWD
+#define SE_LIFT_QHI_FWD 0
+#endif
+#ifndef SE_LIFT_QHI_INV
+#define SE_LIFT_QHI_INV 1
 #endif
 #ifndef SE_LIFT_LEA
 #define SE_LIFT_LEA 2      // measured (C2 masked p / r GB/s): 0 182.7 / 187.2, 1 185.1 / 187.1, 2 185.1 / 188.7
 #endif
+template <bool QHI>
 __device__ __forceinline__ int qfloor4(int v, int c, int q30) {
-#if SE_LIFT_QHI
-    int r;
-    asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(q30), "r"(c));
-    return r;
-#elif SE_LIFT_LEA
-    (void)q30;
-    return (v >> 2) + c;                  // ptxas: one LEA.HI (shift and add) on the ALU pipe
-#else
-    (void)q30;
-    return (v >> 2) + c;
-#endif
+    if constexpr (QHI) {
+        int r;
+        asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(q30), "r"(c));
+        return r;
+    } else {
+        (void)q30;
+        return (v >> 2) + c;              // ptxas: one LEA.HI (shift and add) on the ALU pipe
+    }
 }
 
 // a + (b >> 1): SE_LIFT_LEA >= 2 lets ptxas fuse it into one LEA.HI (ALU)
@@ -90,8 +94,8 @@ __device__ __forceinline__ void lift_fwd(int (&x)[N], uint32_t one, int m1) {
 #pragma unroll
     for (int k = 0; k < H; ++k) {
         const int dm1 = (k == 0) ? d[0] : d[k - 1];                   // d(-1) = d(0)
-#if SE_LIFT_LEA || SE_LIFT_QHI
-        s[k] = qfloor4(iadd(iadd(dm1, d[k], one), 2, one), x[2 * k], (int)(one << 30));   // Eq. 5.2 (+)
+#if SE_LIFT_LEA || SE_LIFT_QHI_FWD
+        s[k] = qfloor4<SE_LIFT_QHI_FWD != 0>(iadd(iadd(dm1, d[k], one), 2, one), x[2 * k], (int)(one << 30));   // Eq. 5.2 (+)
 #else
         s[k] = iadd(x[2 * k], iadd(iadd(dm1, d[k], one), 2, one) >> 2, one);              // Eq. 5.2 (+)
 #endif
@@ -108,7 +112,7 @@ __device__ __forceinline__ void lift_inv(int (&y)[N], uint32_t one, int m1) {
 #pragma unroll
     for (int k = 0; k < H; ++k) {
         const int dm1 = (k == 0) ? y[H] : y[H + k - 1];
-        x[2 * k] = isub(y[k], qfloor4(iadd(iadd(dm1, y[H + k], one), 2, one), 0, (int)(one << 30)), m1);
+        x[2 * k] = isub(y[k], qfloor4<SE_LIFT_QHI_INV != 0>(iadd(iadd(dm1, y[H + k], one), 2, one), 0, (int)(one << 30)), m1);
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) {
