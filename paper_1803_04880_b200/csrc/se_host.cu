@@ -53,6 +53,9 @@ struct Chunk {
 #ifndef SE_HOST_RAMP
 #define SE_HOST_RAMP 0
 #endif
+#ifndef SE_HOST_BALANCE
+#define SE_HOST_BALANCE 1
+#endif
 // chunk_bytes == 0: a quarter of the input, within [4 MiB, 16 MiB] — small
 // files need >= 3-4 chunks to overlap at all, large ones lose ~15 % of the
 // PCIe rate to per-chunk costs below ~16 MiB (tools/e2e_probe.py: 256 MiB
@@ -68,6 +71,14 @@ static std::vector<Chunk> make_chunks(const se_geom* g, const se_layout& lay, ui
     const uint64_t unit = ga / gcd64(ga, bpr);                 // block-rows per alignment unit
     const uint64_t row_bytes = 8ull * g->width;
     uint64_t rows_per = std::max<uint64_t>(1, chunk_bytes / row_bytes);
+    if (SE_HOST_BALANCE && rows_per < block_rows) {
+        // equal chunks near the requested size, no short remainder chunk (C2 at
+        // 4 MiB: 86 + 85 + 85 block rows, not 85 + 85 + 85 + 1, whose extra
+        // pipeline step cost as much as a full chunk's)
+        const uint64_t k = std::max<uint64_t>(1, (block_rows + rows_per / 2) / rows_per);
+        rows_per = (block_rows + k - 1) / k;
+        rows_per = (rows_per + unit - 1) / unit * unit;
+    }
     rows_per = std::max<uint64_t>(unit, rows_per / unit * unit);
     auto units = [&](uint64_t rows) { return std::max<uint64_t>(unit, rows / unit * unit); };
     // sizes in block rows: ramp up, full chunks, ramp down
