@@ -30,8 +30,23 @@ constexpr int kKsNarrowCtasPerSm = 1;
 // which then XOR it into the private fragment, see fused_cta.cuh).
 // LANE: the 64 KB lane-replicated table (standalone cipher), else the 5 KB
 // tables (keystream next to a running fused kernel).
+#ifdef SE_TRACE
+// diagnostic builds (tools/cta_trace.py): per CTA of the last keystream launch,
+// SM id and %globaltimer at entry and exit
+constexpr int kKsTraceMax = 4096;
+__device__ unsigned long long g_trace_ks[3 * kKsTraceMax];
+extern "C" int se_trace_ks_read(unsigned long long* host, int n_ctas) {
+    if (n_ctas > kKsTraceMax) n_ctas = kKsTraceMax;
+    return (int)cudaMemcpyFromSymbol(host, g_trace_ks, sizeof(unsigned long long) * 3 * n_ctas);
+}
+#endif
+
 template <bool LANE, int NT>
 __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ CipherParams p) {
+#ifdef SE_TRACE
+    unsigned long long tr0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+#endif
     // a dependent kernel launched with programmatic stream serialization may
     // start now; it waits (griddepcontrol.wait) before reading our output
     asm volatile("griddepcontrol.launch_dependents;");
@@ -75,6 +90,18 @@ __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ Ciphe
             }
         }
     }
+#ifdef SE_TRACE
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < kKsTraceMax) {
+        unsigned long long tr1;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_trace_ks[3 * blockIdx.x] = sm;
+        g_trace_ks[3 * blockIdx.x + 1] = tr0;
+        g_trace_ks[3 * blockIdx.x + 2] = tr1;
+    }
+#endif
 }
 
 
@@ -185,15 +212,23 @@ int launch_cipher_ctr(const CipherParams& p, void* stream) {
     const uint64_t nblk = (p.n + 15) / 16;
     const bool lane = p.in != nullptr || p.lane_lut;
     const bool narrow = SE_KS_NARROW && !lane && p.narrow;
-    const int nt = lane ? kLaneThreads : narrow ? kKsNarrowThreads : kKsThreads;
+    // lane table next to a fused kernel (p.narrow): one 128-thread CTA per SM,
+    // whose 4 warps fit beside the fused kernel's 5 CTAs (registers), so no
+    // SM holds back fused CTAs while the keystream runs
+    const bool lane_narrow = lane && p.in == nullptr && p.narrow;
+    const int nt = lane_narrow ? kKsNarrowThreads : lane ? kLaneThreads : narrow ? kKsNarrowThreads : kKsThreads;
     const uint64_t want = (nblk + nt - 1) / nt;
     // lane table: 64 KB per CTA -> at most 3 CTAs per SM, and 2048 threads per SM
     const int lane_ctas = kCipherCtasPerSm < 2048 / kLaneThreads ? kCipherCtasPerSm : 2048 / kLaneThreads;
-    const uint64_t cap = (uint64_t)sms * (lane ? lane_ctas : narrow ? kKsNarrowCtasPerSm : kKeystreamCtasPerSm);
+    const uint64_t cap = (uint64_t)sms * (lane_narrow ? 1 : lane ? lane_ctas : narrow ? kKsNarrowCtasPerSm
+                                                                                       : kKeystreamCtasPerSm);
     const unsigned grid = (unsigned)(want < cap ? want : cap);
     if (grid == 0) return 0;
     cudaStream_t s = (cudaStream_t)stream;
-    if (lane) {
+    if (lane_narrow) {
+        allow_lut<k_cipher_ctr<true, kKsNarrowThreads>>();
+        k_cipher_ctr<true, kKsNarrowThreads><<<grid, kKsNarrowThreads, kAesLutBytes, s>>>(p);
+    } else if (lane) {
         allow_lut<k_cipher_ctr<true, kLaneThreads>>();
         k_cipher_ctr<true, kLaneThreads><<<grid, kLaneThreads, kAesLutBytes, s>>>(p);
     } else if (narrow) {

@@ -309,6 +309,18 @@ static bool ks_out_enabled() {
     return v != 0;
 }
 
+// Masked per-CTA protect: the keystream kernel first (1), or AES inside the
+// fused kernel (0).  SE_PROT_KS in the environment overrides (measurement knob).
+static bool prot_ks_enabled(uint64_t n_blocks) {
+    static const int v = [] {
+        const char* e = getenv("SE_PROT_KS");
+        return e ? atoi(e) : -1;
+    }();
+    if (v >= 0) return v != 0;
+    (void)n_blocks;
+    return true;
+}
+
 static int launch_keystream_into(const FusedParams& p, uint8_t* out, uint64_t n, void* stream,
                                  se_report* init_report = nullptr, uint32_t cta_ablocks = 0) {
     CipherParams cp;
@@ -326,6 +338,15 @@ static int launch_keystream_into(const FusedParams& p, uint8_t* out, uint64_t n,
     // 1: the 64 KB lane-replicated table (measured: C4 masked protect 4.855 ->
     // 4.721 ms against the 5 KB tables, C2 / C3 slightly faster)
     cp.lane_lut = lut;
+    // SE_KS_LANE_NARROW=1: one 128-thread lane-table CTA per SM beside the
+    // fused kernel instead of 1024-thread CTAs on few SMs.  Measured slower
+    // (C2 89.6 vs 92.5 GB/s, C4 112.8 vs 114.9: the narrow keystream
+    // finishes late and the fused CTAs wait for it at copy-out), so off.
+    static const int narrow = [] {
+        const char* e = getenv("SE_KS_LANE_NARROW");
+        return e ? atoi(e) : 0;
+    }();
+    cp.narrow = narrow;
     memcpy(cp.ctr, p.ctr, sizeof cp.ctr);
     memcpy(cp.rk, p.rk, sizeof cp.rk);
     return launch_cipher_ctr(cp, stream);
@@ -337,11 +358,12 @@ static int report_init(se_report* r, cudaStream_t s) {
     return launch_report_init(r, 1, s) ? SE_ECUDA : SE_OK;
 }
 
-// Protect (rows a1-a9).  BLOCK8 device buffers: the persistent tile kernel
-// (k_tile.cu).  BLOCK8 with o.mapped (fragments in page-locked host memory,
-// se_host.cu): the per-CTA kernel, whose plain stores suit PCIe writes.
-// FULL: whole-matrix transform into o.ws, then the footprint kernel.  AES-CTR
-// of the A slice runs inside the fused kernels in every case.
+// Protect (rows a1-a9).  BLOCK8 on device buffers: PUBLIC_PLAIN on the
+// persistent tile kernel (k_tile.cu, AES warps inside), masked on the per-CTA
+// kernel (k_block8.cu) behind the keystream kernel.  BLOCK8 with o.mapped
+// (fragments in page-locked host memory, se_host.cu): the per-CTA kernel with
+// in-kernel AES, whose plain stores suit PCIe writes.  FULL: whole-matrix
+// transform into o.ws, then the footprint kernel (in-kernel AES).
 int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in, void* d_a,
                  void* d_b, void* d_c, const ImplOpts& o, void* stream) {
     se_layout lay;
@@ -361,7 +383,7 @@ int protect_impl(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], 
         // per-CTA kernel; masked: the keystream kernel writes A' first and the
         // fused kernel XORs it in at its copy-out (programmatic launch overlap);
         // unmasked (and host-mapped A'): AES inside the fused kernel
-        if (mask && !o.mapped) {
+        if (mask && !o.mapped && prot_ks_enabled(lay.n_blocks)) {
             p.ks_in_a = 1;
             if (launch_keystream_into(p, p.a, lay.a_bytes, stream)) return SE_ECUDA;
         }

@@ -47,13 +47,44 @@ def report(name, n):
     print("   start histogram (12 bins over span):", hist.tolist())
 
 
-for _ in range(5):
-    a, b, c = se.fragment_protect(x, W, L, key, iv)
-torch.cuda.synchronize()
+fks = lib.se_trace_ks_read
+fks.argtypes = [ctypes.c_void_p, ctypes.c_int]
+flush = torch.empty(63 << 20, dtype=torch.int32, device="cuda")     # 252 MB > L2, as bench.py
+
+
+def timed(fn):
+    # as bench.py's timed loop: L2 flushed, then CUDA events around the call
+    ms = []
+    for k in range(5):
+        flush.fill_(k)
+        flush.amax()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1) * 1e3)
+    return out, ms
+
+
+def ks_span(n_fused):
+    buf = np.zeros(3 * 4096, np.uint64)
+    assert fks(buf.ctypes.data, 4096) == 0
+    t = buf.reshape(-1, 3).astype(np.int64)
+    t = t[t[:, 1] > 0]
+    _, f0, f1 = trace(n_fused)
+    base = min(t[:, 1].min(), f0.min())
+    print(f"   keystream CTAs (this call): {len(t)}, span {(t[:, 1].min() - base) / 1e3:.1f}..{(t[:, 2].max() - base) / 1e3:.1f} us; "
+          f"fused CTAs {(f0.min() - base) / 1e3:.1f}..{(f1.max() - base) / 1e3:.1f} us (same time base)")
+
+
 nb = x.numel() // 64
 BPC = int(__import__("os").environ.get("BPC", "128"))
+(a, b, c), ms = timed(lambda: se.fragment_protect(x, W, L, key, iv))
+print(f"protect call (events, L2 flushed): {[round(v, 1) for v in ms]} us")
 report("protect", (nb + BPC - 1) // BPC)
-for _ in range(5):
-    y, rep = se.fragment_recover(a, b, c, x.numel(), W, L, key, iv)
-torch.cuda.synchronize()
+ks_span((nb + BPC - 1) // BPC)
+(y, rep), ms = timed(lambda: se.fragment_recover(a, b, c, x.numel(), W, L, key, iv))
+print(f"recover call (events, L2 flushed): {[round(v, 1) for v in ms]} us")
 report("recover", (nb + BPC - 1) // BPC)
+ks_span((nb + BPC - 1) // BPC)
