@@ -31,6 +31,10 @@
 
 #include "fused_cta.cuh"
 
+#ifndef SE_TILE_ORV_IMAD
+#define SE_TILE_ORV_IMAD 1      // measured: C4 PUBLIC_PLAIN recover 0.654 -> 0.638 ms (tools/gpu_r2_call38.sh)
+#endif
+
 namespace se {
 
 // TILE: masked kernels (ALU-bound on SHA-2) 512 blocks = 16 consumer warps;
@@ -292,7 +296,8 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
                 if (MASK) dwt8_fwd<L>(v, p.one);                                  // rows a2-a4 (adds on the FMA pipe)
                 else dwt8_fwd_lean<L>(v, p.one);                                  // rows a2-a4 (fewest instructions)
                 for_each_field<L, 0>([&](int s, int pos, int i, int j, int w) {     // row a5
-                    const int off = (s == 0) ? (1 << (w - 1)) - 128 : (1 << (w - 1));   // C9 (+ C8 on LL)
+                    // C9 (+ C8 on LL); the mixed-pipe forward lifting leaves +1 on every band but LL
+                    const int off = (s == 0) ? (1 << (w - 1)) - 128 : (1 << (w - 1)) - (MASK ? 0 : (SE_LEAN_MIX & 1));
                     if (MASK) {
                         if (s == 0) put_field(A, pos, v[i][j], off, w, p.one);
                         else if (s == 1) put_field(B, pos, v[i][j], off, w, p.one);
@@ -370,12 +375,25 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
                     });
                     dwt8_inv_lean<L>(v, p.one);
                 }
+                // a reconstructed sample outside [0, 255]?
+#if SE_TILE_ORV_IMAD
+                // pairs as v_a + 2^16 v_b (IMAD, FMA pipe): for |v| < 2^15 the
+                // word has bits 8-15 or 24-31 set iff v_a or v_b is outside
+                // [0, 255] (a negative v_a sets bit 15), so half the ORs
+                int orv = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; j += 2) orv |= imad(v[i][j + 1], (int)(p.one << 16), v[i][j]);
+                bad = (orv & 0xff00ff00) != 0;
+#else
                 int orv = 0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) orv |= v[i][j];
-                bad = (orv & ~0xff) != 0;      // a reconstructed sample outside [0, 255]
+                bad = (orv & ~0xff) != 0;
+#endif
                 if (fast) {
                     const uint32_t base = map.base(p, t, ct, T::TILE), st = map.stride(p, T::TILE);
 #pragma unroll

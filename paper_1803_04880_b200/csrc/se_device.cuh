@@ -232,6 +232,68 @@ __device__ __forceinline__ void lift_inv_lean(int (&y)[N], uint32_t one) {
     for (int k = 0; k < N; ++k) y[k] = x[k];
 }
 
+// Mixed-pipe lean lifting (SE_LEAN_MIX bit 0: forward, bit 1: inverse): the
+// sums move to the FMA pipe as IMADs by an opaque +-1 and each lift keeps one
+// ALU op, the shift-and-add (LEA.HI).  Forward:
+//   n_e = 3 - x_e                      (IMAD; each even sample serves two predicts)
+//   u   = 3 - x_l - x_r = IMAD(x_l, -1, n_r)
+//   d'  = x_o + (u >> 1) = d + 1       (LEA.HI; floor((3 - m) / 2) = 1 + floor((1 - m) / 2) = 1 - floor(m / 2))
+//   s   = x_e + ((d'_l + d'_r) >> 2)   (IMAD + LEA.HI; d'_l + d'_r = d_l + d_r + 2)
+// so every high-pass output carries +1 (d' = d + 1).  Lifting passes a
+// constant offset of its inputs through the update and cancels it in the
+// predict, so after dwt8_fwd_mix every band but the final LL holds v + 1
+// (the caller folds the -1 into its field offsets); LL is exact.
+// Inverse (exact values in and out):
+//   m_d = 1 - d                        (IMAD; each d serves two updates)
+//   x_e = s + ((1 - d_l - d_r) >> 2)   (IMAD(d_l, -1, m_r) + LEA.HI)
+//   x_o = d + ((x_l + x_r) >> 1)       (IMAD + LEA.HI)
+// Measured (C4 PUBLIC_PLAIN tile kernels, tools/gpu_r2_call37.sh): lean
+// protect / recover 0.669 / 0.689 ms, mixed 0.627 / 0.653 ms (791 -> 839 GB/s
+// round trip): SE_LEAN_MIX 3.
+#ifndef SE_LEAN_MIX
+#define SE_LEAN_MIX 3
+#endif
+__device__ __forceinline__ int imad(int a, int b, int c) {      // a * b + c on the FMA pipe (b opaque)
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+template <int N>
+__device__ __forceinline__ void lift_fwd_mix(int (&x)[N], int m1) {
+    constexpr int H = N / 2;
+    int n[H] = {}, s[H], d[H];
+#pragma unroll
+    for (int k = 1; k < H; ++k) n[k] = imad(x[2 * k], m1, 3);                    // 3 - x_e (n[0] unused)
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+        if (2 * k + 2 < N) d[k] = x[2 * k + 1] + (imad(x[2 * k], m1, n[k + 1]) >> 1);   // Eq. 5.1, +1
+        else d[k] = x[2 * k + 1] - x[2 * k] + 1;                                 // x(N) = x(N-2), +1
+    }
+#pragma unroll
+    for (int k = 0; k < H; ++k) s[k] = x[2 * k] + (imad(k == 0 ? d[0] : d[k - 1], -m1, d[k]) >> 2);   // Eq. 5.2
+#pragma unroll
+    for (int k = 0; k < H; ++k) { x[k] = s[k]; x[H + k] = d[k]; }
+}
+
+template <int N>
+__device__ __forceinline__ void lift_inv_mix(int (&y)[N], int m1) {
+    constexpr int H = N / 2;
+    int x[N], m[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) m[k] = imad(y[H + k], m1, 1);                   // 1 - d
+#pragma unroll
+    for (int k = 0; k < H; ++k)
+        x[2 * k] = y[k] + (imad(k == 0 ? y[H] : y[H + k - 1], m1, m[k]) >> 2);
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+        if (2 * k + 2 < N) x[2 * k + 1] = y[H + k] + (imad(x[2 * k], -m1, x[2 * k + 2]) >> 1);
+        else x[2 * k + 1] = imad(x[2 * k], -m1, y[H + k]);
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) y[k] = x[k];
+}
+
 template <int M, bool INV>
 __device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8], uint32_t one) {
     // forward: rows then columns (C5); inverse: columns then rows
@@ -243,8 +305,13 @@ __device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8], uint32_t one) {
             int t[M];
 #pragma unroll
             for (int b = 0; b < M; ++b) t[b] = rows ? v[a][b] : v[b][a];
-            if (INV) lift_inv_lean<M>(t, one);
-            else lift_fwd_lean<M>(t);
+            if (INV) {
+                if constexpr ((SE_LEAN_MIX & 2) != 0) lift_inv_mix<M>(t, -(int)one);
+                else lift_inv_lean<M>(t, one);
+            } else {
+                if constexpr ((SE_LEAN_MIX & 1) != 0) lift_fwd_mix<M>(t, -(int)one);
+                else lift_fwd_lean<M>(t);
+            }
 #pragma unroll
             for (int b = 0; b < M; ++b) {
                 if (rows) v[a][b] = t[b];

@@ -108,6 +108,26 @@ def test_tile_report_matches_oracle(dev, orc):
     assert np.array_equal(back.cpu().numpy(), oback)
 
 
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_tile_plain_garbage_fragments(dev, orc, L):
+    """PUBLIC_PLAIN recovery of random fragments: every field at arbitrary
+    values, so the inverse transform reaches its extreme magnitudes and most
+    blocks fail the [0, 255] range check (the only damage signal without
+    masks).  Recovered bytes and report equal the oracle's."""
+    n, W = 512 * 64 * 4 + 2000, 1024
+    lay = orc.layout(n, W, L)
+    rng = np.random.default_rng(40 + L)
+    a, b, c = (rng.integers(0, 256, lay[k], dtype=np.uint8) for k in ("a_bytes", "b_bytes", "c_bytes"))
+    if L == 2:                                 # extreme fields: all ones / all zeros on some blocks
+        c[:3000] = 0xFF
+        b[:1000] = 0x00
+    back, rep = se.fragment_recover(to_dev(a, dev), to_dev(b, dev), to_dev(c, dev), n, W, L, KEY, IV,
+                                    flags=se.FLAG_PUBLIC_PLAIN)
+    oback, orep = orc.recover(a, b, c, n, W, L, KEY, IV, flags=se.FLAG_PUBLIC_PLAIN)
+    assert tuple(rep.cpu().tolist()) == orep and orep[1] > 0
+    assert np.array_equal(back.cpu().numpy(), oback)
+
+
 def test_tile_streams_on_one_stream_back_to_back(dev, orc):
     """Protect then recover then protect again on one non-default stream with
     no host synchronisation in between (programmatic dependent launch: each
