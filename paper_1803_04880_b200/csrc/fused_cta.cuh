@@ -6,6 +6,14 @@
 #include <cuda_runtime.h>
 
 #include "se_device.cuh"
+
+// Masked per-CTA kernels: mixed-pipe lifting (bit 0 forward, bit 1 inverse,
+// se_device.cuh lift_*_mix) and the paired range check (bit 2).  Measured
+// (C4, tools/gpu_r2_call40.sh): forward protect 4.684 -> 4.665 ms, inverse
+// recover 4.668 -> 4.653 ms, paired check recover 4.668 -> 4.714 ms: 3.
+#ifndef SE_MASK_MIX
+#define SE_MASK_MIX 3
+#endif
 #include "sha2_spec.cuh"
 
 namespace se {
@@ -436,7 +444,11 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
         int v[8][8];
         if constexpr (MODE == 0) {
             load_block(p.in, p.n_bytes, p.width, br, bc, v);
+#if SE_MASK_MIX & 1
+            dwt8_fwd_mix<L>(v, p.one);                                      // rows a2-a4 (+1 on all but LL)
+#else
             dwt8_fwd<L>(v, p.one);                                          // rows a2-a4
+#endif
         } else {
             footprint_full<L, false>(p, br, bc, v);                         // row a11
         }
@@ -449,7 +461,8 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
         for (int k = 0; k < R::CW; ++k) C[k] = 0;
         for_each_field<L, MODE>([&](int s, int pos, int i, int j, int w) {  // row a5
             // offset-binary (C9); in BLOCK8 LL_L also absorbs the -128 centering (C8)
-            const int off = (s == 0 && MODE == 0) ? (1 << (w - 1)) - 128 : (1 << (w - 1));
+            const int off = (s == 0 && MODE == 0) ? (1 << (w - 1)) - 128
+                                                  : (1 << (w - 1)) - (MODE == 0 ? (SE_MASK_MIX & 1) : 0);
             if (s == 0) put_field(A, pos, v[i][j], off, w, p.one);
             else if (s == 1) put_field(B, pos, v[i][j], off, w, p.one);
             else put_field(C, pos, v[i][j], off, w, p.one);
@@ -605,13 +618,21 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
         });
         const uint64_t br = blk / p.bpr, bc = blk - br * p.bpr;
         if constexpr (MODE == 0) {
+#if SE_MASK_MIX & 2
+            dwt8_inv_mix<L>(v, p.one);                                       // uncentered bytes
+#else
             dwt8_inv<L>(v, p.one);                                           // uncentered bytes
+#endif
+#if SE_MASK_MIX & 4
+            bad = out_of_range_pairs(v, p.one);   // any sample outside [0, 255]
+#else
             int orv = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) orv |= v[i][j];
             bad = (orv & ~0xff) != 0;      // any sample outside [0, 255]
+#endif
 #if SE_REC_STAGE
             if (staged) {
 #pragma unroll

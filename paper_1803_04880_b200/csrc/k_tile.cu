@@ -377,15 +377,7 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
                 }
                 // a reconstructed sample outside [0, 255]?
 #if SE_TILE_ORV_IMAD
-                // pairs as v_a + 2^16 v_b (IMAD, FMA pipe): for |v| < 2^15 the
-                // word has bits 8-15 or 24-31 set iff v_a or v_b is outside
-                // [0, 255] (a negative v_a sets bit 15), so half the ORs
-                int orv = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; j += 2) orv |= imad(v[i][j + 1], (int)(p.one << 16), v[i][j]);
-                bad = (orv & 0xff00ff00) != 0;
+                bad = out_of_range_pairs(v, p.one);
 #else
                 int orv = 0;
 #pragma unroll

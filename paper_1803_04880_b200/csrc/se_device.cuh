@@ -294,7 +294,7 @@ __device__ __forceinline__ void lift_inv_mix(int (&y)[N], int m1) {
     for (int k = 0; k < N; ++k) y[k] = x[k];
 }
 
-template <int M, bool INV>
+template <int M, bool INV, int MIX = SE_LEAN_MIX>
 __device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8], uint32_t one) {
     // forward: rows then columns (C5); inverse: columns then rows
 #pragma unroll
@@ -306,10 +306,10 @@ __device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8], uint32_t one) {
 #pragma unroll
             for (int b = 0; b < M; ++b) t[b] = rows ? v[a][b] : v[b][a];
             if (INV) {
-                if constexpr ((SE_LEAN_MIX & 2) != 0) lift_inv_mix<M>(t, -(int)one);
+                if constexpr ((MIX & 2) != 0) lift_inv_mix<M>(t, -(int)one);
                 else lift_inv_lean<M>(t, one);
             } else {
-                if constexpr ((SE_LEAN_MIX & 1) != 0) lift_fwd_mix<M>(t, -(int)one);
+                if constexpr ((MIX & 1) != 0) lift_fwd_mix<M>(t, -(int)one);
                 else lift_fwd_lean<M>(t);
             }
 #pragma unroll
@@ -333,6 +333,35 @@ __device__ __forceinline__ void dwt8_inv_lean(int (&v)[8][8], uint32_t one) {
     if (L >= 3) dwt2_level_lean<2, true>(v, one);
     if (L >= 2) dwt2_level_lean<4, true>(v, one);
     dwt2_level_lean<8, true>(v, one);
+}
+
+// The mixed-pipe lifting on its own (the masked kernels, SE_MASK_MIX): the
+// forward leaves +1 on every band but LL (see lift_fwd_mix).
+template <int L>
+__device__ __forceinline__ void dwt8_fwd_mix(int (&v)[8][8], uint32_t one) {
+    dwt2_level_lean<8, false, 3>(v, one);
+    if (L >= 2) dwt2_level_lean<4, false, 3>(v, one);
+    if (L >= 3) dwt2_level_lean<2, false, 3>(v, one);
+}
+
+template <int L>
+__device__ __forceinline__ void dwt8_inv_mix(int (&v)[8][8], uint32_t one) {
+    if (L >= 3) dwt2_level_lean<2, true, 3>(v, one);
+    if (L >= 2) dwt2_level_lean<4, true, 3>(v, one);
+    dwt2_level_lean<8, true, 3>(v, one);
+}
+
+// Any of 64 reconstructed samples outside [0, 255]?  Pairs as v_a + 2^16 v_b
+// (IMAD, FMA pipe): for |v| < 2^15 (every sample the inverse can produce from
+// <= 11-bit fields at L <= 3) the word has a bit of 0xff00ff00 set iff v_a or
+// v_b is outside [0, 255] (a negative v_a sets bit 15), so half the ORs.
+__device__ __forceinline__ bool out_of_range_pairs(const int (&v)[8][8], uint32_t one) {
+    int orv = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) orv |= imad(v[i][j + 1], (int)(one << 16), v[i][j]);
+    return (orv & 0xff00ff00) != 0;
 }
 
 // ------------------------------------------------------------------ records
