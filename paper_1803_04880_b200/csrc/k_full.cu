@@ -46,32 +46,86 @@ struct FStream {
     static constexpr int H = L == 3 ? 16 : 8;                   // halo rows (>= 2(2^L - 1), multiple of 8)
 };
 
+struct StreamCtx {
+    int one, m1;          // 1 and -1, opaque to ptxas (DwtParams::one): IMAD operands
+    int W, R;
+    int c0;               // first column of the lane's chunk (outside [0, W): a dummy lane)
+    bool out_lane;        // lane stores (not an overlap lane, chunk inside the matrix)
+    int A, B;             // output rows of the segment (global, multiples of 8)
+    int row0, rows_out;   // the call's output window (local Mallat / byte offsets)
+    int src0, src_rows;   // inverse: rows present in the local Mallat source
+};
+
+// Lifting steps.  SE_FULL_MIX bit 0 (forward) / bit 1 (inverse): the sums as
+// IMADs by an opaque +-1 (FMA pipe), leaving one shift-and-add (LEA.HI, ALU
+// pipe) per lift, exact values (tests/test_kernel_arith.py checks the
+// identities: -floor(m / 2) = floor((1 - m) / 2), -floor((m + 2) / 4) =
+// floor((1 - m) / 4)); otherwise plain adds and shifts, which ptxas already
+// splits between IADD3 and IMAD.IADD.  Measured (C4-FULL round trip,
+// tools/gpu_r2_call42.sh): plain 98.85, forward mixed 98.53, inverse mixed
+// 98.77, both 98.45 GB/s — so 0.
+#ifndef SE_FULL_MIX
+#define SE_FULL_MIX 0
+#endif
+__device__ __forceinline__ int fm_pred(int xo, int xl, int xr, const StreamCtx& c) {   // xo - floor((xl + xr) / 2)
+#if SE_FULL_MIX & 1
+    return xo + (imad(xl, c.m1, imad(xr, c.m1, 1)) >> 1);
+#else
+    (void)c;
+    return xo - ((xl + xr) >> 1);
+#endif
+}
+__device__ __forceinline__ int fm_upd(int xe, int dl, int dr, const StreamCtx& c) {    // xe + floor((dl + dr + 2) / 4)
+#if SE_FULL_MIX & 1
+    return xe + (imad(dl, c.one, imad(dr, c.one, 2)) >> 2);
+#else
+    (void)c;
+    return xe + ((dl + dr + 2) >> 2);
+#endif
+}
+__device__ __forceinline__ int fm_iupd(int sv, int dl, int dr, const StreamCtx& c) {   // sv - floor((dl + dr + 2) / 4)
+#if SE_FULL_MIX & 2
+    return sv + (imad(dl, c.m1, imad(dr, c.m1, 1)) >> 2);
+#else
+    (void)c;
+    return sv - ((dl + dr + 2) >> 2);
+#endif
+}
+__device__ __forceinline__ int fm_ipred(int d, int xl, int xr, const StreamCtx& c) {   // d + floor((xl + xr) / 2)
+#if SE_FULL_MIX & 2
+    return d + (imad(xl, c.one, xr) >> 1);
+#else
+    (void)c;
+    return d + ((xl + xr) >> 1);
+#endif
+}
+
 // Forward 1-D lifting of one level along a row: v holds NV samples of the
 // level (columns gcol .. gcol + NV - 1 of a level row of Nl samples), even =
 // s, odd = d on return.  Predict (Eq. 5.1) then update (Eq. 5.2, "+").
 template <int NV>
-__device__ __forceinline__ void hfwd(int (&v)[NV], int gcol, int Nl) {
+__device__ __forceinline__ void hfwd(int (&v)[NV], int gcol, int Nl, const StreamCtx& c) {
     int xr = __shfl_down_sync(kLanes, v[0], 1);                // next chunk's first sample
     if (gcol + NV >= Nl) xr = v[NV - 2];                        // x(N) = x(N - 2)
 #pragma unroll
-    for (int m = 1; m < NV; m += 2) v[m] -= (v[m - 1] + (m + 1 < NV ? v[m + 1] : xr)) >> 1;
+    for (int m = 1; m < NV; m += 2) v[m] = fm_pred(v[m], v[m - 1], m + 1 < NV ? v[m + 1] : xr, c);
     int dl = __shfl_up_sync(kLanes, v[NV - 1], 1);             // previous chunk's last d
     if (gcol == 0) dl = v[1];                                   // d(-1) = d(0)
 #pragma unroll
-    for (int m = 0; m < NV; m += 2) v[m] += ((m ? v[m - 1] : dl) + v[m + 1] + 2) >> 2;
+    for (int m = 0; m < NV; m += 2) v[m] = fm_upd(v[m], m ? v[m - 1] : dl, v[m + 1], c);
 }
 
 // Inverse of hfwd: undo the update, then the predict.
 template <int NV>
-__device__ __forceinline__ void hinv(int (&v)[NV], int gcol, int Nl) {
+__device__ __forceinline__ void hinv(int (&v)[NV], int gcol, int Nl, const StreamCtx& c) {
     int dl = __shfl_up_sync(kLanes, v[NV - 1], 1);
     if (gcol == 0) dl = v[1];
 #pragma unroll
-    for (int m = 0; m < NV; m += 2) v[m] -= ((m ? v[m - 1] : dl) + v[m + 1] + 2) >> 2;
+    for (int m = 0; m < NV; m += 2) v[m] = fm_iupd(v[m], m ? v[m - 1] : dl, v[m + 1], c);
     int xr = __shfl_down_sync(kLanes, v[0], 1);
     if (gcol + NV >= Nl) xr = v[NV - 2];
 #pragma unroll
-    for (int m = 1; m < NV; m += 2) v[m] += (v[m - 1] + (m + 1 < NV ? v[m + 1] : xr)) >> 1;
+    for (int m = 1; m < NV; m += 2) v[m] = fm_ipred(v[m], v[m - 1], m + 1 < NV ? v[m + 1] : xr, c);
 }
 
 // NH int16 values (v[OFF], v[OFF + 2], ...) -> 2*NH bytes at g (aligned)
@@ -89,14 +143,7 @@ __device__ __forceinline__ void st_band(int16_t* g, const int (&v)[NV]) {
     }
 }
 
-struct StreamCtx {
-    int W, R;
-    int c0;               // first column of the lane's chunk (outside [0, W): a dummy lane)
-    bool out_lane;        // lane stores (not an overlap lane, chunk inside the matrix)
-    int A, B;             // output rows of the segment (global, multiples of 8)
-    int row0, rows_out;   // the call's output window (local Mallat / byte offsets)
-    int src0, src_rows;   // inverse: rows present in the local Mallat source
-};
+
 
 // ---------------------------------------------------------------- forward
 
@@ -161,13 +208,13 @@ __device__ __forceinline__ void fwd_pair(FwdState& st, const int (&xn)[8 >> (l -
     auto& s = fline<l>(st);
     int d[NV], sv[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) d[i] = s.O[i] - ((s.E[i] + xn[i]) >> 1);
+    for (int i = 0; i < NV; ++i) d[i] = fm_pred(s.O[i], s.E[i], xn[i], c);
     if (s.n == 2) {                                             // first pair: d(-1) = d(0)
 #pragma unroll
         for (int i = 0; i < NV; ++i) s.D[i] = d[i];
     }
 #pragma unroll
-    for (int i = 0; i < NV; ++i) sv[i] = s.E[i] + ((s.D[i] + d[i] + 2) >> 2);
+    for (int i = 0; i < NV; ++i) sv[i] = fm_upd(s.E[i], s.D[i], d[i], c);
 #pragma unroll
     for (int i = 0; i < NV; ++i) s.D[i] = d[i];
     const int k = ((st.kf >> (l - 1)) + s.n - 2) >> 1;
@@ -178,7 +225,7 @@ template <int L, int l, int QM>
 __device__ __forceinline__ void fwd_push(FwdState& st, int (&x)[8 >> (l - 1)], int16_t* coef, const StreamCtx& c) {
     constexpr int NV = 8 >> (l - 1);
     auto& s = fline<l>(st);
-    hfwd<NV>(x, c.c0 >> (l - 1), c.W >> (l - 1));             // row pass of level l
+    hfwd<NV>(x, c.c0 >> (l - 1), c.W >> (l - 1), c);             // row pass of level l
     if constexpr ((QM & 1) == 0) {
         if (s.n >= 2) fwd_pair<L, l, QM>(st, x, coef, c);
 #pragma unroll
@@ -229,6 +276,8 @@ __device__ __forceinline__ void stream_ctx(StreamCtx& c, const DwtParams& p, int
     const int wid = (int)blockIdx.x * kStreamWarps + (int)(threadIdx.x >> 5);
     const int cg = wid % ncg;
     sg = wid / ncg;
+    c.one = (int)p.one;
+    c.m1 = -(int)p.one;
     c.W = (int)p.width;
     c.R = (int)p.rows;
     c.c0 = 8 * (cg * USE - HC + lane);
@@ -411,7 +460,7 @@ template <int L, int l, int T>
 __device__ __forceinline__ void inv_emit(InvState& st, int (&v)[8 >> (l - 1)], int j, InvPre& pre, const InvOut& o,
                                          const StreamCtx& c) {
     constexpr int NV = 8 >> (l - 1);
-    hinv<NV>(v, c.c0 >> (l - 1), c.W >> (l - 1));
+    hinv<NV>(v, c.c0 >> (l - 1), c.W >> (l - 1), c);
     if constexpr (l == 1) {
         if (c.out_lane && j >= c.A && j < c.B) {
             uint32_t w[2] = {0, 0};
@@ -483,11 +532,11 @@ __device__ __forceinline__ void inv_push(InvState& st, const int (&sr)[8 >> (l -
     }
     int x[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) x[i] = sr[i] - ((s.D[i] + dr[i] + 2) >> 2);
+    for (int i = 0; i < NV; ++i) x[i] = fm_iupd(sr[i], s.D[i], dr[i], c);
     if (s.n != 0) {
         int xo[NV];
 #pragma unroll
-        for (int i = 0; i < NV; ++i) xo[i] = s.D[i] + ((s.X[i] + x[i]) >> 1);
+        for (int i = 0; i < NV; ++i) xo[i] = fm_ipred(s.D[i], s.X[i], x[i], c);
         inv_emit<L, l, (T >= 0 ? 2 * T : -1)>(st, xo, 2 * k - 1, pre, o, c);
     }
 #pragma unroll
