@@ -1,0 +1,5 @@
+mkdir -p gpurun_out/c43
+for cfg in 2 3 4; do for rep in 1 2; do for v in paper_1803_04880_b200/libse.so variants/*.so; do
+  SE_LIB_PATH=$v timeout 300 python bench.py --config $cfg --steps 20 --warmup 5 --soak 0 --no-cpu-baseline --no-variants --e2e-steps 0 > gpurun_out/c43/b.json 2>gpurun_out/c43/b.err
+  echo "C$cfg $v $(python -c "import json;t=open('gpurun_out/c43/b.json').read();d=json.loads([l for l in t.splitlines() if l.startswith('{')][-1]);print(d['value'], d['rank0']['kernels_ms'], d.get('comparator_aes128_ctr_gbs'))" 2>&1 | tail -1)"
+done; done; done
