@@ -98,52 +98,28 @@ k_recover_block8(const __grid_constant__ FusedParams p) {
 }
 
 // Many independent files in one launch (C5; SURVEY §8.6 "sharded by file").
-// Each CTA finds its job by binary search over cta_begin, assembles that job's
-// parameters in shared memory (the per-job counter base and SHA midstates were
-// derived on the host by fragment_batch_plan) and runs the same CTA body.
-template <int L, bool MASK, bool RECOVER>
-__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS_BATCH)
-k_batch_block8(const __grid_constant__ BatchParams bp) {
-    __shared__ FusedParams sp;
-    __shared__ uint32_t s_job;
+// A unit is one CTA's worth of a file (128 blocks; a file's last unit may be
+// partial).  Job parameters are assembled in shared memory (the per-job
+// counter base and SHA midstates were derived on the host by
+// fragment_batch_plan) and the same CTA body runs on them.
+//
+// One CTA per unit.  Measured and dropped (C5, tools/gpu_r2_call46.sh /
+// call47.sh): persistent CTAs, 5 per SM, that find the job once per range and
+// then only step the job pointer — contiguous per-CTA ranges 98.9 GB/s,
+// grid-strided chunks of 2 / 4 / 8 / 16 units 98.9 / 99.8 / 100.6 / 101.2,
+// against 107.7 for one CTA per unit.
+
+template <int L>
+__device__ __forceinline__ void batch_job_params(FusedParams& sp, const BatchParams& bp, uint32_t jb) {
     using R = Rec<L>;
-    const uint32_t x = blockIdx.x;
-    // job table / report init written by earlier work; with the keystream kernel
-    // right before (protect, base.ks_in_a: a normal launch, so everything
-    // earlier is complete) only its keystream is waited for, at the copy-out
-    // (recover with base.ks_in_out likewise: report init and jobs precede the
-    // keystream kernel; qualifying CTAs wait for their keystream before use)
-    if (!bp.base.ks_in_a && !bp.base.ks_in_out) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (threadIdx.x < 32) {
-        // largest j with cta_begin <= x: 32-ary search by warp 0 (3 dependent
-        // loads for 10,000 jobs instead of 14 for a binary search)
-        const uint32_t lane = threadIdx.x;
-        uint32_t lo = 0, n = bp.n_jobs;               // answer in [lo, lo + n)
-        while (n > 1) {
-            const uint32_t step = (n + 31) / 32;
-            const uint32_t idx = lo + lane * step;
-            const bool le = lane * step < n && bp.jobs[idx].cta_begin <= x;
-            const uint32_t m = __ballot_sync(0xffffffffu, le);   // lanes 0..k set (sorted)
-            const uint32_t k = 31 - __clz(m);                    // lane 0 always set (cta_begin[lo] <= x)
-            lo += k * step;
-            n = min(step, n - k * step);
-        }
-        if (lane == 0) s_job = lo;
-    }
-    {
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(&bp.base);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(&sp);
-        for (uint32_t i = threadIdx.x; i < sizeof(FusedParams) / 4; i += blockDim.x) dst[i] = src[i];
-    }
-    __syncthreads();
-    const se_job& job = bp.jobs[s_job];
+    const se_job& job = bp.jobs[jb];
     const JobDerived& dv = *reinterpret_cast<const JobDerived*>(job.derived);
     const uint32_t t = threadIdx.x;
     if (t == 0) {
         sp.in = job.in;
         sp.out = job.out;
         sp.a = job.a; sp.b = job.b; sp.c = job.c;
-        sp.report = bp.reports ? bp.reports + s_job : nullptr;
+        sp.report = bp.reports ? bp.reports + jb : nullptr;
         sp.n_bytes = job.n_bytes;
         sp.width = job.width;
         sp.bpr = job.width / 8;
@@ -153,8 +129,6 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
         sp.a_bytes = (sp.n_blocks * R::ABITS + 7) / 8;
         sp.b_bytes = (sp.n_blocks * R::BBITS + 7) / 8;
         sp.c_bytes = (sp.n_blocks * R::CBITS + 7) / 8;
-        if (bp.base.ks_in_out)          // this CTA's keystream parked in its output region, or not
-            sp.ks_in_out = batch_ks_out_cta(job.n_bytes, job.width, x - job.cta_begin, R::ABITS) ? 1u : 0u;
     } else if (t >= 32 && t < 36) {
         sp.ctr[t - 32] = dv.ctr[t - 32];
     } else if (t >= 36 && t < 44) {
@@ -169,6 +143,52 @@ k_batch_block8(const __grid_constant__ BatchParams bp) {
         uint32_t* dst = reinterpret_cast<uint32_t*>(&sp.s512);
         for (uint32_t i = t - 64; i < sizeof(SchedConst512) / 4; i += kBlocksPerCta - 64) dst[i] = src[i];
     }
+}
+
+// largest job j with cta_begin <= unit (jobs sorted, jobs[0].cta_begin == 0):
+// 32-ary search by one warp (3 dependent loads for 10,000 jobs)
+__device__ __forceinline__ uint32_t batch_find_job(const BatchParams& bp, uint64_t unit) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t lo = 0, n = bp.n_jobs;                   // answer in [lo, lo + n)
+    while (n > 1) {
+        const uint32_t step = (n + 31) / 32;
+        const uint32_t idx = lo + lane * step;
+        const bool le = lane * step < n && bp.jobs[idx].cta_begin <= unit;
+        const uint32_t m = __ballot_sync(0xffffffffu, le);   // lanes 0..k set (sorted)
+        const uint32_t k = 31 - __clz(m);                    // lane 0 always set
+        lo += k * step;
+        n = min(step, n - k * step);
+    }
+    return lo;
+}
+
+template <int L, bool MASK, bool RECOVER>
+__global__ void __launch_bounds__(kBlocksPerCta, SE_MIN_CTAS_BATCH)
+k_batch_block8(const __grid_constant__ BatchParams bp) {
+    __shared__ FusedParams sp;
+    __shared__ uint32_t s_job;
+    using R = Rec<L>;
+    // job table / report init written by earlier work; with the keystream kernel
+    // right before (protect, base.ks_in_a: a normal launch, so everything
+    // earlier is complete) only its keystream is waited for, at the copy-out
+    // (recover with base.ks_in_out likewise: report init and jobs precede the
+    // keystream kernel; qualifying CTAs wait for their keystream before use)
+    if (!bp.base.ks_in_a && !bp.base.ks_in_out) asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint32_t x = blockIdx.x;
+    if (threadIdx.x < 32) {
+        const uint32_t jb = batch_find_job(bp, x);
+        if (threadIdx.x == 0) s_job = jb;
+    }
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(&bp.base);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&sp);
+        for (uint32_t i = threadIdx.x; i < sizeof(FusedParams) / 4; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const se_job& job = bp.jobs[s_job];
+    batch_job_params<L>(sp, bp, s_job);
+    if (bp.base.ks_in_out && threadIdx.x == 0)         // this CTA's keystream parked in its output region, or not
+        sp.ks_in_out = batch_ks_out_cta(job.n_bytes, job.width, x - job.cta_begin, R::ABITS) ? 1u : 0u;
     __syncthreads();
     const uint64_t cta = x - job.cta_begin;
     if (RECOVER) recover_cta<L, MASK, 0, kBlocksPerCta, SE_BATCH_SPEC != 0>(sp, cta);

@@ -109,7 +109,56 @@ __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ Ciphe
 // one thread per 16-byte counter block over all CTAs of the launch (a CTA's A
 // slice is exactly ABITS counter blocks), written into each file's own A'
 // buffer; the fused batch kernel follows with programmatic serialization and
-// XORs its records in (no scratch).
+// XORs its records in (no scratch).  Each warp owns one contiguous range of
+// counter blocks, 32 per step: it finds the job of its first block once (a
+// 32-ary search, 3 dependent loads at 10,000 jobs) and then only steps the
+// job pointer forward as the range crosses file boundaries (round 2 did a
+// 14-load binary search per warp and step: C5 3.13 ms, long-scoreboard bound).
+#ifndef SE_BATCH_KS_RANGE
+#define SE_BATCH_KS_RANGE 1
+#endif
+template <int ABITS>
+__device__ __forceinline__ void batch_ks_block(const BatchParams& bp, const AesLane& lane, uint32_t jl, uint64_t idx) {
+    const uint64_t cta = idx / ABITS, t = idx - cta * ABITS;
+    const se_job& job = bp.jobs[jl];
+    const uint64_t rows = ((job.n_bytes + job.width - 1) / job.width + 7) / 8 * 8;
+    const uint64_t a_bytes = (rows / 8 * (job.width / 8) * ABITS + 7) / 8;
+    const uint64_t lcta = cta - job.cta_begin;
+    const uint64_t off = (lcta * ABITS + t) * 16;
+    if (off >= a_bytes) return;
+    uint8_t* dst = job.a + off;
+    if (bp.base.ks_in_out) {        // recover: into the CTA's own output region, where it qualifies
+        if (!batch_ks_out_cta(job.n_bytes, job.width, lcta, ABITS)) return;
+        const uint64_t bpr = job.width / 8, b0 = lcta * kBlocksPerCta, br = b0 / bpr, bc = b0 - br * bpr;
+        dst = job.out + 8 * br * (uint64_t)job.width + 8 * bc + 16 * t;
+    }
+    const JobDerived& dv = *reinterpret_cast<const JobDerived*>(job.derived);
+    uint32_t x[4];
+    ctr_add(dv.ctr, lcta * ABITS + t, x);
+    aes128_block(lane, bp.base.rk, x);
+    if (off + 16 <= a_bytes || bp.base.ks_in_out) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3]));
+    } else {
+        for (uint64_t k = 0; k < a_bytes - off; ++k) dst[k] = (uint8_t)(x[k / 4] >> (24 - 8 * (k % 4)));
+    }
+}
+
+// largest job j with cta_begin <= cta (jobs sorted; jobs[0].cta_begin == 0), by the whole warp
+__device__ __forceinline__ uint32_t batch_job_of(const BatchParams& bp, uint64_t cta) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t lo = 0, n = bp.n_jobs;                       // answer in [lo, lo + n)
+    while (n > 1) {
+        const uint32_t step = (n + 31) / 32;
+        const uint32_t idx = lo + lane * step;
+        const bool le = lane * step < n && bp.jobs[idx].cta_begin <= cta;
+        const uint32_t m = __ballot_sync(0xffffffffu, le);
+        const uint32_t k = 31 - __clz(m);
+        lo += k * step;
+        n = min(step, n - k * step);
+    }
+    return lo;
+}
+
 template <int ABITS>
 __global__ void __launch_bounds__(kLaneThreads) k_batch_keystream(const __grid_constant__ BatchParams bp) {
     asm volatile("griddepcontrol.launch_dependents;");
@@ -118,49 +167,42 @@ __global__ void __launch_bounds__(kLaneThreads) k_batch_keystream(const __grid_c
     __syncthreads();
     const AesLane lane = aes_lane(lut);
     const uint64_t total = bp.total_ctas * (uint64_t)ABITS;
+#if SE_BATCH_KS_RANGE
+    const uint32_t ln = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kLaneThreads / 32);
+    const uint64_t gw = (uint64_t)blockIdx.x * (kLaneThreads / 32) + (threadIdx.x >> 5);
+    const uint64_t per = ((total + nwarps - 1) / nwarps + 31) / 32 * 32;
+    const uint64_t i0 = gw * per, i1 = min(total, i0 + per);
+    if (i0 >= i1) return;
+    uint32_t j = batch_job_of(bp, i0 / ABITS);
+    uint64_t nb = j + 1 < bp.n_jobs ? bp.jobs[j + 1].cta_begin : ~0ull;   // first CTA of the next job
+    for (uint64_t base = i0; base < i1; base += 32) {
+        const uint64_t idx = base + ln;
+        const uint64_t cta = idx / ABITS;
+        uint32_t jl = j;
+        uint64_t nbl = nb;
+        while (cta >= nbl) {                                // crossed into a later file (rare)
+            ++jl;
+            nbl = jl + 1 < bp.n_jobs ? bp.jobs[jl + 1].cta_begin : ~0ull;
+        }
+        if (idx < i1) batch_ks_block<ABITS>(bp, lane, jl, idx);
+        j = __shfl_sync(0xffffffffu, jl, 31);
+        nb = ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(nbl >> 32), 31) << 32) |
+             __shfl_sync(0xffffffffu, (uint32_t)nbl, 31);
+    }
+#else
     const uint64_t stride = (uint64_t)gridDim.x * kLaneThreads;
     for (uint64_t idx = (uint64_t)blockIdx.x * kLaneThreads + threadIdx.x; idx < total; idx += stride) {
-        const uint64_t cta = idx / ABITS, t = idx - cta * ABITS;
-        // the job of this counter block: the warp searches once for its first
-        // lane's fused-kernel CTA; lanes whose CTA lies in a later job search alone
-        const uint64_t cta0 = __shfl_sync(0xffffffffu, cta, 0);
-        uint32_t lo = 0, hi = bp.n_jobs - 1;                   // largest job with cta_begin <= cta0
+        const uint64_t cta = idx / ABITS;
+        uint32_t lo = 0, hi = bp.n_jobs - 1;                   // largest job with cta_begin <= cta
         while (lo < hi) {
             const uint32_t mid = (lo + hi + 1) / 2;
-            if (bp.jobs[mid].cta_begin <= cta0) lo = mid;
+            if (bp.jobs[mid].cta_begin <= cta) lo = mid;
             else hi = mid - 1;
         }
-        if (lo + 1 < bp.n_jobs && bp.jobs[lo + 1].cta_begin <= cta) {
-            uint32_t l2 = lo + 1, h2 = bp.n_jobs - 1;
-            while (l2 < h2) {
-                const uint32_t mid = (l2 + h2 + 1) / 2;
-                if (bp.jobs[mid].cta_begin <= cta) l2 = mid;
-                else h2 = mid - 1;
-            }
-            lo = l2;
-        }
-        const se_job& job = bp.jobs[lo];
-        const uint64_t rows = ((job.n_bytes + job.width - 1) / job.width + 7) / 8 * 8;
-        const uint64_t a_bytes = (rows / 8 * (job.width / 8) * ABITS + 7) / 8;
-        const uint64_t lcta = cta - job.cta_begin;
-        const uint64_t off = (lcta * ABITS + t) * 16;
-        if (off >= a_bytes) continue;
-        uint8_t* dst = job.a + off;
-        if (bp.base.ks_in_out) {        // recover: into the CTA's own output region, where it qualifies
-            if (!batch_ks_out_cta(job.n_bytes, job.width, lcta, ABITS)) continue;
-            const uint64_t bpr = job.width / 8, b0 = lcta * kBlocksPerCta, br = b0 / bpr, bc = b0 - br * bpr;
-            dst = job.out + 8 * br * (uint64_t)job.width + 8 * bc + 16 * t;
-        }
-        const JobDerived& dv = *reinterpret_cast<const JobDerived*>(job.derived);
-        uint32_t x[4];
-        ctr_add(dv.ctr, lcta * ABITS + t, x);
-        aes128_block(lane, bp.base.rk, x);
-        if (off + 16 <= a_bytes || bp.base.ks_in_out) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3]));
-        } else {
-            for (uint64_t k = 0; k < a_bytes - off; ++k) dst[k] = (uint8_t)(x[k / 4] >> (24 - 8 * (k % 4)));
-        }
+        batch_ks_block<ABITS>(bp, lane, lo, idx);
     }
+#endif
 }
 
 // 64 KB of dynamic shared memory needs an opt-in, once per kernel and device
