@@ -145,17 +145,27 @@ __device__ __forceinline__ void batch_job_params(FusedParams& sp, const BatchPar
     }
 }
 
-// largest job j with cta_begin <= unit (jobs sorted, jobs[0].cta_begin == 0):
-// 32-ary search by one warp (3 dependent loads for 10,000 jobs)
+// largest job j with cta_begin <= unit (jobs sorted, jobs[0].cta_begin == 0),
+// by one warp: 32 ways, one candidate per lane (3 dependent passes at 10,000
+// jobs).  SE_BATCH_SEARCH_WAYS 128 (4 candidates per lane, 2 passes) measured
+// slower on C5: 106.7 vs 107.8 GB/s (tools/gpu_r2_call49.sh).
+#ifndef SE_BATCH_SEARCH_WAYS
+#define SE_BATCH_SEARCH_WAYS 32
+#endif
 __device__ __forceinline__ uint32_t batch_find_job(const BatchParams& bp, uint64_t unit) {
+    constexpr uint32_t Q = SE_BATCH_SEARCH_WAYS / 32;
     const uint32_t lane = threadIdx.x & 31;
     uint32_t lo = 0, n = bp.n_jobs;                   // answer in [lo, lo + n)
     while (n > 1) {
-        const uint32_t step = (n + 31) / 32;
-        const uint32_t idx = lo + lane * step;
-        const bool le = lane * step < n && bp.jobs[idx].cta_begin <= unit;
-        const uint32_t m = __ballot_sync(0xffffffffu, le);   // lanes 0..k set (sorted)
-        const uint32_t k = 31 - __clz(m);                    // lane 0 always set
+        const uint32_t step = (n + 32 * Q - 1) / (32 * Q);
+        uint32_t trues = 0;                           // candidates c = lane * Q + q, sorted: a prefix is true
+#pragma unroll
+        for (uint32_t q = 0; q < Q; ++q) {
+            const uint32_t c = lane * Q + q;
+            const bool le = c * step < n && bp.jobs[lo + c * step].cta_begin <= unit;
+            trues += __popc(__ballot_sync(0xffffffffu, le));
+        }
+        const uint32_t k = trues - 1;                 // candidate 0 always true
         lo += k * step;
         n = min(step, n - k * step);
     }
