@@ -8,8 +8,13 @@
 
 using namespace se;
 
+// Level-2 protect's keystream kernel on the 64 KB lane-replicated table (1)
+// or the 5 KB tables (0).  Round 2 (tools/gpu_r2_call50.sh, two passes):
+// 4800x4800 protect 95.5 -> 93.3 us, the smaller Table 4.1 images unchanged.
+// (Level 1 with a separate lane-table keystream instead of the in-kernel AES:
+// 4800x4800 28.8 -> 27.5 us but 1024x768 10.6 -> 14.0 us, so level 1 keeps it.)
 #ifndef SE_DCT_LANE_KS
-#define SE_DCT_LANE_KS 0
+#define SE_DCT_LANE_KS 1
 #endif
 
 static int check_dct(const se_dct_geom* g, bool need_level) {
