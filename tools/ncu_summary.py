@@ -28,6 +28,12 @@ def main(path):
             if k in hdr:
                 i = hdr.index(k)
                 print(f"  {k:70s} {r[i]} {units[i]}")
+        try:                                                   # SM active share of the kernel's elapsed cycles
+            act = float(r[hdr.index("sm__cycles_active.avg")].replace(",", ""))
+            ela = float(r[hdr.index("sm__cycles_elapsed.avg")].replace(",", ""))
+            print(f"  {'sm active / elapsed cycles (avg over SMs)':70s} {act / ela:.4f}")
+        except (ValueError, IndexError, ZeroDivisionError):
+            pass
         stalls = []
         for i, h in enumerate(hdr):
             if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
