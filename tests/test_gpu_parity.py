@@ -295,6 +295,33 @@ def test_batch_1100_files_multi_pass_search(dev, orc):
     assert (reps.cpu().numpy() == np.array([-1, 0])).all()
 
 
+@pytest.mark.parametrize("flags", [0, 1])
+def test_batch_with_empty_and_tiny_files(dev, orc, flags):
+    """Empty files (zero CTAs: several jobs share one cta_begin, including the
+    first and the last job), one-byte files and whole-row files (W = 1024,
+    where recover parks each CTA's keystream in its output region) mixed in one
+    batch: every stream equals the oracle, every file round-trips, every report
+    is clean - the job search and the keystream kernel's job stepping must skip
+    the empty jobs."""
+    sizes = [0, 1, 0, 0, 5000, 3 * 1024 * 1024, 0, 1, 70000, 2 * 1024 * 1024 + 512, 0, 64, 0]
+    files = [synth.random_bytes(s, 400 + i) if s else np.zeros(0, np.uint8) for i, s in enumerate(sizes)]
+    widths = [synth.width_rule(max(s, 1)) for s in sizes]
+    ivs = [synth.iv_for(5, 900 + i) for i in range(len(sizes))]
+    batch = se.Batch([to_dev(f, dev) for f in files], widths, ivs, 2, KEY, flags=flags)
+    begins = [int(batch.jobs[i].cta_begin) for i in range(len(sizes))]
+    assert begins[0] == begins[1] and begins[2] == begins[3] == begins[4]
+    streams = batch.protect()
+    for f, w, iv, (a, b, c) in zip(files, widths, ivs, streams):
+        oa, ob, oc = orc.protect(f, w, 2, KEY, iv, flags=flags)
+        assert np.array_equal(a.cpu().numpy(), oa)
+        assert np.array_equal(b.cpu().numpy(), ob)
+        assert np.array_equal(c.cpu().numpy(), oc)
+    outs, reps = batch.recover()
+    for f, o in zip(files, outs):
+        assert np.array_equal(o.cpu().numpy(), f)
+    assert (reps.cpu().numpy() == np.array([-1, 0])).all()
+
+
 @pytest.mark.parametrize("W,rows,L", [(1024, 8 * 37, 2), (2048, 8 * 11, 3), (6144, 8 * 5, 2)])
 def test_recover_keystream_in_output_region(dev, orc, W, rows, L):
     """Masked per-CTA recovery on whole rows of a multiple of 1024 bytes: the
