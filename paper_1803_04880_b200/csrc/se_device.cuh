@@ -235,8 +235,8 @@ __device__ __forceinline__ void lift_inv_lean(int (&y)[N], uint32_t one) {
 // Mixed-pipe lean lifting (SE_LEAN_MIX bit 0: forward, bit 1: inverse): the
 // sums move to the FMA pipe as IMADs by an opaque +-1 and each lift keeps one
 // ALU op, the shift-and-add (LEA.HI).  Forward:
-//   n_e = 3 - x_e                      (IMAD; each even sample serves two predicts)
-//   u   = 3 - x_l - x_r = IMAD(x_l, -1, n_r)
+//   u   = 3 - x_l - x_r                (one IADD3; or, SE_MIX_FWD_PRED_LEAN 0, IMAD(x_l, -1, n_r)
+//                                       with n_e = 3 - x_e by one IMAD per even sample)
 //   d'  = x_o + (u >> 1) = d + 1       (LEA.HI; floor((3 - m) / 2) = 1 + floor((1 - m) / 2) = 1 - floor(m / 2))
 //   s   = x_e + ((d'_l + d'_r) >> 2)   (IMAD + LEA.HI; d'_l + d'_r = d_l + d_r + 2)
 // so every high-pass output carries +1 (d' = d + 1).  Lifting passes a
@@ -259,15 +259,28 @@ __device__ __forceinline__ int imad(int a, int b, int c) {      // a * b + c on 
     return r;
 }
 
+// SE_MIX_FWD_PRED_LEAN 1: the forward predict as IADD3 + LEA.HI (two ALU ops,
+// no n_e), the update mixed - fewer instructions, more ALU-pipe work.
+// Measured (tools/gpu_r2_call51.sh, two passes): C4 PUBLIC_PLAIN protect
+// 0.6259 -> 0.6237 ms, masked protect 4.659 -> 4.651 ms: 1.
+#ifndef SE_MIX_FWD_PRED_LEAN
+#define SE_MIX_FWD_PRED_LEAN 1
+#endif
 template <int N>
 __device__ __forceinline__ void lift_fwd_mix(int (&x)[N], int m1) {
     constexpr int H = N / 2;
     int n[H] = {}, s[H], d[H];
+#if !SE_MIX_FWD_PRED_LEAN
 #pragma unroll
     for (int k = 1; k < H; ++k) n[k] = imad(x[2 * k], m1, 3);                    // 3 - x_e (n[0] unused)
+#endif
 #pragma unroll
     for (int k = 0; k < H; ++k) {
+#if SE_MIX_FWD_PRED_LEAN
+        if (2 * k + 2 < N) d[k] = x[2 * k + 1] + ((3 - x[2 * k] - x[2 * k + 2]) >> 1);   // Eq. 5.1, +1
+#else
         if (2 * k + 2 < N) d[k] = x[2 * k + 1] + (imad(x[2 * k], m1, n[k + 1]) >> 1);   // Eq. 5.1, +1
+#endif
         else d[k] = x[2 * k + 1] - x[2 * k] + 1;                                 // x(N) = x(N-2), +1
     }
 #pragma unroll
