@@ -41,6 +41,16 @@ extern "C" int se_trace_ks_read(unsigned long long* host, int n_ctas) {
 }
 #endif
 
+// SE_LUT4 1: the lane-table kernels use the 128 KB table with stored
+// rotations (se_device.cuh aes_load_lut4), one CTA per SM.  Measured
+// (tools/gpu_r2_call52.sh, two passes): AES-CTR comparator 788 -> 801 GB/s
+// (the kernel is shared-memory-wavefront bound as much as ALU bound), C4
+// masked 115.24 -> 115.36 GB/s, C5 107.53 -> 107.67 GB/s: 1.
+#ifndef SE_LUT4
+#define SE_LUT4 1
+#endif
+constexpr int kLaneLutBytes = SE_LUT4 ? kAesLut4Bytes : kAesLutBytes;
+
 template <bool LANE, int NT>
 __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ CipherParams p) {
 #ifdef SE_TRACE
@@ -56,8 +66,12 @@ __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ Ciphe
     }
     extern __shared__ __align__(16) uint32_t lut[];
     __shared__ AesSmem small;
-    if constexpr (LANE) aes_load_lut(lut, threadIdx.x, NT);
-    else aes_load_tables(small, threadIdx.x, NT);
+    if constexpr (LANE) {
+        if constexpr (SE_LUT4) aes_load_lut4(lut, threadIdx.x, NT);
+        else aes_load_lut(lut, threadIdx.x, NT);
+    } else {
+        aes_load_tables(small, threadIdx.x, NT);
+    }
     __syncthreads();
     const AesLane lane = aes_lane(lut);
     const uint64_t nblk = (p.n + 15) / 16;
@@ -65,7 +79,8 @@ __global__ void __launch_bounds__(NT) k_cipher_ctr(const __grid_constant__ Ciphe
     for (uint64_t j = (uint64_t)blockIdx.x * NT + threadIdx.x; j < nblk; j += stride) {
         uint32_t x[4];
         ctr_add(p.ctr, j, x);
-        if constexpr (LANE) aes128_block(lane, p.rk, x);
+        if constexpr (LANE && SE_LUT4) aes128_block4(lane, p.rk, x);
+        else if constexpr (LANE) aes128_block(lane, p.rk, x);
         else aes128_block(small, p.rk, x);
         const uint64_t off = j * 16;
         if (p.cta_ablocks) {                  // scatter: keystream only, whole AES blocks (se_api.cu checks)
@@ -135,7 +150,8 @@ __device__ __forceinline__ void batch_ks_block(const BatchParams& bp, const AesL
     const JobDerived& dv = *reinterpret_cast<const JobDerived*>(job.derived);
     uint32_t x[4];
     ctr_add(dv.ctr, lcta * ABITS + t, x);
-    aes128_block(lane, bp.base.rk, x);
+    if constexpr (SE_LUT4) aes128_block4(lane, bp.base.rk, x);
+    else aes128_block(lane, bp.base.rk, x);
     if (off + 16 <= a_bytes || bp.base.ks_in_out) {
         *reinterpret_cast<uint4*>(dst) = make_uint4(bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3]));
     } else {
@@ -163,7 +179,8 @@ template <int ABITS>
 __global__ void __launch_bounds__(kLaneThreads) k_batch_keystream(const __grid_constant__ BatchParams bp) {
     asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ __align__(16) uint32_t lut[];
-    aes_load_lut(lut, threadIdx.x, kLaneThreads);          // lane-replicated table (as k_cipher_ctr)
+    if constexpr (SE_LUT4) aes_load_lut4(lut, threadIdx.x, kLaneThreads);   // lane-replicated table (as k_cipher_ctr)
+    else aes_load_lut(lut, threadIdx.x, kLaneThreads);
     __syncthreads();
     const AesLane lane = aes_lane(lut);
     const uint64_t total = bp.total_ctas * (uint64_t)ABITS;
@@ -212,7 +229,7 @@ static void allow_lut() {
     int dev = 0;
     cudaGetDevice(&dev);
     if (done == dev) return;
-    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAesLutBytes);
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLaneLutBytes);
     done = dev;
 }
 
@@ -228,20 +245,20 @@ int launch_batch_keystream(const BatchParams& bp, uint32_t a_bits, void* stream)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t total = bp.total_ctas * (uint64_t)a_bits;
     const uint64_t want = (total + kLaneThreads - 1) / kLaneThreads;
-    const int lane_ctas = kCipherCtasPerSm < 2048 / kLaneThreads ? kCipherCtasPerSm : 2048 / kLaneThreads;
+    const int lane_ctas = SE_LUT4 ? 1 : kCipherCtasPerSm < 2048 / kLaneThreads ? kCipherCtasPerSm : 2048 / kLaneThreads;
     const uint64_t cap = (uint64_t)sms * lane_ctas;
     const unsigned grid = (unsigned)(want < cap ? want : cap);
     cudaStream_t s = (cudaStream_t)stream;
     if (grid == 0) return 0;
     if (a_bits == 40) {
         allow_lut<k_batch_keystream<40>>();
-        k_batch_keystream<40><<<grid, kLaneThreads, kAesLutBytes, s>>>(bp);
+        k_batch_keystream<40><<<grid, kLaneThreads, kLaneLutBytes, s>>>(bp);
     } else if (a_bits == 160) {
         allow_lut<k_batch_keystream<160>>();
-        k_batch_keystream<160><<<grid, kLaneThreads, kAesLutBytes, s>>>(bp);
+        k_batch_keystream<160><<<grid, kLaneThreads, kLaneLutBytes, s>>>(bp);
     } else {
         allow_lut<k_batch_keystream<10>>();
-        k_batch_keystream<10><<<grid, kLaneThreads, kAesLutBytes, s>>>(bp);
+        k_batch_keystream<10><<<grid, kLaneThreads, kLaneLutBytes, s>>>(bp);
     }
     note_launch();
     return (int)cudaGetLastError();
@@ -261,7 +278,7 @@ int launch_cipher_ctr(const CipherParams& p, void* stream) {
     const int nt = lane_narrow ? kKsNarrowThreads : lane ? kLaneThreads : narrow ? kKsNarrowThreads : kKsThreads;
     const uint64_t want = (nblk + nt - 1) / nt;
     // lane table: 64 KB per CTA -> at most 3 CTAs per SM, and 2048 threads per SM
-    const int lane_ctas = kCipherCtasPerSm < 2048 / kLaneThreads ? kCipherCtasPerSm : 2048 / kLaneThreads;
+    const int lane_ctas = SE_LUT4 ? 1 : kCipherCtasPerSm < 2048 / kLaneThreads ? kCipherCtasPerSm : 2048 / kLaneThreads;
     const uint64_t cap = (uint64_t)sms * (lane_narrow ? 1 : lane ? lane_ctas : narrow ? kKsNarrowCtasPerSm
                                                                                        : kKeystreamCtasPerSm);
     const unsigned grid = (unsigned)(want < cap ? want : cap);
@@ -269,10 +286,10 @@ int launch_cipher_ctr(const CipherParams& p, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (lane_narrow) {
         allow_lut<k_cipher_ctr<true, kKsNarrowThreads>>();
-        k_cipher_ctr<true, kKsNarrowThreads><<<grid, kKsNarrowThreads, kAesLutBytes, s>>>(p);
+        k_cipher_ctr<true, kKsNarrowThreads><<<grid, kKsNarrowThreads, kLaneLutBytes, s>>>(p);
     } else if (lane) {
         allow_lut<k_cipher_ctr<true, kLaneThreads>>();
-        k_cipher_ctr<true, kLaneThreads><<<grid, kLaneThreads, kAesLutBytes, s>>>(p);
+        k_cipher_ctr<true, kLaneThreads><<<grid, kLaneThreads, kLaneLutBytes, s>>>(p);
     } else if (narrow) {
         k_cipher_ctr<false, kKsNarrowThreads><<<grid, kKsNarrowThreads, 0, s>>>(p);
     } else {

@@ -603,6 +603,52 @@ __device__ __forceinline__ void aes128_block(const AesLane& a, const uint32_t* _
     }
 }
 
+// The same table with its rotations stored too (128 KB: the first 64 KB as
+// above, the second holding Te1[x] = ror8(Te0[x]) and Te3[x] = ror8(Te2[x])
+// in the same row / lane positions, read at +64 KB by the same PRMT-built
+// address): a middle-round column is 4 PRMT + 4 LDS + 2 LOP3 instead of
+// 4 PRMT + 4 LDS + 3 LOP3 + 1 SHF.  Only the standalone cipher / keystream
+// kernels use it (one CTA per SM).
+constexpr int kAesLut4Bytes = 2 * kAesLutBytes;
+
+__device__ __forceinline__ void aes_load_lut4(uint32_t* lut, int tid, int nthreads) {
+    uint4* l4 = reinterpret_cast<uint4*>(lut);
+    for (int i = tid; i < 2 * 256 * 16; i += nthreads) {          // two halves of 16 x 16 B per row
+        const int h = i >> 12, j = i & 4095;
+        const uint32_t t = g_aes_te0[j >> 4];
+        uint32_t v = (j & 15) < 8 ? t : __funnelshift_r(t, t, 16);
+        if (h) v = __funnelshift_r(v, v, 8);
+        l4[i] = make_uint4(v, v, v, v);
+    }
+}
+
+__device__ __forceinline__ uint32_t aes_col4(const AesLane& a, uint32_t sa, uint32_t sb, uint32_t sc, uint32_t sd,
+                                             uint32_t k) {
+    const uint32_t hi = aes_lu<3>(a, sa, a.c0) ^ aes_lu<1>(a, sc, a.c2) ^ k;
+    const uint32_t t1 = *reinterpret_cast<const uint32_t*>(a.lut + kAesLutBytes + __byte_perm(sb, a.c0, 0x5524));
+    const uint32_t t3 = *reinterpret_cast<const uint32_t*>(a.lut + kAesLutBytes + __byte_perm(sd, a.c2, 0x5504));
+    return hi ^ t1 ^ t3;
+}
+
+__device__ __forceinline__ void aes128_block4(const AesLane& a, const uint32_t* __restrict__ rk, uint32_t (&x)[4]) {
+    uint32_t s0 = x[0] ^ rk[0], s1 = x[1] ^ rk[1], s2 = x[2] ^ rk[2], s3 = x[3] ^ rk[3];
+#pragma unroll
+    for (int r = 1; r < 10; ++r) {
+        const uint32_t t0 = aes_col4(a, s0, s1, s2, s3, rk[4 * r + 0]);
+        const uint32_t t1 = aes_col4(a, s1, s2, s3, s0, rk[4 * r + 1]);
+        const uint32_t t2 = aes_col4(a, s2, s3, s0, s1, rk[4 * r + 2]);
+        const uint32_t t3 = aes_col4(a, s3, s0, s1, s2, rk[4 * r + 3]);
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    const uint32_t s[4] = {s0, s1, s2, s3};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t hi = __byte_perm(aes_lu<3>(a, s[j], a.c0), aes_lu<2>(a, s[(j + 1) & 3], a.c0), 0x2600);
+        const uint32_t lo = __byte_perm(aes_lu<1>(a, s[(j + 2) & 3], a.c0), aes_lu<0>(a, s[(j + 3) & 3], a.c0), 0x0026);
+        x[j] = __byte_perm(lo, hi, 0x7610) ^ rk[40 + j];
+    }
+}
+
 // Small T-tables (5 KB): te[0..3][256] (Te1..3 = byte rotations of Te0) + the
 // S-box.  Random indices conflict in the shared-memory banks (~3.5 wavefronts
 // per lookup), but the footprint is small: used for the keystream kernels
