@@ -462,6 +462,11 @@ __device__ __forceinline__ void put_field_lean(uint32_t (&r)[NW], int pos, int v
 #ifndef SE_EXTRACT_FMA
 #define SE_EXTRACT_FMA 1
 #endif
+// SE_EXTRACT_HI 1: the sign-extending right shift as IMAD.HI.  Measured
+// (tools/gpu_r2_call53.sh): C4 PUBLIC_PLAIN recover 0.637 -> 0.730 ms, so 0.
+#ifndef SE_EXTRACT_HI
+#define SE_EXTRACT_HI 0
+#endif
 template <int NW>
 __device__ __forceinline__ int get_field_lean(const uint32_t (&r)[NW], int pos, int w, uint32_t one) {
     const int word = pos >> 5, start = pos & 31, end = start + w;
@@ -479,7 +484,14 @@ __device__ __forceinline__ int get_field_lean(const uint32_t (&r)[NW], int pos, 
     } else {
         top = __funnelshift_l(r[word + 1], r[word], start);
     }
+#if SE_EXTRACT_HI
+    // the sign-extending right shift as IMAD.HI: (top * 2^w) >> 32 (FMA pipe)
+    int v;
+    asm("mul.hi.s32 %0, %1, %2;" : "=r"(v) : "r"(top), "r"(one << w));
+    return v;
+#else
     return (int)top >> (32 - w);
+#endif
 }
 
 template <int NW>
