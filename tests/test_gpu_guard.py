@@ -188,3 +188,38 @@ def test_dct_guards(dev, level):
     check_all(img, a, p, o, f, i8)
     assert int((o.view.int() - img.view.int()).abs().max()) <= 8       # lossy by design (~60 dB)
     assert int((i8.view.int() - img.view.int()).abs().max()) <= 1
+
+
+@pytest.mark.parametrize("n,W,L,world", [(256 * 256 + 77, 256, 2, 3), (1024 * 200, 1024, 3, 2)])
+def test_full_stripe_guards(dev, n, W, L, world):
+    """FULL-mode stripes with halo rows: each stripe's source window, slices,
+    workspace and recovered bytes are guarded; the stripes reassemble the file."""
+    from paper_1803_04880_b200 import shard
+    x_np = synth.random_bytes(n, 11 * n)
+    plan = [s for s in shard.plan_full_stripes(n, W, L, world) if s is not None]
+    frags = {k: [] for k in "abc"}
+    for st in plan:
+        src = gin(x_np[st["src_byte_begin"]: st["src_byte_end"]], dev)
+        sizes = [st["out"][k][1] - st["out"][k][0] for k in "abc"]
+        outs = [gout(s, dev) for s in sizes]
+        stripe = (st["row_begin"], st["row_end"], st["src_row0"], min(-(-src.n // W), st["src_rows"]))
+        ws = gout(se.fragment_workspace_size(n, W, L, se.MODE_FULL, stripe), dev)
+        se.fragment_protect_stripe(src.view, n, W, L, KEY, IV, st["row_begin"], st["row_end"], st["src_row0"],
+                                   out=tuple(o.view for o in outs), workspace=ws.view)
+        check_all(src, ws, *outs)
+        for k, o in zip("abc", outs):
+            frags[k].append(o.view.cpu().numpy())
+    whole = {k: np.concatenate(v) for k, v in frags.items()}
+    back = []
+    for st in plan:
+        ins = [gin(whole[k][slice(*st["rec_in"][k])], dev) for k in "abc"]
+        nb = st["byte_end"] - st["byte_begin"]
+        out, rep = gout(nb, dev), gout(2, dev, torch.int64)
+        stripe = (st["row_begin"], st["row_end"], st["rec_row0"], st["rec_rows"])
+        ws = gout(se.fragment_workspace_size(n, W, L, se.MODE_FULL, stripe), dev)
+        se.fragment_recover_stripe(*(i.view for i in ins), n, W, L, KEY, IV, st["row_begin"], st["row_end"],
+                                   st["rec_row0"], st["rec_rows"], out=out.view, report=rep.view, workspace=ws.view)
+        check_all(*ins, out, rep, ws)
+        assert rep.view.cpu().tolist() == [-1, 0]
+        back.append(out.view.cpu().numpy())
+    assert np.array_equal(np.concatenate(back), x_np)
