@@ -223,3 +223,44 @@ def test_full_stripe_guards(dev, n, W, L, world):
         assert rep.view.cpu().tolist() == [-1, 0]
         back.append(out.view.cpu().numpy())
     assert np.array_equal(np.concatenate(back), x_np)
+
+
+class HostGuarded:
+    """A pinned host uint8 view of n bytes with guard bands (16-byte aligned)."""
+
+    def __init__(self, n, fill=None):
+        self.raw = torch.full((2 * G + n,), PAT, dtype=torch.uint8).pin_memory()
+        self.n = n
+        self.view = self.raw[G:G + n]
+        if fill is not None:
+            self.view.copy_(torch.from_numpy(fill))
+
+    def guards_ok(self):
+        torch.cuda.synchronize()
+        return bool((self.raw[:G] == PAT).all()) and bool((self.raw[G + self.n:] == PAT).all())
+
+
+@pytest.mark.parametrize("n,W,chunk", [(300000, 512, 64 * 1024), (6144 * 8 * 9 + 5, 6144, 0), (999, 8, 0)])
+@pytest.mark.parametrize("asyn", [False, True])
+def test_host_api_guards(dev, n, W, chunk, asyn):
+    """Host streaming (staged chunks; protect's kernels write the fragments
+    straight into the pinned buffers): nothing outside the host views changes."""
+    L = 2
+    x_np = synth.random_bytes(n, 5 * n + 1)
+    x = HostGuarded(n, x_np)
+    lay = se.fragment_layout(n, W, L)
+    a, b, c = (HostGuarded(lay[k]) for k in ("a_bytes", "b_bytes", "c_bytes"))
+    y = HostGuarded(n)
+    kw = dict(chunk_bytes=chunk, n_streams=3)
+    if asyn:
+        _, t1 = se.fragment_protect_host_async(x.view, W, L, KEY, IV, out=(a.view, b.view, c.view), **kw)
+        _, t2 = se.fragment_recover_host_async(a.view, b.view, c.view, n, W, L, KEY, IV, out=y.view, after=t1, **kw)
+        rep = t2.wait()
+        t1.wait()
+    else:
+        se.fragment_protect_host(x.view, W, L, KEY, IV, out=(a.view, b.view, c.view), **kw)
+        _, rep = se.fragment_recover_host(a.view, b.view, c.view, n, W, L, KEY, IV, out=y.view, **kw)
+    for i, h in enumerate((x, a, b, c, y)):
+        assert h.guards_ok(), f"host guard band of buffer {i} overwritten"
+    assert np.array_equal(x.view.numpy(), x_np) and np.array_equal(y.view.numpy(), x_np)
+    assert tuple(rep) == (-1, 0)
