@@ -480,6 +480,7 @@ int fragment_workspace_size(const se_geom* g, const se_stripe* st, uint64_t* byt
 
 int fragment_protect_ws(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in, void* d_a,
                         void* d_b, void* d_c, void* d_ws, uint64_t ws_bytes, void* stream) {
+    SE_RANGE("fragment_protect_ws");
     ImplOpts o;
     o.ws = d_ws;
     o.ws_bytes = ws_bytes;
@@ -489,6 +490,7 @@ int fragment_protect_ws(const se_geom* g, const uint8_t key[16], const uint8_t i
 int fragment_recover_ws(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
                         const void* d_b, const void* d_c, void* d_out, se_report* d_report, void* d_ws,
                         uint64_t ws_bytes, void* stream) {
+    SE_RANGE("fragment_recover_ws");
     ImplOpts o;
     o.ws = d_ws;
     o.ws_bytes = ws_bytes;
@@ -497,11 +499,13 @@ int fragment_recover_ws(const se_geom* g, const uint8_t key[16], const uint8_t i
 
 int fragment_protect(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in,
                      void* d_a, void* d_b, void* d_c, void* stream) {
+    SE_RANGE("fragment_protect");
     return protect_impl(g, key, iv, d_in, d_a, d_b, d_c, ImplOpts(), stream);
 }
 
 int fragment_recover(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
                      const void* d_b, const void* d_c, void* d_out, se_report* d_report, void* stream) {
+    SE_RANGE("fragment_recover");
     return recover_impl(g, key, iv, d_a, d_b, d_c, d_out, d_report, ImplOpts(), stream);
 }
 
@@ -558,6 +562,7 @@ extern "C" {
 int fragment_protect_stripe(const se_geom* g, const se_stripe* st, const uint8_t key[16], const uint8_t iv[16],
                             const void* d_in, void* d_a, void* d_b, void* d_c, void* d_ws, uint64_t ws_bytes,
                             void* stream) {
+    SE_RANGE("fragment_protect_stripe");
     se_layout lay;
     int rc = stripe_checks(g, st, key, iv, lay, false);
     if (rc) return rc;
@@ -582,6 +587,7 @@ int fragment_protect_stripe(const se_geom* g, const se_stripe* st, const uint8_t
 int fragment_recover_stripe(const se_geom* g, const se_stripe* st, const uint8_t key[16], const uint8_t iv[16],
                             const void* d_a, const void* d_b, const void* d_c, void* d_out, se_report* d_report,
                             void* d_ws, uint64_t ws_bytes, void* stream) {
+    SE_RANGE("fragment_recover_stripe");
     se_layout lay;
     int rc = stripe_checks(g, st, key, iv, lay, true);
     if (rc) return rc;
@@ -615,6 +621,7 @@ int fragment_recover_stripe(const se_geom* g, const se_stripe* st, const uint8_t
 }
 
 int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream) {
+    SE_RANGE("dwt_fwd");
     se_layout lay;
     int rc = fragment_layout(g, &lay);
     if (rc) return rc;
@@ -629,6 +636,7 @@ int dwt_fwd(const se_geom* g, const void* d_in, int16_t* d_coef, void* stream) {
 }
 
 int dwt_inv(const se_geom* g, const int16_t* d_coef, void* d_out, void* stream) {
+    SE_RANGE("dwt_inv");
     se_layout lay;
     int rc = fragment_layout(g, &lay);
     if (rc) return rc;
@@ -644,6 +652,7 @@ int dwt_inv(const se_geom* g, const int16_t* d_coef, void* d_out, void* stream) 
 
 int cipher_encrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block_offset, const void* d_in,
                    void* d_out, uint64_t n, void* stream) {
+    SE_RANGE("cipher_encrypt");
     if (!key || !iv) return SE_EINVAL;
     if (n == 0) return SE_OK;
     if (!d_in || !d_out) return SE_EINVAL;
@@ -658,11 +667,13 @@ int cipher_encrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_blo
 
 int cipher_decrypt(const uint8_t key[16], const uint8_t iv[16], uint64_t ctr_block_offset, const void* d_in,
                    void* d_out, uint64_t n, void* stream) {
+    SE_RANGE("cipher_decrypt");
     return cipher_encrypt(key, iv, ctr_block_offset, d_in, d_out, n, stream);
 }
 
 int se_stats_accumulate(const void* d_x, const void* d_y, uint64_t n, uint32_t width, se_stats* d_stats,
                         uint32_t* d_joint, void* stream) {
+    SE_RANGE("se_stats_accumulate");
     if (width == 0 || !d_stats) return SE_EINVAL;
     if (n == 0) return SE_OK;
     if (!d_y) return SE_EINVAL;
@@ -670,6 +681,7 @@ int se_stats_accumulate(const void* d_x, const void* d_y, uint64_t n, uint32_t w
 }
 
 int64_t fragment_batch_plan(se_job* jobs, uint32_t n_jobs, uint32_t levels, const uint8_t key[16]) {
+    SE_RANGE("fragment_batch_plan");
     if (!jobs || !key || levels < 1 || levels > 3) return SE_EINVAL;
     uint64_t cta = 0;
     for (uint32_t j = 0; j < n_jobs; ++j) {
@@ -738,11 +750,13 @@ static int batch_common(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ct
 
 int fragment_protect_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas, uint32_t levels,
                            uint32_t flags, const uint8_t key[16], void* stream) {
+    SE_RANGE("fragment_protect_batch");
     return batch_common(n_jobs, d_jobs, total_ctas, levels, flags, key, nullptr, false, stream);
 }
 
 int fragment_recover_batch(uint32_t n_jobs, const se_job* d_jobs, uint64_t total_ctas, uint32_t levels,
                            uint32_t flags, const uint8_t key[16], se_report* d_reports, void* stream) {
+    SE_RANGE("fragment_recover_batch");
     return batch_common(n_jobs, d_jobs, total_ctas, levels, flags, key, d_reports, true, stream);
 }
 

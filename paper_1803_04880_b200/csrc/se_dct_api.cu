@@ -78,6 +78,7 @@ int dct_layout(const se_dct_geom* g, se_dct_layout* out) {
 
 int dct_protect(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_in, void* d_a,
                 void* d_p, void* stream) {
+    SE_RANGE("dct_protect");
     se_dct_layout lay;
     int rc = dct_layout(g, &lay);
     if (rc) return rc;
@@ -98,6 +99,7 @@ int dct_protect(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
 
 int dct_recover(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* d_a,
                 const void* d_p, void* d_out, void* stream) {
+    SE_RANGE("dct_recover");
     se_dct_layout lay;
     int rc = dct_layout(g, &lay);
     if (rc) return rc;
@@ -117,6 +119,7 @@ int dct_recover(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
 }
 
 int dct_select(const se_dct_geom* g, const void* d_in, float* d_coef, void* stream) {
+    SE_RANGE("dct_select");
     int rc = check_dct(g, false);
     if (rc) return rc;
     if (!d_in || !d_coef) return SE_EINVAL;
@@ -142,6 +145,7 @@ static int dct8_common(const se_dct_geom* g, se_dct_layout& lay) {
 }
 
 int dct8_forward(const se_dct_geom* g, const void* d_in, float* d_coef, void* stream) {
+    SE_RANGE("dct8_forward");
     se_dct_layout lay;
     int rc = dct8_common(g, lay);
     if (rc) return rc;
@@ -154,6 +158,7 @@ int dct8_forward(const se_dct_geom* g, const void* d_in, float* d_coef, void* st
 }
 
 int dct8_inverse(const se_dct_geom* g, const float* d_coef, void* d_out, void* stream) {
+    SE_RANGE("dct8_inverse");
     se_dct_layout lay;
     int rc = dct8_common(g, lay);
     if (rc) return rc;

@@ -554,12 +554,14 @@ extern "C" {
 
 int fragment_protect_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_in,
                           void* h_a, void* h_b, void* h_c, uint64_t chunk_bytes, uint32_t n_streams) {
+    SE_RANGE("fragment_protect_host");
     return protect_host_impl(g, key, iv, h_in, h_a, h_b, h_c, chunk_bytes, n_streams, nullptr);
 }
 
 int fragment_protect_host_async(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_in,
                                 void* h_a, void* h_b, void* h_c, uint64_t chunk_bytes, uint32_t n_streams,
                                 se_host_ticket** out) {
+    SE_RANGE("fragment_protect_host_async");
     if (!out) return SE_EINVAL;
     *out = nullptr;
     se_host_ticket* t = new se_host_ticket();
@@ -747,12 +749,14 @@ extern "C" {
 int fragment_recover_host(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_a,
                           const void* h_b, const void* h_c, void* h_out, se_report* h_report, uint64_t chunk_bytes,
                           uint32_t n_streams) {
+    SE_RANGE("fragment_recover_host");
     return recover_host_impl(g, key, iv, h_a, h_b, h_c, h_out, h_report, chunk_bytes, n_streams, nullptr, nullptr);
 }
 
 int fragment_recover_host_async(const se_geom* g, const uint8_t key[16], const uint8_t iv[16], const void* h_a,
                                 const void* h_b, const void* h_c, void* h_out, uint64_t chunk_bytes,
                                 uint32_t n_streams, const se_host_ticket* after, se_host_ticket** out) {
+    SE_RANGE("fragment_recover_host_async");
     if (!out) return SE_EINVAL;
     *out = nullptr;
     if (after && after->op != 0) return SE_EINVAL;
@@ -770,6 +774,7 @@ int fragment_recover_host_async(const se_geom* g, const uint8_t key[16], const u
 }
 
 int se_host_wait(se_host_ticket* t, se_report* h_report) {
+    SE_RANGE("se_host_wait");
     if (!t) return SE_EINVAL;
     HostCtx* c = (HostCtx*)t->ctx;
     int st;

@@ -7,6 +7,29 @@
 #include "../../include/se.h"
 #include "../../include/se_dct.h"
 
+// NVTX ranges around every public entry point (host side: the range covers
+// argument checks and the enqueue of the call's kernels / copies), so
+// profilers show library calls on the timeline and `ncu --nvtx
+// --nvtx-include "fragment_protect/"` selects one call's kernels.  Header-only
+// NVTX3: no cost beyond a predicted branch when no tool is attached.
+#ifndef SE_NVTX
+#define SE_NVTX 1
+#endif
+#if SE_NVTX
+#include <nvtx3/nvToolsExt.h>
+namespace se {
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace se
+#define SE_RANGE(name) ::se::NvtxRange se_nvtx_range_(name)
+#else
+#define SE_RANGE(name) ((void)0)
+#endif
+
 namespace se {
 
 constexpr int kBlocksPerCta = 128;   // one thread per 8x8 block, 128 blocks per CTA
