@@ -280,8 +280,34 @@ extern "C" int se_trace_read(unsigned long long* host, int n_ctas) {
 // Launch with programmatic stream serialization: the kernel may start while
 // the preceding keystream kernel (k_cipher_ctr) still runs; it synchronises
 // with griddepcontrol.wait where it needs the keystream (fused_cta.cuh).
+// SE_CARVEOUT_MAX 1: ask for the maximum shared-memory carveout on the fused
+// kernels (and the lane-table keystream kernels, k_cipher.cu), so kernels
+// that follow each other on a stream never need an L1 / shared-memory
+// reconfiguration of the SMs between them.  Measured (tools/gpu_r2_call55.sh,
+// two passes): C2 93.0 -> 93.3, C3 110.5 -> 111.3, C4 115.61 -> 115.79 GB/s: 1.
+#ifndef SE_CARVEOUT_MAX
+#define SE_CARVEOUT_MAX 1
+#endif
+template <typename P>
+static void carveout_once(void (*kernel)(P)) {
+#if SE_CARVEOUT_MAX
+    static thread_local const void* seen[64];
+    static thread_local int n_seen = 0, seen_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != seen_dev) { n_seen = 0; seen_dev = dev; }
+    for (int i = 0; i < n_seen; ++i)
+        if (seen[i] == (const void*)kernel) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    if (n_seen < 64) seen[n_seen++] = (const void*)kernel;
+#else
+    (void)kernel;
+#endif
+}
+
 template <typename P>
 void launch_pdl(void (*kernel)(P), unsigned grid, unsigned block, cudaStream_t s, const P& p) {
+    carveout_once(kernel);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);

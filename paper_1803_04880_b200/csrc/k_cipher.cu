@@ -46,6 +46,9 @@ extern "C" int se_trace_ks_read(unsigned long long* host, int n_ctas) {
 // (tools/gpu_r2_call52.sh, two passes): AES-CTR comparator 788 -> 801 GB/s
 // (the kernel is shared-memory-wavefront bound as much as ALU bound), C4
 // masked 115.24 -> 115.36 GB/s, C5 107.53 -> 107.67 GB/s: 1.
+#ifndef SE_CARVEOUT_MAX
+#define SE_CARVEOUT_MAX 1      // as k_block8.cu: maximum shared-memory carveout
+#endif
 #ifndef SE_LUT4
 #define SE_LUT4 1
 #endif
@@ -230,6 +233,9 @@ static void allow_lut() {
     cudaGetDevice(&dev);
     if (done == dev) return;
     cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLaneLutBytes);
+#if SE_CARVEOUT_MAX
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+#endif
     done = dev;
 }
 
