@@ -212,6 +212,7 @@ __global__ void k_report_init(se_report* r, uint32_t n) {
 }
 
 int launch_report_init(se_report* r, uint32_t n, void* stream) {
+    carveout_max_once((const void*)k_report_init);
     k_report_init<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(r, n);
     note_launch();
     return (int)cudaGetLastError();
@@ -288,21 +289,25 @@ extern "C" int se_trace_read(unsigned long long* host, int n_ctas) {
 #ifndef SE_CARVEOUT_MAX
 #define SE_CARVEOUT_MAX 1
 #endif
-template <typename P>
-static void carveout_once(void (*kernel)(P)) {
+void carveout_max_once(const void* kernel) {
 #if SE_CARVEOUT_MAX
-    static thread_local const void* seen[64];
+    static thread_local const void* seen[128];
     static thread_local int n_seen = 0, seen_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev != seen_dev) { n_seen = 0; seen_dev = dev; }
     for (int i = 0; i < n_seen; ++i)
-        if (seen[i] == (const void*)kernel) return;
+        if (seen[i] == kernel) return;
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    if (n_seen < 64) seen[n_seen++] = (const void*)kernel;
+    if (n_seen < 128) seen[n_seen++] = kernel;
 #else
     (void)kernel;
 #endif
+}
+
+template <typename P>
+static void carveout_once(void (*kernel)(P)) {
+    carveout_max_once((const void*)kernel);
 }
 
 template <typename P>
@@ -368,6 +373,7 @@ int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t lev
                         void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (recover && bp.reports && !bp.reports_ready) {
+        carveout_max_once((const void*)k_report_init);
         k_report_init<<<(bp.n_jobs + 255) / 256, 256, 0, s>>>(bp.reports, bp.n_jobs);
         note_launch();
     }

@@ -305,6 +305,29 @@ __device__ __forceinline__ void fwd_rows(FwdState& st, const uint2 (&q)[8], int1
     }
 }
 
+// Shared-memory carveout of the streaming transforms (no shared memory of
+// their own): SE_FULL_CARVEOUT 0 leave the driver default, 1 maximum shared
+// (as the footprint kernels around them), 2 maximum L1.  Measured
+// (tools/gpu_r2_call57.sh, C4-FULL round trip): 0 99.0, 1 97.7 (the inverse
+// transform loses its L1: recover 197.3 -> 192.8 GB/s), 2 99.0 GB/s: 0.
+#ifndef SE_FULL_CARVEOUT
+#define SE_FULL_CARVEOUT 0
+#endif
+static void full_carveout(const void* kernel) {
+#if SE_FULL_CARVEOUT == 1
+    carveout_max_once(kernel);
+#elif SE_FULL_CARVEOUT == 2
+    static thread_local const void* seen[8];
+    static thread_local int n = 0;
+    for (int i = 0; i < n; ++i)
+        if (seen[i] == kernel) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxL1);
+    if (n < 8) seen[n++] = kernel;
+#else
+    (void)kernel;
+#endif
+}
+
 template <int L>
 __global__ void __launch_bounds__(kStreamThreads) k_dwt_full_fwd(const __grid_constant__ DwtParams p, int seg,
                                                                  int ncg, int nseg) {
@@ -649,6 +672,7 @@ static int full_fwd_l(const DwtParams& p, cudaStream_t s) {
     int seg, ncg, nseg;
     unsigned grid;
     stream_shape<L>(p, seg, ncg, nseg, grid);
+    full_carveout((const void*)k_dwt_full_fwd<L>);
     if (grid) k_dwt_full_fwd<L><<<grid, kStreamThreads, 0, s>>>(p, seg, ncg, nseg);
     return (int)cudaGetLastError();
 }
@@ -658,6 +682,7 @@ static int full_inv_l(const DwtParams& p, se_report* rep, cudaStream_t s) {
     int seg, ncg, nseg;
     unsigned grid;
     stream_shape<L>(p, seg, ncg, nseg, grid);
+    full_carveout((const void*)k_dwt_full_inv<L>);
     if (grid) k_dwt_full_inv<L><<<grid, kStreamThreads, 0, s>>>(p, rep, seg, ncg, nseg);
     return (int)cudaGetLastError();
 }

@@ -225,6 +225,8 @@ int launch_batch_block8(const BatchParams& bp, uint64_t total_ctas, uint32_t lev
                         void* stream);
 int launch_batch_keystream(const BatchParams& bp, uint32_t a_bits, void* stream);   // into each job's A'
 int launch_dwt_fwd_block8(const DwtParams& p, uint32_t levels, void* stream);
+// the maximum shared-memory carveout for a kernel, once per device (k_block8.cu, SE_CARVEOUT_MAX)
+void carveout_max_once(const void* kernel);
 int launch_report_init(se_report* r, uint32_t n, void* stream);   // {-1, 0} x n
 // FULL mode (row a11): whole-matrix transform kernels and the footprint CTA kernels
 int launch_dwt_full_fwd(const DwtParams& p, uint32_t levels, void* stream);
