@@ -31,6 +31,12 @@
 
 #include "fused_cta.cuh"
 
+// SE_TILE_LUT_BY_AES 1: only the AES warps fill the lane table, the consumers
+// start their bulk copies at once.  Measured slower (tools/gpu_r2_call58.sh:
+// C4 PUBLIC_PLAIN 852 -> 832 GB/s, C2 / C3 lower too), so 0.
+#ifndef SE_TILE_LUT_BY_AES
+#define SE_TILE_LUT_BY_AES 0
+#endif
 #ifndef SE_TILE_ORV_IMAD
 #define SE_TILE_ORV_IMAD 1      // measured: C4 PUBLIC_PLAIN recover 0.654 -> 0.638 ms (tools/gpu_r2_call38.sh)
 #endif
@@ -215,6 +221,18 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
         s_first = ~0ull;
         s_bad = 0;
     }
+#if SE_TILE_LUT_BY_AES
+    // the AES warps fill their table alone (bar 2 among them) while the
+    // consumers go straight to their first bulk copies
+    __syncthreads();                                      // barrier init visible
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (threadIdx.x >= T::NC) {                           // AES warps
+        aes_load_lut(lut, threadIdx.x - T::NC, 32 * T::NAW);   // constant tables only
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * T::NAW) : "memory");
+        aes_producer<L, MASK>(p, lut, smem + S::KS_OFF, ks_full, ks_empty);
+        return;
+    }
+#else
     aes_load_lut(lut, threadIdx.x, T::NT);               // constant tables only: before the grid dependency
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;");
@@ -222,6 +240,7 @@ __global__ void __launch_bounds__(TileCfg<L, MASK>::NT, 1) k_tile(const __grid_c
         aes_producer<L, MASK>(p, lut, smem + S::KS_OFF, ks_full, ks_empty);
         return;
     }
+#endif
 
     // ---- consumers
     asm volatile("griddepcontrol.wait;" ::: "memory");   // inputs written / buffers read by earlier work
