@@ -599,8 +599,6 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
     const uint64_t sblk0 = cta * BPC, sbr0 = sblk0 / p.bpr, sbc0 = sblk0 - sbr0 * p.bpr;
     const bool staged = MODE == 0 && sbc0 + BPC <= p.bpr && (p.width % 16) == 0 && (sbc0 % 2) == 0 &&
                         8 * sbr0 * (uint64_t)p.width + 8 * sbc0 + 7ull * p.width + 8 * BPC <= p.n_bytes;
-#else
-    constexpr bool staged = false;
 #endif
     bool bad = false;
     if (valid) {

@@ -269,10 +269,13 @@ __device__ __forceinline__ int imad(int a, int b, int c) {      // a * b + c on 
 template <int N>
 __device__ __forceinline__ void lift_fwd_mix(int (&x)[N], int m1) {
     constexpr int H = N / 2;
-    int n[H] = {}, s[H], d[H];
+    int s[H], d[H];
 #if !SE_MIX_FWD_PRED_LEAN
+    int n[H] = {};
 #pragma unroll
     for (int k = 1; k < H; ++k) n[k] = imad(x[2 * k], m1, 3);                    // 3 - x_e (n[0] unused)
+#else
+    (void)m1;
 #endif
 #pragma unroll
     for (int k = 0; k < H; ++k) {
