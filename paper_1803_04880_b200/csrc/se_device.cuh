@@ -287,7 +287,9 @@ __device__ __forceinline__ void lift_fwd_mix(int (&x)[N], int m1) {
         else d[k] = x[2 * k + 1] - x[2 * k] + 1;                                 // x(N) = x(N-2), +1
     }
 #pragma unroll
-    for (int k = 0; k < H; ++k) s[k] = x[2 * k] + (imad(k == 0 ? d[0] : d[k - 1], -m1, d[k]) >> 2);   // Eq. 5.2
+    for (int k = 0; k < H; ++k)                                                  // Eq. 5.2
+        s[k] = k == 0 ? x[0] + (d[0] >> 1)                   // d(-1) = d(0): (2 d'_0) >> 2 = d'_0 >> 1, one LEA.HI
+                      : x[2 * k] + (imad(d[k - 1], -m1, d[k]) >> 2);
 #pragma unroll
     for (int k = 0; k < H; ++k) { x[k] = s[k]; x[H + k] = d[k]; }
 }
@@ -295,12 +297,13 @@ __device__ __forceinline__ void lift_fwd_mix(int (&x)[N], int m1) {
 template <int N>
 __device__ __forceinline__ void lift_inv_mix(int (&y)[N], int m1) {
     constexpr int H = N / 2;
-    int x[N], m[H];
+    int x[N], m[H] = {};
 #pragma unroll
-    for (int k = 0; k < H; ++k) m[k] = imad(y[H + k], m1, 1);                   // 1 - d
+    for (int k = 1; k < H; ++k) m[k] = imad(y[H + k], m1, 1);                   // 1 - d (m[0] unused)
+    // k = 0 (d(-1) = d(0)): floor((1 - 2 d) / 4) = floor(-d / 2), one IMAD (-d) and one LEA.HI
+    x[0] = y[0] + (imad(y[H], m1, 0) >> 1);
 #pragma unroll
-    for (int k = 0; k < H; ++k)
-        x[2 * k] = y[k] + (imad(k == 0 ? y[H] : y[H + k - 1], m1, m[k]) >> 2);
+    for (int k = 1; k < H; ++k) x[2 * k] = y[k] + (imad(y[H + k - 1], m1, m[k]) >> 2);
 #pragma unroll
     for (int k = 0; k < H; ++k) {
         if (2 * k + 2 < N) x[2 * k + 1] = y[H + k] + (imad(x[2 * k], -m1, x[2 * k + 2]) >> 1);

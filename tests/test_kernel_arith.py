@@ -6,8 +6,8 @@ SHF / LEA.HI floors), so a wrong identity in DESIGN.md §5.3 fails here
 without a GPU; the GPU parity tests then compare the kernels themselves.
 
   lift_fwd_mix   d' = x_o + ((3 - x_l - x_r) >> 1) = d + 1,
-                 s  = x_e + ((d'_l + d'_r) >> 2)          (P:2023-2032, Eq. 5.1-5.2)
-  lift_inv_mix   x_e = s + ((1 - d_l - d_r) >> 2), x_o = d + ((x_l + x_r) >> 1)
+                 s  = x_e + ((d'_l + d'_r) >> 2) (first: x_e + (d'_0 >> 1)) (P:2023-2032, Eq. 5.1-5.2)
+  lift_inv_mix   x_e = s + ((1 - d_l - d_r) >> 2) (first: s + ((-d) >> 1)), x_o = d + ((x_l + x_r) >> 1)
   dwt8_fwd_mix   every band but the final LL leaves as v + 1
   out_of_range_pairs  (v_a + 2^16 v_b) & 0xff00ff00 != 0  <=>  v_a or v_b outside [0, 255]
                  for |v| < 2^15, and every inverse of <= 11-bit fields stays inside that
@@ -31,7 +31,7 @@ def lift_fwd_mix(x):
             d.append(x[2 * k + 1] + ((-x[2 * k] + nn[k + 1]) >> 1))
         else:
             d.append(x[2 * k + 1] - x[2 * k] + 1)
-    s = [x[2 * k] + (((d[0] if k == 0 else d[k - 1]) + d[k]) >> 2) for k in range(h)]
+    s = [x[0] + (d[0] >> 1) if k == 0 else x[2 * k] + ((d[k - 1] + d[k]) >> 2) for k in range(h)]
     return s + d
 
 
@@ -41,8 +41,9 @@ def lift_inv_mix(y):
     n_, h = len(y), len(y) // 2
     m = [1 - y[h + k] for k in range(h)]
     x = [0] * n_
-    for k in range(h):
-        x[2 * k] = y[k] + ((-(y[h] if k == 0 else y[h + k - 1]) + m[k]) >> 2)
+    x[0] = y[0] + ((-y[h]) >> 1)                   # floor((1 - 2 d) / 4) = floor(-d / 2)
+    for k in range(1, h):
+        x[2 * k] = y[k] + ((-y[h + k - 1] + m[k]) >> 2)
     for k in range(h):
         if 2 * k + 2 < n_:
             x[2 * k + 1] = y[h + k] + ((x[2 * k] + x[2 * k + 2]) >> 1)
