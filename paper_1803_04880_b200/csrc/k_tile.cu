@@ -34,6 +34,13 @@
 // SE_TILE_LUT_BY_AES 1: only the AES warps fill the lane table, the consumers
 // start their bulk copies at once.  Measured slower (tools/gpu_r2_call58.sh:
 // C4 PUBLIC_PLAIN 852 -> 832 GB/s, C2 / C3 lower too), so 0.
+// AES warps of the PUBLIC_PLAIN tile kernels.  Measured (tools/gpu_r2_call61.sh):
+// 4 -> 859 GB/s C4 round trip, 3 / 2 -> 737 / 736 (the keystream falls
+// behind: 120 AES blocks per tile need one pass of 128 lanes); the mbarrier
+// suspend hint (1000 / 4000 / 20000 ns) makes no difference.
+#ifndef SE_TILE_NAW_PLAIN
+#define SE_TILE_NAW_PLAIN 4
+#endif
 #ifndef SE_TILE_LUT_BY_AES
 #define SE_TILE_LUT_BY_AES 0
 #endif
@@ -53,7 +60,9 @@ struct TileCfg {
     using R = Rec<L>;
     static constexpr int TILE = (L == 1) ? 256 : MASK ? 512 : 384;
     static constexpr int NCW = TILE / 32;
-    static constexpr int NAW = 4;      // masked: 20 warps = 5 per SM sub-partition: 96 registers per thread
+    // AES warps.  masked: 20 warps = 5 per SM sub-partition: 96 registers per
+    // thread.  PUBLIC_PLAIN: SE_TILE_NAW_PLAIN.
+    static constexpr int NAW = MASK ? 4 : SE_TILE_NAW_PLAIN;
     static constexpr int NC = 32 * NCW;
     static constexpr int NT = 32 * (NCW + NAW);
     static constexpr int A_BYTES = TILE * R::ABITS / 8;
