@@ -266,24 +266,20 @@ __device__ __forceinline__ int imad(int a, int b, int c) {      // a * b + c on 
 #ifndef SE_MIX_FWD_PRED_LEAN
 #define SE_MIX_FWD_PRED_LEAN 1
 #endif
-template <int N>
+template <int N, bool PL = SE_MIX_FWD_PRED_LEAN != 0>
 __device__ __forceinline__ void lift_fwd_mix(int (&x)[N], int m1) {
     constexpr int H = N / 2;
     int s[H], d[H];
-#if !SE_MIX_FWD_PRED_LEAN
     int n[H] = {};
+    if constexpr (!PL) {
 #pragma unroll
-    for (int k = 1; k < H; ++k) n[k] = imad(x[2 * k], m1, 3);                    // 3 - x_e (n[0] unused)
-#else
-    (void)m1;
-#endif
+        for (int k = 1; k < H; ++k) n[k] = imad(x[2 * k], m1, 3);                // 3 - x_e (n[0] unused)
+    }
 #pragma unroll
     for (int k = 0; k < H; ++k) {
-#if SE_MIX_FWD_PRED_LEAN
-        if (2 * k + 2 < N) d[k] = x[2 * k + 1] + ((3 - x[2 * k] - x[2 * k + 2]) >> 1);   // Eq. 5.1, +1
-#else
-        if (2 * k + 2 < N) d[k] = x[2 * k + 1] + (imad(x[2 * k], m1, n[k + 1]) >> 1);   // Eq. 5.1, +1
-#endif
+        if (2 * k + 2 < N)
+            d[k] = PL ? x[2 * k + 1] + ((3 - x[2 * k] - x[2 * k + 2]) >> 1)      // Eq. 5.1, +1
+                      : x[2 * k + 1] + (imad(x[2 * k], m1, n[k + 1]) >> 1);
         else d[k] = x[2 * k + 1] - x[2 * k] + 1;                                 // x(N) = x(N-2), +1
     }
 #pragma unroll
@@ -328,7 +324,7 @@ __device__ __forceinline__ void dwt2_level_lean(int (&v)[8][8], uint32_t one) {
                 if constexpr ((MIX & 2) != 0) lift_inv_mix<M>(t, -(int)one);
                 else lift_inv_lean<M>(t, one);
             } else {
-                if constexpr ((MIX & 1) != 0) lift_fwd_mix<M>(t, -(int)one);
+                if constexpr ((MIX & 1) != 0) lift_fwd_mix<M, (MIX & 4) ? false : (SE_MIX_FWD_PRED_LEAN != 0)>(t, -(int)one);
                 else lift_fwd_lean<M>(t);
             }
 #pragma unroll
@@ -356,11 +352,19 @@ __device__ __forceinline__ void dwt8_inv_lean(int (&v)[8][8], uint32_t one) {
 
 // The mixed-pipe lifting on its own (the masked kernels, SE_MASK_MIX): the
 // forward leaves +1 on every band but LL (see lift_fwd_mix).
+// SE_MASK_PRED_IMAD 1: the masked kernels' forward predicts with IMAD sums
+// (n_e = 3 - x_e precomputed) instead of IADD3 - ~80 fewer ALU-pipe ops per
+// block, but measured equal (C4 protect 4.609 vs 4.611 ms, three passes,
+// tools/gpu_r2_call62.sh), so 0.
+#ifndef SE_MASK_PRED_IMAD
+#define SE_MASK_PRED_IMAD 0
+#endif
 template <int L>
 __device__ __forceinline__ void dwt8_fwd_mix(int (&v)[8][8], uint32_t one) {
-    dwt2_level_lean<8, false, 3>(v, one);
-    if (L >= 2) dwt2_level_lean<4, false, 3>(v, one);
-    if (L >= 3) dwt2_level_lean<2, false, 3>(v, one);
+    constexpr int MX = SE_MASK_PRED_IMAD ? 7 : 3;        // 7: the predicts' sums as IMADs too
+    dwt2_level_lean<8, false, MX>(v, one);
+    if (L >= 2) dwt2_level_lean<4, false, MX>(v, one);
+    if (L >= 3) dwt2_level_lean<2, false, MX>(v, one);
 }
 
 template <int L>
