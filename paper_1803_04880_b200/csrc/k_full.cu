@@ -67,9 +67,20 @@ struct StreamCtx {
 #ifndef SE_FULL_MIX
 #define SE_FULL_MIX 0
 #endif
+// SE_FULL_LEAN bit 0: the forward predict, bit 1: the inverse update as
+// x + ((1 - a - b) >> k), one IADD3 and one LEA.HI, instead of a sum (which
+// ptxas puts on the FMA pipe as IMAD.IADD), a shift and a subtraction.
+// Measured (tools/gpu_r2_call65.sh, C4-FULL): bit 0 protect 198.6 -> 196.7
+// GB/s (the forward transform is ALU-bound), bit 1 recover 197.4 -> 197.8: 2.
+#ifndef SE_FULL_LEAN
+#define SE_FULL_LEAN 2
+#endif
 __device__ __forceinline__ int fm_pred(int xo, int xl, int xr, const StreamCtx& c) {   // xo - floor((xl + xr) / 2)
 #if SE_FULL_MIX & 1
     return xo + (imad(xl, c.m1, imad(xr, c.m1, 1)) >> 1);
+#elif SE_FULL_LEAN & 1
+    (void)c;
+    return xo + ((1 - xl - xr) >> 1);                            // one IADD3 + one LEA.HI
 #else
     (void)c;
     return xo - ((xl + xr) >> 1);
@@ -86,6 +97,9 @@ __device__ __forceinline__ int fm_upd(int xe, int dl, int dr, const StreamCtx& c
 __device__ __forceinline__ int fm_iupd(int sv, int dl, int dr, const StreamCtx& c) {   // sv - floor((dl + dr + 2) / 4)
 #if SE_FULL_MIX & 2
     return sv + (imad(dl, c.m1, imad(dr, c.m1, 1)) >> 2);
+#elif SE_FULL_LEAN & 2
+    (void)c;
+    return sv + ((1 - dl - dr) >> 2);                            // -floor((m + 2) / 4) = floor((1 - m) / 4)
 #else
     (void)c;
     return sv - ((dl + dr + 2) >> 2);
