@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(kBlocksPerCta, SE_DCT8_MINB) k_dct8_inv(const 
 
 template <int C, int LEVEL, bool KEYED>
 void launch_c(const DctParams& p, int op, unsigned grid, cudaStream_t s) {
-    if (dct_fused_aes(op, LEVEL)) {
+    if (dct_fused_aes(op, LEVEL, p.n_pos)) {
         if (op == 0) k_dct_protect<C, LEVEL, KEYED, true><<<grid, kBlocksPerCta, 0, s>>>(p);
         else k_dct_recover<C, LEVEL, KEYED, true><<<grid, kBlocksPerCta, 0, s>>>(p);
     } else {
@@ -589,8 +589,15 @@ void launch_level(const DctParams& p, uint32_t level, bool keyed, int op, unsign
 // Measured (4800x4800): the fused AES pays off where the kernel has issue
 // slots to spare (level 1, and recovery, which also skips the keystream
 // scratch), not in the ALU-bound level-2 protect (100.4 vs 97.3 us).
-bool dct_fused_aes(int op, uint32_t level) {
-    return op == 1 || (SE_DCT_FUSED_AES && level == 1);    // recovery: always in-kernel (no scratch)
+// Level-1 protect of large images: the separate lane-table keystream kernel
+// wins there (4800x4800: 28.8 -> 27.5 us) but costs a launch on small ones
+// (1024x768: 10.6 -> 14.0 us), so from SE_DCT_KS_MIN_POS block positions on.
+#ifndef SE_DCT_KS_MIN_POS
+#define SE_DCT_KS_MIN_POS 200000
+#endif
+bool dct_fused_aes(int op, uint32_t level, uint64_t n_pos) {
+    if (op == 1) return true;                               // recovery: always in-kernel (no scratch)
+    return SE_DCT_FUSED_AES && level == 1 && n_pos < (uint64_t)SE_DCT_KS_MIN_POS;
 }
 
 int launch_dct(const DctParams& p, uint32_t channels, uint32_t level, bool keyed, int op, void* stream) {

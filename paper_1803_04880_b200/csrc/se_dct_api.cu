@@ -93,7 +93,7 @@ int dct_protect(const se_dct_geom* g, const uint8_t key[16], const uint8_t iv[16
         dct_sched_consts(p, (g->flags & SE_DCT_KEYED) != 0);
     }
     aes_params(p, key, iv, g);
-    if (!dct_fused_aes(0, g->level) && launch_ks(key, iv, g, p.a, lay.a_bytes, stream)) return SE_ECUDA;
+    if (!dct_fused_aes(0, g->level, p.n_pos) && launch_ks(key, iv, g, p.a, lay.a_bytes, stream)) return SE_ECUDA;
     return launch_dct(p, g->channels, g->level, (g->flags & SE_DCT_KEYED) != 0, 0, stream) ? SE_ECUDA : SE_OK;
 }
 

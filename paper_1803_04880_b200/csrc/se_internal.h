@@ -193,7 +193,7 @@ struct DctParams {
 };
 // whether the DCT kernel of `op` (0 protect, 1 recover) runs the AES of
 // Fragment 1 itself (k_dct.cu) instead of a keystream kernel before it
-bool dct_fused_aes(int op, uint32_t level);
+bool dct_fused_aes(int op, uint32_t level, uint64_t n_pos);
 // message words of the level-2 hash that depend on the record: unkeyed rec9
 // (words 0, 1), keyed K||IV||be64(r)||rec9 (words 4, 5, 6)
 constexpr uint32_t kDctMsgUnkeyed = 0x3u;
