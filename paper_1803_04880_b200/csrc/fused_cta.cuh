@@ -10,9 +10,11 @@
 // Masked per-CTA kernels: mixed-pipe lifting (bit 0 forward, bit 1 inverse,
 // se_device.cuh lift_*_mix) and the paired range check (bit 2).  Measured
 // (C4, tools/gpu_r2_call40.sh): forward protect 4.684 -> 4.665 ms, inverse
-// recover 4.668 -> 4.653 ms, paired check recover 4.668 -> 4.714 ms: 3.
+// recover 4.668 -> 4.653 ms, paired check recover 4.668 -> 4.714 ms then;
+// re-measured on the final build (three passes): paired check recover 4.643
+// -> 4.595 ms: 7.
 #ifndef SE_MASK_MIX
-#define SE_MASK_MIX 3
+#define SE_MASK_MIX 7
 #endif
 #include "sha2_spec.cuh"
 
