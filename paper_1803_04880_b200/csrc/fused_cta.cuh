@@ -197,6 +197,18 @@ __device__ __forceinline__ void xor_g2s(uint32_t* s, const uint8_t* __restrict__
 }
 
 // SHA-256 mask of B from the plain A record (framing C15: K||IV||be64(b)||A).
+// SE_SHA256_BODY_P: the SHA-256 loop body of the single-file protect kernels
+// (16: measured on C4, two passes, protect 4.610 -> 4.595 ms; in the batch
+// kernels the 16-round body was slower, C5 108.3 -> 107.2 GB/s).
+#ifndef SE_SHA256_BODY_P
+#define SE_SHA256_BODY_P 16
+#endif
+// SE_SPEC_REC256 1: the single-file recover kernels specialise the SHA-256
+// schedule too (measured on C4, two passes: recover 4.585 -> 4.567 ms, while
+// protect is faster with the generic 16-round body: 4.612 vs 4.595 ms).
+#ifndef SE_SPEC_REC256
+#define SE_SPEC_REC256 1
+#endif
 #ifndef SE_SPEC
 #define SE_SPEC 2      // bit 0: SHA-256 (B mask), bit 1: SHA-512 (C mask) schedules specialised
                        // (2: the SHA-256 one costs more in instruction fetch than it saves)
@@ -204,7 +216,7 @@ __device__ __forceinline__ void xor_g2s(uint32_t* s, const uint8_t* __restrict__
 // SPEC: the message schedule specialised with the launch's host-computed
 // constants (p.s256 / p.s512, sha2_spec.cuh); batches (per-file IV) use the
 // generic schedule.
-template <int L, int MODE, bool SPEC = true>
+template <int L, int MODE, bool SPEC = true, bool SPEC256 = (SE_SPEC & 1) != 0, int BODY = SE_SHA_BODY>
 __device__ __forceinline__ void mask_b(const FusedParams& p, uint64_t gb, const uint32_t (&A)[Rec<L, MODE>::AW],
                                        uint32_t (&B)[Rec<L, MODE>::BW]) {
     using R = Rec<L, MODE>;
@@ -225,8 +237,8 @@ __device__ __forceinline__ void mask_b(const FusedParams& p, uint64_t gb, const 
     const uint32_t h0[8] = {p.h256[0], p.h256[1], p.h256[2], p.h256[3],
                             p.h256[4], p.h256[5], p.h256[6], p.h256[7]};
     uint32_t H[8];
-    if constexpr (SPEC && (SE_SPEC & 1)) sha256_from_round8_spec<msg_var256(R::ABYTES)>(st, h0, W, p.s256, H, p.one);
-    else sha256_from_round8(st, h0, W, H, p.one);
+    if constexpr (SPEC && SPEC256) sha256_from_round8_spec<msg_var256(R::ABYTES)>(st, h0, W, p.s256, H, p.one);
+    else sha256_from_round8<BODY>(st, h0, W, H, p.one);
 #pragma unroll
     for (int k = 0; k < R::BW; ++k) {
         const uint32_t m = (k == R::BW - 1) ? (H[k] & head_mask(R::BBITS % 32)) : H[k];
@@ -416,7 +428,7 @@ __device__ __forceinline__ void footprint_full(const FusedParams& p, uint64_t br
 // the lifting and hashing and the fused kernel carries no AES tables.
 // BPC = blocks (threads) per CTA: 128 everywhere but the single-file BLOCK8
 // kernels at L = 1, 2, where 32 or 64 give finer work units (k_block8.cu).
-template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta, bool SPEC = true>
+template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta, bool SPEC = true, int B256 = SE_SHA_BODY>
 __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
     static_assert((BPC * R::ABITS) % 128 == 0 && (BPC * R::BBITS) % 128 == 0 && (BPC * R::CBITS) % 128 == 0,
@@ -472,7 +484,7 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
         if (MASK) {
             const uint64_t gb = p.block_offset + blk;
             if (R::BBITS) {
-                mask_b<L, MODE, SPEC>(p, gb, A, B);                         // row a7
+                mask_b<L, MODE, SPEC, (SE_SPEC & 1) != 0, B256>(p, gb, A, B);   // row a7
                 mask_c<R::BW, R::BBYTES, SPEC>(p, gb, B, C);                // row a8
             } else {
                 mask_c<R::AW, R::ABYTES, SPEC>(p, gb, A, C);                // C21 (L = 1)
@@ -523,7 +535,10 @@ __device__ __forceinline__ void protect_cta(const FusedParams& p, const uint64_t
 #ifndef SE_REC_STAGE
 #define SE_REC_STAGE 0
 #endif
-template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta, bool SPEC = true>
+// S256: the single-file recovery kernels (whose FusedParams carry the
+// launch's SHA-256 schedule constants p.s256) also specialise the B-mask
+// schedule (SE_SPEC_REC256; batches have no per-file s256).
+template <int L, bool MASK, int MODE = 0, int BPC = kBlocksPerCta, bool SPEC = true, bool S256 = false>
 __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t cta) {
     using R = Rec<L, MODE>;
     static_assert((BPC * R::ABITS) % 128 == 0 && (BPC * R::BBITS) % 128 == 0 && (BPC * R::CBITS) % 128 == 0,
@@ -606,7 +621,7 @@ __device__ __forceinline__ void recover_cta(const FusedParams& p, const uint64_t
     if (valid) {
         smem_get_record<R::AW, R::ABITS>(sa, SA_W, (uint32_t)tid * R::ABITS, A);
         if (MASK) {
-            if (R::BBITS) mask_b<L, MODE, SPEC>(p, gb, A, B);                // B from A
+            if (R::BBITS) mask_b<L, MODE, SPEC, S256 || (SE_SPEC & 1) != 0>(p, gb, A, B);   // B from A
             else mask_c<R::AW, R::ABYTES, SPEC>(p, gb, A, C);                // C21 (L = 1)
         }
         int v[8][8];

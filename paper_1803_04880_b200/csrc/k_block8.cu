@@ -87,14 +87,14 @@ template <int L, bool MASK>
 __global__ void __launch_bounds__(bpc_for<L>(), MASK ? SE_MINB_MASK(bpc_for<L>()) : SE_MIN_CTAS_PLAIN_P * kBlocksPerCta / bpc_for<L>())
 k_protect_block8(const __grid_constant__ FusedParams p) {
     SE_CTA_TRACE
-    protect_cta<L, MASK, 0, bpc_for<L>()>(p, blockIdx.x);
+    protect_cta<L, MASK, 0, bpc_for<L>(), true, SE_SHA256_BODY_P>(p, blockIdx.x);
 }
 
 template <int L, bool MASK>
 __global__ void __launch_bounds__(bpc_for<L>(), MASK ? SE_MINB_MASK(bpc_for<L>()) : SE_MIN_CTAS_PLAIN_R * kBlocksPerCta / bpc_for<L>())
 k_recover_block8(const __grid_constant__ FusedParams p) {
     SE_CTA_TRACE
-    recover_cta<L, MASK, 0, bpc_for<L>()>(p, blockIdx.x);
+    recover_cta<L, MASK, 0, bpc_for<L>(), true, SE_SPEC_REC256 != 0>(p, blockIdx.x);
 }
 
 // Many independent files in one launch (C5; SURVEY §8.6 "sharded by file").

@@ -267,6 +267,9 @@ __device__ __forceinline__ void sha256_sched_rounds(uint32_t (&S)[8], uint32_t (
     }
 }
 
+// Loop body of the generic schedules: 8 rounds with a sliding 16-word window
+// (half the code) or 16 rounds with rotating indices (no window moves).  The
+// single-file protect kernels take 16 for their SHA-256 (SE_SHA256_BODY_P).
 #ifndef SE_SHA_BODY
 #define SE_SHA_BODY 8
 #endif
@@ -292,6 +295,7 @@ __device__ __forceinline__ void sha256_sched8_rounds(uint32_t (&S)[8], uint32_t 
 
 // SHA-256 of one block whose words W[0..7] were consumed by the host
 // midstate `st` (state after round 7); h0 = H(0).  Digest -> H.
+template <int BODY = SE_SHA_BODY>
 __device__ __forceinline__ void sha256_from_round8(const uint32_t (&st)[8], const uint32_t (&h0)[8],
                                                    uint32_t (&W)[16], uint32_t (&H)[8], uint32_t one) {
     // S[(i - 8) & 7] = S[i] holds variable i at round 8
@@ -305,18 +309,18 @@ __device__ __forceinline__ void sha256_from_round8(const uint32_t (&st)[8], cons
     sha256_round<13>(S, fadd(W[13], c_sha256_k[13], one), one);
     sha256_round<14>(S, fadd(W[14], c_sha256_k[14], one), one);
     sha256_round<15>(S, fadd(W[15], c_sha256_k[15], one), one);
-#if SE_SHA_BODY == 8
+    if constexpr (BODY == 8) {
 #pragma unroll 1
-    for (int r = 16; r < 64; r += 8) {
-        uint32_t N[8];
-        sha256_sched8_rounds<0>(S, W, N, c_sha256_k + r, one);
+        for (int r = 16; r < 64; r += 8) {
+            uint32_t N[8];
+            sha256_sched8_rounds<0>(S, W, N, c_sha256_k + r, one);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { W[i] = W[8 + i]; W[8 + i] = N[i]; }
-    }
-#else
+            for (int i = 0; i < 8; ++i) { W[i] = W[8 + i]; W[8 + i] = N[i]; }
+        }
+    } else {
 #pragma unroll 1
-    for (int r = 16; r < 64; r += 16) sha256_sched_rounds<0>(S, W, c_sha256_k + r, one);
-#endif
+        for (int r = 16; r < 64; r += 16) sha256_sched_rounds<0>(S, W, c_sha256_k + r, one);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) H[i] = fadd(h0[i], S[i], one);   // 64 rounds: roles back in place
 }
@@ -368,10 +372,6 @@ __device__ __forceinline__ void sha512_msg_rounds(W64 (&S)[8], W64 (&W)[16], uin
         sha512_msg_rounds<T + 1>(S, W, one);
     }
 }
-
-#ifndef SE_SHA_BODY
-#define SE_SHA_BODY 8
-#endif
 
 // 8-round loop body: W holds w(t-16..t-1), N receives w(t..t+7); at the end
 // the window slides by 8 (16 register moves on the FMA pipe per 8 rounds).
